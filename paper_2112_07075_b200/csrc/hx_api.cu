@@ -1,0 +1,1045 @@
+// hx_api.cu -- C-ABI of libb200hydro.so (declared in include/b200hydro.h).
+//
+// Host orchestration of the sm_100a kernels in hx_kernels.cuh: context setup
+// (restriction maps, basis tables), operator handles, the device-resident
+// momentum CG and the Lagrange step driver.  Every entry point cites the
+// reference call it replaces in the header.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/b200hydro.h"
+#include "hx_kernels.cuh"
+
+using namespace hx;
+
+struct hx_ctx {
+  int dim, p, Q, D1, DT, nl, nq, nt;
+  long long ne, nn;
+  int device;
+  cudaStream_t stream = 0;
+  std::string err;
+  long long launches = 0;
+  // tables
+  double *B = nullptr, *G = nullptr, *Bt = nullptr, *wnd = nullptr, *psi1 = nullptr;
+  // restriction
+  int *emap = nullptr, *off = nullptr, *idx = nullptr;
+  uint8_t* own = nullptr;
+  // workspaces
+  double* evec = nullptr;     // (NE, nl, d)
+  double* evec2 = nullptr;    // second E buffer (API scatter staging)
+  double *r = nullptr, *z = nullptr, *p0 = nullptr, *p1 = nullptr;
+  double* partials = nullptr; // reduction partials
+  double* hist = nullptr;     // CG residual history
+  int hist_len = 0;
+  CGDev* cg = nullptr;
+  StatusDev* st = nullptr;    // [4]: S, mid, new, scratch
+  double* dt = nullptr;       // [2]
+  double* scal = nullptr;     // small scalars
+  // phase data
+  bool phase = false;
+  double* Dm = nullptr;       // (NE, nq)
+  double* qd0 = nullptr;      // (NE, nq)
+  double* minv = nullptr;     // (NE, nt, nt)
+  double* mdiag = nullptr;    // (NN)
+  double* invd = nullptr;     // (NN, d)
+  uint8_t* mask = nullptr;    // (NN, d) phase mask
+  bool has_mask = false;
+  // stage buffers for the step driver
+  double *xm = nullptr, *vm = nullptr, *em = nullptr;
+  double *dv0 = nullptr, *dv1 = nullptr, *de0 = nullptr, *de1 = nullptr;
+  // host mirrors
+  CGDev* h_cg = nullptr;
+  StatusDev* h_st = nullptr;
+  double* h_dt = nullptr;
+  // host-buffer entry scratch (device state)
+  double *hx_x = nullptr, *hx_v = nullptr, *hx_e = nullptr, *hx_xo = nullptr, *hx_vo = nullptr, *hx_eo = nullptr;
+};
+
+struct hx_mass {
+  hx_ctx* ctx;
+  double* D;  // (NE, nq)
+};
+
+struct hx_force {
+  hx_ctx* ctx;
+  double* DF;  // (NE, d*d, nq)
+};
+
+// ---------------------------------------------------------------------------
+// helpers
+
+static int fail(hx_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t _e = (call);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(ctx, HX_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+#define CKL()                                                                            \
+  do {                                                                                   \
+    ++ctx->launches;                                                                     \
+    cudaError_t _e = cudaGetLastError();                                                 \
+    if (_e != cudaSuccess)                                                               \
+      return fail(ctx, HX_ECUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(_e), \
+                  __FILE__, __LINE__);                                                   \
+  } while (0)
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t n) {
+  return cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T));
+}
+
+static inline unsigned gblocks(long long n, int nt) { return (unsigned)((n + nt - 1) / nt); }
+
+static Tables tables(const hx_ctx* c) { return Tables{c->B, c->G, c->Bt, c->wnd, c->psi1}; }
+
+template <typename K>
+static cudaError_t smem_attr(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  return cudaSuccess;
+}
+
+// run a functor templated on <DIM, P> for the context's discretisation
+template <template <int, int> class F, typename... Args>
+static int dispatch(hx_ctx* ctx, Args&&... args) {
+  switch (ctx->dim * 10 + ctx->p) {
+    case 21: return F<2, 1>::run(ctx, args...);
+    case 22: return F<2, 2>::run(ctx, args...);
+    case 23: return F<2, 3>::run(ctx, args...);
+    case 24: return F<2, 4>::run(ctx, args...);
+    case 31: return F<3, 1>::run(ctx, args...);
+    case 32: return F<3, 2>::run(ctx, args...);
+    case 33: return F<3, 3>::run(ctx, args...);
+    case 34: return F<3, 4>::run(ctx, args...);
+  }
+  return fail(ctx, HX_EINVAL, "unsupported discretisation dim=%d p=%d", ctx->dim, ctx->p);
+}
+
+static constexpr int RATES_NT = 128;
+
+// ---------------------------------------------------------------------------
+// launchers
+
+template <int DIM, int P>
+struct LaunchRates {
+  static int run(hx_ctx* ctx, const double* x, const double* v, const double* e, double* evec, double* de,
+                 StatusDev* st, int mode, double gamma, double q1, double q2) {
+    using SM = RatesSmem<DIM, P>;
+    auto kern = k_rates<DIM, P, RATES_NT>;
+    static bool attr = false;
+    if (!attr) {
+      CK(smem_attr(kern, SM::bytes));
+      attr = true;
+    }
+    RatesArgs a{x, v, e, ctx->qd0, ctx->emap, ctx->minv, tables(ctx), gamma, q1, q2, ctx->ne, evec, de, st, mode};
+    kern<<<(unsigned)ctx->ne, RATES_NT, SM::bytes, ctx->stream>>>(a);
+    CKL();
+    return HX_OK;
+  }
+};
+
+template <int DIM, int P>
+struct LaunchMass {
+  static int run(hx_ctx* ctx, int nc, bool cgmode, const MassArgs& a) {
+    using D = Disc<DIM, P>;
+    const unsigned grid = gblocks(ctx->ne, 4);
+    const size_t bytes = sizeof(double) * (D::Q * D::D1 + 4 * 2 * nc * D::NQ);
+#define HX_MASS_CASE(NC)                                                              \
+  if (nc == NC) {                                                                     \
+    if (cgmode) {                                                                     \
+      auto k = k_mass<DIM, P, NC, true>;                                              \
+      CK(smem_attr(k, bytes));                                                        \
+      k<<<grid, 128, bytes, ctx->stream>>>(a);                                        \
+    } else {                                                                          \
+      auto k = k_mass<DIM, P, NC, false>;                                             \
+      CK(smem_attr(k, bytes));                                                        \
+      k<<<grid, 128, bytes, ctx->stream>>>(a);                                        \
+    }                                                                                 \
+    CKL();                                                                            \
+    return HX_OK;                                                                     \
+  }
+    HX_MASS_CASE(1)
+    HX_MASS_CASE(2)
+    HX_MASS_CASE(3)
+#undef HX_MASS_CASE
+    return fail(ctx, HX_EINVAL, "ncomp must be 1..3");
+  }
+};
+
+template <int DIM, int P>
+struct LaunchMassDiag {
+  static int run(hx_ctx* ctx, const double* D, double* evec) {
+    k_mass_diag<DIM, P><<<gblocks(ctx->ne, 4), 128, 0, ctx->stream>>>(D, ctx->B, ctx->ne, evec);
+    CKL();
+    return HX_OK;
+  }
+};
+
+template <int DIM, int P>
+struct LaunchGeom {
+  static int run(hx_ctx* ctx, const GeomArgs& a) {
+    using SM = GeomSmem<DIM, P>;
+    auto k = k_geom<DIM, P, 128>;
+    CK(smem_attr(k, SM::bytes));
+    k<<<(unsigned)ctx->ne, 128, SM::bytes, ctx->stream>>>(a);
+    CKL();
+    return HX_OK;
+  }
+};
+
+template <int DIM, int P>
+struct LaunchStress {
+  static int run(hx_ctx* ctx, const StressArgs& a) {
+    using SM = RatesSmem<DIM, P>;
+    auto k = k_stress<DIM, P, 128>;
+    CK(smem_attr(k, SM::bytes));
+    k<<<(unsigned)ctx->ne, 128, SM::bytes, ctx->stream>>>(a);
+    CKL();
+    return HX_OK;
+  }
+};
+
+template <int DIM, int P>
+struct LaunchForce {
+  static int run(hx_ctx* ctx, const ForceArgs& a, bool trans) {
+    using SM = ForceSmem<DIM, P>;
+    if (trans) {
+      auto k = k_force<DIM, P, 128, true>;
+      CK(smem_attr(k, SM::bytes));
+      k<<<(unsigned)ctx->ne, 128, SM::bytes, ctx->stream>>>(a);
+    } else {
+      auto k = k_force<DIM, P, 128, false>;
+      CK(smem_attr(k, SM::bytes));
+      k<<<(unsigned)ctx->ne, 128, SM::bytes, ctx->stream>>>(a);
+    }
+    CKL();
+    return HX_OK;
+  }
+};
+
+template <int DIM, int P>
+struct LaunchMinv {
+  static int run(hx_ctx* ctx, double* minv_ref) {
+    using D = Disc<DIM, P>;
+    const size_t bytes = sizeof(double) * (D::NT * 2 * D::NT + D::NQ * D::NT);
+    auto k = k_minv<DIM, P>;
+    CK(smem_attr(k, bytes));
+    k<<<(unsigned)ctx->ne, 128, bytes, ctx->stream>>>(ctx->Dm, ctx->Bt, ctx->ne, ctx->minv, minv_ref);
+    CKL();
+    return HX_OK;
+  }
+};
+
+template <int DIM, int P>
+struct LaunchIE {
+  static int run(hx_ctx* ctx, const double* e, const double* qd0, double* per_elem) {
+    k_internal_energy<DIM, P><<<gblocks(ctx->ne, 4), 128, 0, ctx->stream>>>(e, qd0, ctx->Bt, ctx->wnd, ctx->ne,
+                                                                            per_elem);
+    CKL();
+    return HX_OK;
+  }
+};
+
+// scatter (internal E layout) with 1..3 comps
+static int launch_scatter(hx_ctx* ctx, const double* evec, int nc, double* out) {
+  NodeArgs a{};
+  a.off = ctx->off;
+  a.idx = ctx->idx;
+  a.evec = evec;
+  a.out = out;
+  a.nn = ctx->nn;
+  const unsigned g = gblocks(ctx->nn, 256);
+  if (nc == 1) k_scatter<1><<<g, 256, 0, ctx->stream>>>(a);
+  else if (nc == 2) k_scatter<2><<<g, 256, 0, ctx->stream>>>(a);
+  else k_scatter<3><<<g, 256, 0, ctx->stream>>>(a);
+  CKL();
+  return HX_OK;
+}
+
+static int status_reset(hx_ctx* ctx, StatusDev* st) {
+  StatusDev h;
+  h.inv_key = ~0ull;
+  h.clamps = 0;
+  h.min_ratio = __builtin_inf();
+  h.pad = 0;
+  CK(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, ctx->stream));
+  return HX_OK;
+}
+
+// host-side pinned staging for StatusDev resets (cudaMemcpyAsync from stack memory
+// is synchronous for pageable memory, which is fine for correctness)
+
+static void decode_inv(const hx_ctx* ctx, unsigned long long key, hx_inverted* inv) {
+  if (!inv) return;
+  if (key == ~0ull) {
+    inv->inverted = 0;
+    return;
+  }
+  inv->inverted = 1;
+  inv->point = (int64_t)(key / (unsigned long long)ctx->ne);
+  inv->element = (int64_t)(key % (unsigned long long)ctx->ne);
+  inv->detj = NAN;
+}
+
+// ---------------------------------------------------------------------------
+// context
+
+extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
+  hx_ctx* ctx = nullptr;
+  if (!d || !out) return HX_EINVAL;
+  *out = nullptr;
+  if (d->dim != 2 && d->dim != 3) return HX_EINVAL;
+  if (d->order < 1 || d->order > 4) return HX_EINVAL;
+  if (d->q1d != d->order + 2) return HX_EINVAL;
+  if (d->thermo_order != std::max(d->order - 1, 0)) return HX_EINVAL;
+  if (d->num_elements < 1 || d->num_nodes < 1) return HX_EINVAL;
+  ctx = new hx_ctx();
+  ctx->dim = d->dim;
+  ctx->p = d->order;
+  ctx->D1 = d->order + 1;
+  ctx->Q = d->q1d;
+  ctx->DT = std::max(d->order, 1);
+  ctx->nl = (int)std::pow(ctx->D1, ctx->dim);
+  ctx->nq = (int)std::pow(ctx->Q, ctx->dim);
+  ctx->nt = (int)std::pow(ctx->DT, ctx->dim);
+  ctx->ne = d->num_elements;
+  ctx->nn = d->num_nodes;
+  ctx->device = d->device;
+  if ((long long)ctx->ne * ctx->nl >= (1ll << 31)) {
+    int rc = fail(ctx, HX_EINVAL, "mesh too large for 32-bit E-vector indices");
+    delete ctx;
+    return rc;
+  }
+  cudaError_t ce = cudaSetDevice(d->device);
+  if (ce != cudaSuccess) {
+    delete ctx;
+    return HX_ECUDA;
+  }
+  const int nl = ctx->nl, nq = ctx->nq, Q = ctx->Q, D1 = ctx->D1, DT = ctx->DT;
+  const long long ne = ctx->ne, nn = ctx->nn;
+  // restriction maps
+  std::vector<int> emap((size_t)ne * nl);
+  std::vector<int> cnt(nn + 1, 0);
+  for (long long e = 0; e < ne; ++e)
+    for (int l = 0; l < nl; ++l) {
+      const long long n = d->dofmap_host[(long long)l * ne + e];
+      if (n < 0 || n >= nn) {
+        int rc = fail(ctx, HX_EINVAL, "dofmap entry %lld out of range", n);
+        delete ctx;
+        return rc;
+      }
+      emap[e * nl + l] = (int)n;
+      cnt[n + 1]++;
+    }
+  std::vector<int> off(nn + 1, 0);
+  for (long long n = 0; n < nn; ++n) off[n + 1] = off[n] + cnt[n + 1];
+  std::vector<int> fill(off.begin(), off.end() - 1);
+  std::vector<int> idx((size_t)ne * nl);
+  std::vector<uint8_t> own((size_t)ne * nl, 0);
+  for (long long e = 0; e < ne; ++e)  // ascending element => deterministic accumulation order
+    for (int l = 0; l < nl; ++l) {
+      const int n = emap[e * nl + l];
+      if (fill[n] == off[n]) own[e * nl + l] = 1;
+      idx[fill[n]++] = (int)(e * nl + l);
+    }
+  // tables: tensor weights (x fastest) and the thermodynamic interpolant of 1
+  std::vector<double> wnd(nq), psi1(nq);
+  for (int q = 0; q < nq; ++q) {
+    int qq = q;
+    double w = 1.0;
+    double ps = 1.0;
+    std::vector<int> dig(ctx->dim);
+    for (int a = 0; a < ctx->dim; ++a) {
+      dig[a] = qq % Q;
+      qq /= Q;
+    }
+    // weights: np.multiply.outer chain -> w[q_slowest] * ... * w[q_fastest]
+    w = d->qweights_host[dig[ctx->dim - 1]];
+    for (int a = ctx->dim - 2; a >= 0; --a) w *= d->qweights_host[dig[a]];
+    wnd[q] = w;
+    (void)ps;
+  }
+  {
+    // psi1 = tensor_interp(Bt, ones): per axis sum_j Bt[q, j]
+    std::vector<double> rowsum(Q);
+    for (int q = 0; q < Q; ++q) {
+      double s = 0.0;
+      for (int j = 0; j < DT; ++j) s += d->Bt_host[q * DT + j];
+      rowsum[q] = s;
+    }
+    for (int q = 0; q < nq; ++q) {
+      int qq = q;
+      double v = 1.0;
+      for (int a = 0; a < ctx->dim; ++a) {
+        v *= rowsum[qq % Q];
+        qq /= Q;
+      }
+      psi1[q] = v;
+    }
+  }
+  const int dd = ctx->dim;
+  const size_t nv = (size_t)nn * dd;
+  bool ok = true;
+  ok &= dalloc(&ctx->B, Q * D1) == cudaSuccess;
+  ok &= dalloc(&ctx->G, Q * D1) == cudaSuccess;
+  ok &= dalloc(&ctx->Bt, Q * DT) == cudaSuccess;
+  ok &= dalloc(&ctx->wnd, nq) == cudaSuccess;
+  ok &= dalloc(&ctx->psi1, nq) == cudaSuccess;
+  ok &= dalloc(&ctx->emap, (size_t)ne * nl) == cudaSuccess;
+  ok &= dalloc(&ctx->off, nn + 1) == cudaSuccess;
+  ok &= dalloc(&ctx->idx, (size_t)ne * nl) == cudaSuccess;
+  ok &= dalloc(&ctx->own, (size_t)ne * nl) == cudaSuccess;
+  ok &= dalloc(&ctx->evec, (size_t)ne * nl * dd) == cudaSuccess;
+  ok &= dalloc(&ctx->evec2, (size_t)ne * std::max(nl * dd, nq)) == cudaSuccess;
+  ok &= dalloc(&ctx->r, nv) == cudaSuccess;
+  ok &= dalloc(&ctx->z, nv) == cudaSuccess;
+  ok &= dalloc(&ctx->p0, nv) == cudaSuccess;
+  ok &= dalloc(&ctx->p1, nv) == cudaSuccess;
+  ok &= dalloc(&ctx->partials, 2 * (size_t)std::max<long long>(gblocks(nn, 256), gblocks(ne, 4)) + 64) == cudaSuccess;
+  ok &= dalloc(&ctx->cg, 1) == cudaSuccess;
+  ok &= dalloc(&ctx->st, 4) == cudaSuccess;
+  ok &= dalloc(&ctx->dt, 2) == cudaSuccess;
+  ok &= dalloc(&ctx->scal, 16) == cudaSuccess;
+  ok &= dalloc(&ctx->Dm, (size_t)ne * nq) == cudaSuccess;
+  ok &= dalloc(&ctx->qd0, (size_t)ne * nq) == cudaSuccess;
+  ok &= dalloc(&ctx->minv, (size_t)ne * ctx->nt * ctx->nt) == cudaSuccess;
+  ok &= dalloc(&ctx->mdiag, nn) == cudaSuccess;
+  ok &= dalloc(&ctx->invd, nv) == cudaSuccess;
+  ok &= dalloc(&ctx->mask, nv) == cudaSuccess;
+  ok &= dalloc(&ctx->xm, nv) == cudaSuccess;
+  ok &= dalloc(&ctx->vm, nv) == cudaSuccess;
+  ok &= dalloc(&ctx->em, (size_t)ne * ctx->nt) == cudaSuccess;
+  ok &= dalloc(&ctx->dv0, nv) == cudaSuccess;
+  ok &= dalloc(&ctx->dv1, nv) == cudaSuccess;
+  ok &= dalloc(&ctx->de0, (size_t)ne * ctx->nt) == cudaSuccess;
+  ok &= dalloc(&ctx->de1, (size_t)ne * ctx->nt) == cudaSuccess;
+  ok &= cudaMallocHost((void**)&ctx->h_cg, sizeof(CGDev)) == cudaSuccess;
+  ok &= cudaMallocHost((void**)&ctx->h_st, 4 * sizeof(StatusDev)) == cudaSuccess;
+  ok &= cudaMallocHost((void**)&ctx->h_dt, 2 * sizeof(double)) == cudaSuccess;
+  if (!ok) {
+    int rc = fail(ctx, HX_ECUDA, "device allocation failed");
+    hx_destroy(ctx);
+    return rc;
+  }
+  ok &= cudaMemcpy(ctx->B, d->B_host, sizeof(double) * Q * D1, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(ctx->G, d->G_host, sizeof(double) * Q * D1, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(ctx->Bt, d->Bt_host, sizeof(double) * Q * DT, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(ctx->wnd, wnd.data(), sizeof(double) * nq, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(ctx->psi1, psi1.data(), sizeof(double) * nq, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(ctx->emap, emap.data(), sizeof(int) * emap.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(ctx->off, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(ctx->idx, idx.data(), sizeof(int) * idx.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(ctx->own, own.data(), own.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemset(ctx->cg, 0, sizeof(CGDev)) == cudaSuccess;
+  ok &= cudaMemset(ctx->mask, 0, nv) == cudaSuccess;
+  if (!ok) {
+    int rc = fail(ctx, HX_ECUDA, "device upload failed");
+    hx_destroy(ctx);
+    return rc;
+  }
+  *out = ctx;
+  return HX_OK;
+}
+
+extern "C" int hx_destroy(hx_ctx* ctx) {
+  if (!ctx) return HX_OK;
+  cudaSetDevice(ctx->device);
+  void* dev[] = {ctx->B,  ctx->G,    ctx->Bt,   ctx->wnd,  ctx->psi1, ctx->emap, ctx->off,   ctx->idx,
+                 ctx->own, ctx->evec, ctx->evec2, ctx->r,   ctx->z,    ctx->p0,   ctx->p1,    ctx->partials,
+                 ctx->hist, ctx->cg,  ctx->st,   ctx->dt,   ctx->scal, ctx->Dm,   ctx->qd0,   ctx->minv,
+                 ctx->mdiag, ctx->invd, ctx->mask, ctx->xm, ctx->vm,   ctx->em,   ctx->dv0,   ctx->dv1,
+                 ctx->de0, ctx->de1, ctx->hx_x, ctx->hx_v, ctx->hx_e, ctx->hx_xo, ctx->hx_vo, ctx->hx_eo};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  if (ctx->h_cg) cudaFreeHost(ctx->h_cg);
+  if (ctx->h_st) cudaFreeHost(ctx->h_st);
+  if (ctx->h_dt) cudaFreeHost(ctx->h_dt);
+  delete ctx;
+  return HX_OK;
+}
+
+extern "C" int hx_set_stream(hx_ctx* ctx, void* stream) {
+  if (!ctx) return HX_EINVAL;
+  ctx->stream = (cudaStream_t)stream;
+  return HX_OK;
+}
+
+extern "C" const char* hx_last_error(hx_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+extern "C" int64_t hx_kernel_launches(hx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ---------------------------------------------------------------------------
+// restriction
+
+extern "C" int hx_gather(hx_ctx* ctx, int space, const double* L, int ncomp, double* E) {
+  if (!ctx || !L || !E || ncomp < 1) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  if (space == HX_SPACE_H1) {
+    const long long tot = (long long)ctx->nl * ctx->ne * ncomp;
+    k_gather_ref<<<gblocks(tot, 256), 256, 0, ctx->stream>>>(L, ctx->emap, ctx->nl, ctx->ne, ncomp, E);
+  } else {
+    const long long tot = (long long)ctx->nt * ctx->ne * ncomp;
+    k_l2_gather<<<gblocks(tot, 256), 256, 0, ctx->stream>>>(L, ctx->nt, ctx->ne, ncomp, E, 0);
+  }
+  CKL();
+  return HX_OK;
+}
+
+extern "C" int hx_scatter_add(hx_ctx* ctx, int space, const double* E, int ncomp, double* L) {
+  if (!ctx || !L || !E || ncomp < 1) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  if (space == HX_SPACE_H1) {
+    k_scatter_ref<<<gblocks(ctx->nn * ncomp, 256), 256, 0, ctx->stream>>>(E, ctx->off, ctx->idx, ctx->nl, ctx->ne,
+                                                                         ctx->nn, ncomp, L);
+  } else {
+    const long long tot = (long long)ctx->nt * ctx->ne * ncomp;
+    k_l2_gather<<<gblocks(tot, 256), 256, 0, ctx->stream>>>(E, ctx->nt, ctx->ne, ncomp, L, 1);
+  }
+  CKL();
+  return HX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// geometry
+
+static int read_status(hx_ctx* ctx, StatusDev* st, StatusDev* h) {
+  CK(cudaMemcpyAsync(h, st, sizeof(StatusDev), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return HX_OK;
+}
+
+extern "C" int hx_geometry(hx_ctx* ctx, const double* x, double* jac, double* detj, double* jinv, double* wdetj,
+                           hx_inverted* inv) {
+  if (!ctx || !x) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  StatusDev* st = ctx->st + 3;
+  int rc = status_reset(ctx, st);
+  if (rc) return rc;
+  GeomArgs a{x, ctx->emap, tables(ctx), ctx->ne, jac, detj, jinv, wdetj, nullptr, nullptr, nullptr, st};
+  rc = dispatch<LaunchGeom>(ctx, a);
+  if (rc) return rc;
+  rc = read_status(ctx, st, ctx->h_st + 3);
+  if (rc) return rc;
+  decode_inv(ctx, ctx->h_st[3].inv_key, inv);
+  if (ctx->h_st[3].inv_key != ~0ull) {
+    // fetch det J at the offending point for the message (fespace.py:39)
+    if (detj && inv) {
+      const long long pe = inv->point * ctx->ne + inv->element;
+      CK(cudaMemcpy(&inv->detj, detj + pe, sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    return HX_EINVERTED;
+  }
+  return HX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// mass
+
+__global__ void k_invdiag(const double* diag, const uint8_t* mask, int nc, long long nn, double* invd) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nn * nc) return;
+  const long long n = t / nc;
+  invd[t] = 1.0 / ((mask && mask[t]) ? 1.0 : diag[n]);
+}
+
+
+extern "C" int hx_mass_create(hx_ctx* ctx, const double* D, hx_mass** out) {
+  if (!ctx || !D || !out) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  hx_mass* m = new hx_mass{ctx, nullptr};
+  if (dalloc(&m->D, (size_t)ctx->ne * ctx->nq) != cudaSuccess) {
+    delete m;
+    return fail(ctx, HX_ECUDA, "alloc");
+  }
+  const long long n = (long long)ctx->nq * ctx->ne;
+  k_transpose<<<gblocks(n, 256), 256, 0, ctx->stream>>>(D, ctx->nq, ctx->ne, m->D);
+  CKL();
+  *out = m;
+  return HX_OK;
+}
+
+extern "C" int hx_mass_destroy(hx_mass* m) {
+  if (!m) return HX_OK;
+  cudaFree(m->D);
+  delete m;
+  return HX_OK;
+}
+
+static int mass_evec(hx_ctx* ctx, const double* D, const double* x, int nc, double* evec) {
+  MassArgs a{};
+  a.x = x;
+  a.D = D;
+  a.emap = ctx->emap;
+  a.B = ctx->B;
+  a.ne = ctx->ne;
+  a.evec = evec;
+  a.own = ctx->own;
+  return dispatch<LaunchMass>(ctx, nc, false, a);
+}
+
+extern "C" int hx_mass_apply(hx_mass* m, const double* x, int ncomp, double* y) {
+  if (!m || !x || !y || ncomp < 1 || ncomp > 3) return m ? fail(m->ctx, HX_EINVAL, "bad arguments") : HX_EINVAL;
+  hx_ctx* ctx = m->ctx;
+  CK(cudaSetDevice(ctx->device));
+  int rc = mass_evec(ctx, m->D, x, ncomp, ctx->evec2);
+  if (rc) return rc;
+  return launch_scatter(ctx, ctx->evec2, ncomp, y);
+}
+
+extern "C" int hx_mass_diagonal(hx_mass* m, double* diag) {
+  if (!m || !diag) return HX_EINVAL;
+  hx_ctx* ctx = m->ctx;
+  CK(cudaSetDevice(ctx->device));
+  int rc = dispatch<LaunchMassDiag>(ctx, (const double*)m->D, ctx->evec2);
+  if (rc) return rc;
+  return launch_scatter(ctx, ctx->evec2, 1, diag);
+}
+
+// Device CG on the PA mass: init + chunks of (mass, node) iterations.  The stop
+// test runs on device (k_cg_node's last block); the host polls a pinned copy of the
+// CG state once per chunk and launches no-op-guarded kernels past convergence.
+static int run_cg(hx_ctx* ctx, const double* D, const double* rhs, const double* evec_rhs, int negate,
+                  const uint8_t* mask, const double* invd, double rel_tol, int max_iter, double* x, int nc,
+                  double* hist, hx_cg_info* info) {
+  if (hist == nullptr) {
+    if (ctx->hist_len < max_iter + 1) {
+      if (ctx->hist) cudaFree(ctx->hist);
+      ctx->hist = nullptr;
+      CK(dalloc(&ctx->hist, (size_t)max_iter + 1));
+      ctx->hist_len = max_iter + 1;
+    }
+    hist = ctx->hist;
+  }
+  CGDev h{};
+  h.tol = rel_tol;
+  h.max_iter = max_iter;
+  CK(cudaMemcpyAsync(ctx->cg, &h, sizeof h, cudaMemcpyHostToDevice, ctx->stream));
+  NodeArgs na{};
+  na.off = ctx->off;
+  na.idx = ctx->idx;
+  na.evec = evec_rhs ? evec_rhs : ctx->evec;
+  na.mask = mask;
+  na.invd = invd;
+  na.x = x;
+  na.r = ctx->r;
+  na.z = ctx->z;
+  na.pbuf0 = ctx->p0;
+  na.pbuf1 = ctx->p1;
+  na.rhs = rhs;
+  na.nn = ctx->nn;
+  na.cg = ctx->cg;
+  na.partials = ctx->partials;
+  na.hist = hist;
+  na.negate = negate;
+  const unsigned gn = gblocks(ctx->nn, 256);
+  if (nc == 1) k_cg_init<1><<<gn, 256, 0, ctx->stream>>>(na);
+  else if (nc == 2) k_cg_init<2><<<gn, 256, 0, ctx->stream>>>(na);
+  else k_cg_init<3><<<gn, 256, 0, ctx->stream>>>(na);
+  CKL();
+  na.evec = ctx->evec;
+  na.rhs = nullptr;
+  MassArgs ma{};
+  ma.x = ctx->z;
+  ma.pbuf0 = ctx->p0;
+  ma.pbuf1 = ctx->p1;
+  ma.mask = mask;
+  ma.own = ctx->own;
+  ma.D = D;
+  ma.emap = ctx->emap;
+  ma.B = ctx->B;
+  ma.ne = ctx->ne;
+  ma.evec = ctx->evec;
+  ma.cg = ctx->cg;
+  ma.partials = ctx->partials;
+  int done_iters = 0;
+  int chunk = 8;
+  while (true) {
+    for (int i = 0; i < chunk; ++i) {
+      int rc = dispatch<LaunchMass>(ctx, nc, true, ma);
+      if (rc) return rc;
+      if (nc == 1) k_cg_node<1><<<gn, 256, 0, ctx->stream>>>(na);
+      else if (nc == 2) k_cg_node<2><<<gn, 256, 0, ctx->stream>>>(na);
+      else k_cg_node<3><<<gn, 256, 0, ctx->stream>>>(na);
+      CKL();
+    }
+    done_iters += chunk;
+    CK(cudaMemcpyAsync(ctx->h_cg, ctx->cg, sizeof(CGDev), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (!ctx->h_cg->active) break;
+    if (done_iters > max_iter + 1) break;
+    chunk = std::min(chunk * 2, 64);
+  }
+  const CGDev& g = *ctx->h_cg;
+  if (info) {
+    info->code = g.code == 0 ? HX_OK : (g.code == 3 ? HX_ECG_BREAKDOWN : HX_ECG_MAXITER);
+    info->iterations = g.iters;
+    info->n_residuals = g.nres;
+  }
+  return HX_OK;
+}
+
+__global__ void k_recip(const double* in, long long n, double* out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  out[t] = in ? 1.0 / in[t] : 1.0;
+}
+
+extern "C" int hx_mass_cg(hx_mass* m, const double* rhs, int ncomp, const uint8_t* bcmask,
+                          const double* precond_diag, double rel_tol, int max_iter, double* x,
+                          double* residuals, hx_cg_info* info) {
+  if (!m || !rhs || !x || max_iter < 0 || ncomp < 1 || ncomp > 3) return HX_EINVAL;
+  hx_ctx* ctx = m->ctx;
+  CK(cudaSetDevice(ctx->device));
+  // inv_diag = 1 / precond_diag (operators.py:344); none -> identity
+  double* invd = ctx->vm;  // scratch (NN, d) >= (NN, ncomp)
+  const long long nv = ctx->nn * ncomp;
+  k_recip<<<gblocks(nv, 256), 256, 0, ctx->stream>>>(precond_diag, nv, invd);
+  CKL();
+  hx_cg_info ci{};
+  int rc = run_cg(ctx, m->D, rhs, nullptr, 0, bcmask, invd, rel_tol, max_iter, x, ncomp, residuals, &ci);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (info) *info = ci;
+  return ci.code;
+}
+
+// ---------------------------------------------------------------------------
+// force
+
+extern "C" int hx_force_create(hx_ctx* ctx, const double* sigma, const double* jinv, const double* wdetj,
+                               double* D_out, hx_force** out) {
+  if (!ctx || !sigma || !jinv || !wdetj || !out) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  hx_force* f = new hx_force{ctx, nullptr};
+  if (dalloc(&f->DF, (size_t)ctx->ne * ctx->dim * ctx->dim * ctx->nq) != cudaSuccess) {
+    delete f;
+    return fail(ctx, HX_ECUDA, "alloc");
+  }
+  const long long n = (long long)ctx->nq * ctx->ne;
+  if (ctx->dim == 2) k_force_D<2><<<gblocks(n, 256), 256, 0, ctx->stream>>>(sigma, jinv, wdetj, ctx->ne, ctx->nq, f->DF, D_out);
+  else k_force_D<3><<<gblocks(n, 256), 256, 0, ctx->stream>>>(sigma, jinv, wdetj, ctx->ne, ctx->nq, f->DF, D_out);
+  CKL();
+  *out = f;
+  return HX_OK;
+}
+
+extern "C" int hx_force_destroy(hx_force* f) {
+  if (!f) return HX_OK;
+  cudaFree(f->DF);
+  delete f;
+  return HX_OK;
+}
+
+extern "C" int hx_force_apply(hx_force* f, const double* e, double* y) {
+  if (!f || !e || !y) return HX_EINVAL;
+  hx_ctx* ctx = f->ctx;
+  CK(cudaSetDevice(ctx->device));
+  ForceArgs a{e, f->DF, ctx->emap, tables(ctx), ctx->ne, ctx->evec2, nullptr};
+  int rc = dispatch<LaunchForce>(ctx, a, false);
+  if (rc) return rc;
+  return launch_scatter(ctx, ctx->evec2, ctx->dim, y);
+}
+
+extern "C" int hx_force_apply_t(hx_force* f, const double* v, double* y) {
+  if (!f || !v || !y) return HX_EINVAL;
+  hx_ctx* ctx = f->ctx;
+  CK(cudaSetDevice(ctx->device));
+  ForceArgs a{v, f->DF, ctx->emap, tables(ctx), ctx->ne, nullptr, y};
+  return dispatch<LaunchForce>(ctx, a, true);
+}
+
+// ---------------------------------------------------------------------------
+// phase
+
+extern "C" int hx_phase_begin(hx_ctx* ctx, const double* x, const double* qdata0, const uint8_t* bcmask,
+                              double* mass_D_out, double* mass_diag_out, double* minv_out) {
+  if (!ctx || !x || !qdata0) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  StatusDev* st = ctx->st + 3;
+  int rc = status_reset(ctx, st);
+  if (rc) return rc;
+  GeomArgs a{x, ctx->emap, tables(ctx), ctx->ne, nullptr, nullptr, nullptr, nullptr, ctx->Dm, mass_D_out, qdata0, st};
+  rc = dispatch<LaunchGeom>(ctx, a);
+  if (rc) return rc;
+  const long long n = (long long)ctx->nq * ctx->ne;
+  k_transpose<<<gblocks(n, 256), 256, 0, ctx->stream>>>(qdata0, ctx->nq, ctx->ne, ctx->qd0);
+  CKL();
+  rc = dispatch<LaunchMassDiag>(ctx, (const double*)ctx->Dm, ctx->evec2);
+  if (rc) return rc;
+  rc = launch_scatter(ctx, ctx->evec2, 1, ctx->mdiag);
+  if (rc) return rc;
+  const long long nv = ctx->nn * ctx->dim;
+  if (bcmask) CK(cudaMemcpyAsync(ctx->mask, bcmask, nv, cudaMemcpyDeviceToDevice, ctx->stream));
+  else CK(cudaMemsetAsync(ctx->mask, 0, nv, ctx->stream));
+  ctx->has_mask = bcmask != nullptr;
+  k_invdiag<<<gblocks(nv, 256), 256, 0, ctx->stream>>>(ctx->mdiag, ctx->mask, ctx->dim, ctx->nn, ctx->invd);
+  CKL();
+  rc = dispatch<LaunchMinv>(ctx, minv_out);
+  if (rc) return rc;
+  if (mass_diag_out) CK(cudaMemcpyAsync(mass_diag_out, ctx->mdiag, sizeof(double) * ctx->nn, cudaMemcpyDeviceToDevice, ctx->stream));
+  rc = read_status(ctx, st, ctx->h_st + 3);
+  if (rc) return rc;
+  if (ctx->h_st[3].inv_key != ~0ull) return fail(ctx, HX_EINVERTED, "inverted element in begin_phase");
+  ctx->phase = true;
+  return HX_OK;
+}
+
+extern "C" int hx_stress(hx_ctx* ctx, const hx_params* prm, const double* x, const double* v, const double* e,
+                         const double* qdata0, double* sigma, double* min_ratio, int64_t* clamped,
+                         hx_inverted* inv) {
+  if (!ctx || !prm || !x || !v || !e || !qdata0) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  StatusDev* st = ctx->st + 3;
+  int rc = status_reset(ctx, st);
+  if (rc) return rc;
+  StressArgs a{x, v, e, qdata0, ctx->emap, tables(ctx), prm->gamma, prm->q1, prm->q2, ctx->ne, sigma, st};
+  rc = dispatch<LaunchStress>(ctx, a);
+  if (rc) return rc;
+  rc = read_status(ctx, st, ctx->h_st + 3);
+  if (rc) return rc;
+  const StatusDev& h = ctx->h_st[3];
+  if (min_ratio) *min_ratio = h.min_ratio;
+  if (clamped) *clamped = (int64_t)h.clamps;
+  decode_inv(ctx, h.inv_key, inv);
+  return h.inv_key != ~0ull ? HX_EINVERTED : HX_OK;
+}
+
+extern "C" int hx_energy_solve(hx_ctx* ctx, const double* rhs, double* out) {
+  if (!ctx || !rhs || !out || !ctx->phase) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  const long long n = ctx->ne * ctx->nt;
+  k_energy_solve<<<gblocks(n, 256), 256, 0, ctx->stream>>>(ctx->minv, rhs, ctx->nt, ctx->ne, out);
+  CKL();
+  return HX_OK;
+}
+
+// One rates() evaluation on device: fused qpoint/force kernel then the masked CG.
+// Status lands in st; CG info in *cgi.  No host sync except inside the CG poll.
+static int rates_device(hx_ctx* ctx, const hx_params* prm, const double* x, const double* v, const double* e,
+                        double* dv, double* de, StatusDev* st, hx_cg_info* cgi) {
+  int rc = status_reset(ctx, st);
+  if (rc) return rc;
+  rc = dispatch<LaunchRates>(ctx, x, v, e, ctx->evec, de, st, 0, prm->gamma, prm->q1, prm->q2);
+  if (rc) return rc;
+  // rhs = where(mask, 0, -F.1) built inside k_cg_init from the element vectors
+  return run_cg(ctx, ctx->Dm, nullptr, ctx->evec, 1, ctx->has_mask ? ctx->mask : nullptr, ctx->invd,
+                prm->rel_tol, prm->max_iter, dv, ctx->dim, nullptr, cgi);
+}
+
+extern "C" int hx_rates(hx_ctx* ctx, const hx_params* prm, const double* x, const double* v, const double* e,
+                        double* dv, double* de, hx_step_info* info) {
+  if (!ctx || !prm || !x || !v || !e || !dv || !de || !ctx->phase) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  hx_cg_info ci{};
+  StatusDev* st = ctx->st + 0;
+  int rc = rates_device(ctx, prm, x, v, e, dv, de, st, &ci);
+  if (rc) return rc;
+  rc = read_status(ctx, st, ctx->h_st);
+  if (rc) return rc;
+  const StatusDev& h = ctx->h_st[0];
+  hx_step_info out{};
+  out.cg_iterations[0] = ci.iterations;
+  out.clamped = (int64_t)h.clamps;
+  out.min_h_over_speed = h.min_ratio;
+  decode_inv(ctx, h.inv_key, &out.inv);
+  out.code = out.inv.inverted ? HX_EINVERTED : ci.code;
+  if (info) *info = out;
+  return out.code;
+}
+
+// timestep_estimate (dt_fixed < 0) + rk2_step on device (hydro.py:364-405)
+static int step_impl(hx_ctx* ctx, const hx_params* prm, double t, double dt_fixed, const double* x,
+                     const double* v, const double* e, double* x_out, double* v_out, double* e_out,
+                     hx_step_info* info) {
+  if (!ctx || !prm || !x || !v || !e || !x_out || !v_out || !e_out || !ctx->phase) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  const bool estimate = dt_fixed < 0.0;
+  hx_step_info out{};
+  const long long nv = ctx->nn * ctx->dim, nte = ctx->ne * ctx->nt;
+  const unsigned ga = gblocks(std::max(nv, nte), 256);
+  long long clamps_total = 0;
+  for (int attempt = 0; attempt <= prm->max_retries; ++attempt) {
+    // stage 1: rates(S) -- its ratio is also timestep_estimate's (same state)
+    hx_cg_info c0{}, c1{};
+    int rc = rates_device(ctx, prm, x, v, e, ctx->dv0, ctx->de0, ctx->st + 0, &c0);
+    if (rc) return rc;
+    DtArgs da{ctx->st + 0, ctx->dt, prm->cfl, prm->dt_max, prm->t_final, t, dt_fixed, attempt};
+    k_dt<<<1, 1, 0, ctx->stream>>>(da);
+    CKL();
+    AxpyArgs m{x, v, e, v, ctx->dv0, ctx->de0, ctx->xm, ctx->vm, ctx->em, ctx->dt + 1, 0.5, nv, nte};
+    k_axpy_state<<<ga, 256, 0, ctx->stream>>>(m);
+    CKL();
+    rc = read_status(ctx, ctx->st + 0, ctx->h_st + 0);
+    if (rc) return rc;
+    const StatusDev s0 = ctx->h_st[0];
+    CK(cudaMemcpy(ctx->h_dt, ctx->dt, 2 * sizeof(double), cudaMemcpyDeviceToHost));
+    if (!estimate && s0.inv_key != ~0ull) {  // rates(state) raised inside rk2_step: retry
+      out.failed_stage = 0;
+      decode_inv(ctx, s0.inv_key, &out.inv);
+      out.retries = attempt + 1;
+      continue;
+    }
+    if (estimate && attempt == 0) {
+      if (s0.inv_key != ~0ull) {  // timestep_estimate on an inverted state raises
+        out.code = HX_EINVERTED;
+        out.failed_stage = 0;
+        decode_inv(ctx, s0.inv_key, &out.inv);
+        if (info) *info = out;
+        return out.code;
+      }
+      clamps_total += (long long)s0.clamps;  // timestep_estimate's stress_qdata call
+      out.dt = ctx->h_dt[0];
+      if (ctx->h_dt[0] < prm->dt_min) {
+        out.code = HX_EUNDERFLOW;
+        out.failed_stage = 0;
+        if (info) *info = out;
+        return out.code;
+      }
+    }
+    clamps_total += (long long)s0.clamps;  // rates(state)
+    if (c0.code) {
+      out.code = c0.code;
+      if (info) *info = out;
+      return out.code;
+    }
+    // stage 2: rates(mid)
+    rc = rates_device(ctx, prm, ctx->xm, ctx->vm, ctx->em, ctx->dv1, ctx->de1, ctx->st + 1, &c1);
+    if (rc) return rc;
+    AxpyArgs n{x, v, e, ctx->vm, ctx->dv1, ctx->de1, x_out, v_out, e_out, ctx->dt + 1, 1.0, nv, nte};
+    k_axpy_state<<<ga, 256, 0, ctx->stream>>>(n);
+    CKL();
+    // validity of the new geometry (hydro.py:400-401)
+    rc = status_reset(ctx, ctx->st + 2);
+    if (rc) return rc;
+    rc = dispatch<LaunchRates>(ctx, (const double*)x_out, (const double*)nullptr, (const double*)nullptr,
+                               (double*)nullptr, (double*)nullptr, ctx->st + 2, 1, 0.0, 0.0, 0.0);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(ctx->h_st + 1, ctx->st + 1, 2 * sizeof(StatusDev), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const StatusDev s1 = ctx->h_st[1], s2 = ctx->h_st[2];
+    out.cg_iterations[0] = c0.iterations;
+    out.cg_iterations[1] = c1.iterations;
+    if (s1.inv_key != ~0ull) {  // rates(mid) raised before stress_qdata
+      out.failed_stage = 1;
+      decode_inv(ctx, s1.inv_key, &out.inv);
+      out.retries = attempt + 1;
+      continue;
+    }
+    clamps_total += (long long)s1.clamps;
+    if (c1.code) {
+      out.code = c1.code;
+      if (info) *info = out;
+      return out.code;
+    }
+    if (s2.inv_key != ~0ull) {
+      out.failed_stage = 2;
+      decode_inv(ctx, s2.inv_key, &out.inv);
+      out.retries = attempt + 1;
+      continue;
+    }
+    out.code = HX_OK;
+    out.retries = attempt;
+    out.dt = ctx->h_dt[1];
+    out.min_h_over_speed = s1.min_ratio;
+    out.t_new = t + ctx->h_dt[1];
+    out.clamped = clamps_total;
+    out.inv.inverted = 0;
+    if (info) *info = out;
+    return HX_OK;
+  }
+  out.code = HX_EUNDERFLOW;
+  out.clamped = clamps_total;
+  if (info) *info = out;
+  return out.code;
+}
+
+extern "C" int hx_step(hx_ctx* ctx, const hx_params* prm, double t, const double* x, const double* v,
+                       const double* e, double* x_out, double* v_out, double* e_out, hx_step_info* info) {
+  return step_impl(ctx, prm, t, -1.0, x, v, e, x_out, v_out, e_out, info);
+}
+
+extern "C" int hx_rk2_step(hx_ctx* ctx, const hx_params* prm, double t, double dt, const double* x,
+                           const double* v, const double* e, double* x_out, double* v_out, double* e_out,
+                           hx_step_info* info) {
+  if (!(dt >= 0.0)) return fail(ctx, HX_EINVAL, "dt must be >= 0");
+  return step_impl(ctx, prm, t, dt, x, v, e, x_out, v_out, e_out, info);
+}
+
+extern "C" int hx_step_host(hx_ctx* ctx, const hx_params* prm, double t, double* x_host, double* v_host,
+                            double* e_host, hx_step_info* info) {
+  if (!ctx || !prm || !x_host || !v_host || !e_host) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  const size_t nvb = sizeof(double) * ctx->nn * ctx->dim, neb = sizeof(double) * ctx->ne * ctx->nt;
+  if (!ctx->hx_x) {
+    CK(cudaMalloc(&ctx->hx_x, nvb));
+    CK(cudaMalloc(&ctx->hx_v, nvb));
+    CK(cudaMalloc(&ctx->hx_e, neb));
+    CK(cudaMalloc(&ctx->hx_xo, nvb));
+    CK(cudaMalloc(&ctx->hx_vo, nvb));
+    CK(cudaMalloc(&ctx->hx_eo, neb));
+  }
+  CK(cudaMemcpyAsync(ctx->hx_x, x_host, nvb, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->hx_v, v_host, nvb, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->hx_e, e_host, neb, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = hx_step(ctx, prm, t, ctx->hx_x, ctx->hx_v, ctx->hx_e, ctx->hx_xo, ctx->hx_vo, ctx->hx_eo, info);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(x_host, ctx->hx_xo, nvb, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(v_host, ctx->hx_vo, nvb, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(e_host, ctx->hx_eo, neb, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return HX_OK;
+}
+
+extern "C" int hx_energies(hx_ctx* ctx, const double* v, const double* e, const double* qdata0, double* kinetic,
+                           double* internal) {
+  if (!ctx || !v || !e || !qdata0 || !ctx->phase) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  // KE = 0.5 v . (M v)  (hydro.py:409-411)
+  int rc = mass_evec(ctx, ctx->Dm, v, ctx->dim, ctx->evec2);
+  if (rc) return rc;
+  rc = launch_scatter(ctx, ctx->evec2, ctx->dim, ctx->xm);
+  if (rc) return rc;
+  k_dot<<<1, 256, 0, ctx->stream>>>(v, ctx->xm, ctx->nn * ctx->dim, ctx->scal);
+  CKL();
+  // IE = sum w qdata0 e_q (hydro.py:413-420); qdata0 given in reference layout
+  const long long n = (long long)ctx->nq * ctx->ne;
+  k_transpose<<<gblocks(n, 256), 256, 0, ctx->stream>>>(qdata0, ctx->nq, ctx->ne, ctx->evec2);
+  CKL();
+  rc = dispatch<LaunchIE>(ctx, e, (const double*)ctx->evec2, ctx->vm);
+  if (rc) return rc;
+  k_sum<<<1, 256, 0, ctx->stream>>>(ctx->vm, ctx->ne, ctx->scal + 1);
+  CKL();
+  double h[2];
+  CK(cudaMemcpyAsync(h, ctx->scal, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (kinetic) *kinetic = 0.5 * h[0];
+  if (internal) *internal = h[1];
+  return HX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// multi-GPU: not yet wired in this build (the Python layer partitions and
+// exchanges through torch.distributed); reported inactive.
+
+extern "C" int hx_comm_init(hx_ctx* ctx, const void*, int, int, int, const int32_t*, const int64_t*, const int32_t*,
+                            const uint8_t*) {
+  return fail(ctx, HX_EINVAL, "hx_comm_init: device-side NCCL halo not built in this version");
+}
+extern "C" int hx_comm_active(hx_ctx*) { return 0; }

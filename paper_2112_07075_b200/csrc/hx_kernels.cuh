@@ -1,0 +1,1120 @@
+// hx_kernels.cuh -- sm_100a kernels of the PA Lagrange hot path (fp64).
+//
+// Device layouts (internal, chosen for coalescing; the C-ABI converts at the edge):
+//   emap   (NE, nl) int32       element-major node ids (dofmap transposed)
+//   csr    node -> E-vector entries e*nl+l in ascending element order (deterministic G^T)
+//   own    (NE, nl) uint8       1 on the first (lowest-element) occurrence of each node
+//   Dm     (NE, nq)             mass point data  w*rho0*detJ0  (operators.py:85-95)
+//   qd0    (NE, nq)             rho0*detJ0  (hydro.py:195)
+//   DF     (NE, d*d, nq)        force point data (operators.py:258)
+//   minv   (NE, nt, nt)         inverse thermodynamic mass blocks (hydro.py:229-232)
+//   evec   (NE, nl, ncomp)      element results before the scatter
+#pragma once
+
+#include "hx_core.cuh"
+
+namespace hx {
+
+// ---------------------------------------------------------------------------
+// shared argument blocks
+
+struct Tables {
+  const double* B;    // (Q, D1)
+  const double* G;    // (Q, D1)
+  const double* Bt;   // (Q, DT)
+  const double* wnd;  // (nq) tensor weights, x fastest (fespace.py:339-344)
+  const double* psi1; // (nq) thermodynamic interpolant of the constant 1
+};
+
+template <int Q, int D1, int DT>
+__device__ __forceinline__ void load_tables(const Tables& t, double* sB, double* sG, double* sBt) {
+  for (int i = threadIdx.x; i < Q * D1; i += blockDim.x) {
+    sB[i] = t.B[i];
+    sG[i] = t.G[i];
+  }
+  for (int i = threadIdx.x; i < Q * DT; i += blockDim.x) sBt[i] = t.Bt[i];
+}
+
+struct StatusDev {
+  unsigned long long inv_key;  // min over det<=0 points of q*NE+e (~0ull if none)
+  unsigned long long clamps;   // e<0 clamps (hydro.py:275-278)
+  double min_ratio;            // min h/(c_s+|v|)  (hydro.py:311-315)
+  int pad;
+};
+
+// ---------------------------------------------------------------------------
+// per-point physics (hydro.py:271-315, fespace.py:280-302, operators.py:258)
+
+template <int DIM>
+struct PointOut {
+  double det;
+  double jinv[DIM][DIM];
+  double sigma[DIM][DIM];
+  double ratio;
+  int clamped;
+};
+
+// dx[a][b] = d x_a / d xi_b ; reference "inverse": 2D adj/det, 3D cof/det
+template <int DIM>
+__device__ __forceinline__ double det_inv(const double (&J)[DIM][DIM], double (&inv)[DIM][DIM]) {
+  if constexpr (DIM == 2) {
+    const double det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    inv[0][0] = J[1][1] / det;
+    inv[0][1] = -J[0][1] / det;
+    inv[1][0] = -J[1][0] / det;
+    inv[1][1] = J[0][0] / det;
+    return det;
+  } else {
+    const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                       J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                       J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int r0 = r == 0 ? 1 : 0, r1 = r == 2 ? 1 : 2;
+        const int c0 = c == 0 ? 1 : 0, c1 = c == 2 ? 1 : 2;
+        const double m = J[r0][c0] * J[r1][c1] - J[r0][c1] * J[r1][c0];
+        inv[r][c] = (((r + c) & 1) ? -m : m) / det;
+      }
+    return det;
+  }
+}
+
+template <int DIM>
+__device__ __forceinline__ void point_physics(const double (&J)[DIM][DIM], const double (&dv)[DIM][DIM],
+                                              const double (&vq)[DIM], double eq, double qd0,
+                                              double gamma, double q1, double q2, PointOut<DIM>& o) {
+  o.det = det_inv<DIM>(J, o.jinv);
+  const double det = o.det;
+  const double rho = qd0 / det;
+  o.clamped = 0;
+  if (eq < 0.0) {
+    o.clamped = 1;
+    eq = 0.0;
+  }
+  const double p = (gamma - 1.0) * rho * eq;
+  const double cs = sqrt(gamma * (gamma - 1.0) * eq);
+  double gv[DIM][DIM];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a)
+#pragma unroll
+    for (int b = 0; b < DIM; ++b) {
+      double s = 0.0;
+#pragma unroll
+      for (int l = 0; l < DIM; ++l) s = fma(dv[a][l], o.jinv[l][b], s);
+      gv[a][b] = s;
+    }
+#pragma unroll
+  for (int a = 0; a < DIM; ++a)
+#pragma unroll
+    for (int b = 0; b < DIM; ++b) o.sigma[a][b] = (a == b) ? -p : 0.0;
+  double div = 0.0;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) div += gv[a][a];
+  const double h = (DIM == 3) ? pow(det, 1.0 / 3.0) : pow(det, 0.5);
+  if (q1 > 0.0 || q2 > 0.0) {
+    double mu = rho * h * (q1 * cs + q2 * h * fabs(div));
+    mu = div < 0.0 ? mu : 0.0;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) o.sigma[a][b] += mu * (0.5 * (gv[a][b] + gv[b][a]));
+  }
+  double v2 = 0.0;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) v2 += vq[a] * vq[a];
+  const double speed = cs + sqrt(v2);
+  o.ratio = speed > 0.0 ? h / fmax(speed, 1e-300) : __longlong_as_double(0x7ff0000000000000ll);
+}
+
+// D_F[a][l] = sum_b sigma[a][b] jinv[l][b] wdetj  (operators.py:258)
+template <int DIM>
+__device__ __forceinline__ void force_point(const double (&sig)[DIM][DIM], const double (&jinv)[DIM][DIM],
+                                            double wdetj, double (&DF)[DIM][DIM]) {
+#pragma unroll
+  for (int a = 0; a < DIM; ++a)
+#pragma unroll
+    for (int l = 0; l < DIM; ++l) {
+      double s = 0.0;
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) s = fma(sig[a][b], jinv[l][b], s);
+      DF[a][l] = s * wdetj;
+    }
+}
+
+// block-level status publication: ratio min, clamp sum, inversion key
+template <int NT>
+__device__ __forceinline__ void publish_status(StatusDev* st, double rmin, long long clamps,
+                                               unsigned long long key, double* sbuf) {
+  rmin = warp_min(rmin);
+  clamps = warp_sum_ll(clamps);
+  if ((threadIdx.x & 31) == 0) {
+    if (clamps) atomicAdd(&st->clamps, (unsigned long long)clamps);
+    atomic_min_nonneg(&st->min_ratio, rmin);
+  }
+  if (key != ~0ull) atomicMin(&st->inv_key, key);
+  (void)sbuf;
+}
+
+// ---------------------------------------------------------------------------
+// K_rates: fused quadrature-point setup + F.1 + F^T v + M_e^{-1}
+// (LagrangeHydro.rates hydro.py:346-360 minus the momentum solve: geometry
+//  fespace.py:305-346, stress_qdata hydro.py:254-315, ForcePA operators.py:247-300,
+//  solve_energy hydro.py:339-344).  One CTA per element; D_F never leaves smem.
+
+struct RatesArgs {
+  const double* x;     // (NN, d)
+  const double* v;     // (NN, d)
+  const double* e;     // (NE*nt)
+  const double* qd0;   // (NE, nq)
+  const int* emap;     // (NE, nl)
+  const double* minv;  // (NE, nt, nt)
+  Tables tab;
+  double gamma, q1, q2;
+  long long ne;
+  double* evec;        // (NE, nl, d)  element F.1
+  double* de;          // (NE*nt)      M_e^{-1} F^T v
+  StatusDev* st;
+  int mode;            // 0: full rates; 1: geometry validity only
+};
+
+template <int DIM, int P>
+struct RatesSmem {
+  using D = Disc<DIM, P>;
+  static constexpr int NCG = 2 * DIM;
+  static constexpr int A = cmax(NCG * D::NL, DIM == 3 ? 3 * NCG * D::Q * D::Q * D::D1 : 0);
+  static constexpr int S = 2 * NCG * D::Q * ipow(D::D1, DIM - 1);
+  static constexpr int OUT = NCG * (DIM + 1) * D::NQ;
+  static constexpr int TH = 2 * D::NQ;
+  static constexpr int TABS = 2 * D::Q * D::D1 + D::Q * D::DT;
+  static constexpr int RED = 32;
+  static constexpr int TOTAL = TABS + A + S + OUT + TH + D::NT + RED;
+  static constexpr size_t bytes = sizeof(double) * TOTAL;
+};
+
+template <int DIM, int P, int NT>
+__global__ void __launch_bounds__(NT) k_rates(RatesArgs a) {
+  using D = Disc<DIM, P>;
+  using SM = RatesSmem<DIM, P>;
+  constexpr int D1 = D::D1, Q = D::Q, DT = D::DT, NL = D::NL, NQ = D::NQ, NTH = D::NT;
+  constexpr int NCG = SM::NCG;
+  extern __shared__ double smem[];
+  double* sB = smem;
+  double* sG = sB + Q * D1;
+  double* sBt = sG + Q * D1;
+  double* rA = sBt + Q * DT;
+  double* rS = rA + SM::A;
+  double* rOut = rS + SM::S;
+  double* rTH = rOut + SM::OUT;
+  double* rMV = rTH + SM::TH;
+  double* red = rMV + NTH;
+  const int tid = threadIdx.x;
+  const long long e = blockIdx.x;
+  load_tables<Q, D1, DT>(a.tab, sB, sG, sBt);
+
+  // gather x and v (components 0..DIM-1 = x, DIM..2DIM-1 = v), and e
+  const int* em = a.emap + e * NL;
+  for (int i = tid; i < NL * DIM; i += NT) {
+    const int l = i / DIM, c = i - l * DIM;
+    const long long n = em[l];
+    rA[c * NL + l] = a.x[n * DIM + c];
+    if (a.mode == 0) rA[(DIM + c) * NL + l] = a.v[n * DIM + c];
+  }
+  if (a.mode == 0)
+    for (int i = tid; i < NTH; i += NT) rTH[i] = a.e[e * NTH + i];
+  __syncthreads();
+  if (a.mode == 1) {
+    grad<DIM, D1, Q, DIM, DIM + 1, NT>(sB, sG, rA, rS, rA, rOut, tid);
+    __syncthreads();
+    unsigned long long key = ~0ull;
+    for (int q = tid; q < NQ; q += NT) {
+      double J[DIM][DIM], inv[DIM][DIM];
+#pragma unroll
+      for (int c = 0; c < DIM; ++c)
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) J[c][b] = rOut[(c * (DIM + 1) + b) * NQ + q];
+      const double det = det_inv<DIM>(J, inv);
+      if (det <= 0.0) {
+        const unsigned long long k = (unsigned long long)q * a.ne + e;
+        key = k < key ? k : key;
+      }
+    }
+    if (key != ~0ull) atomicMin(&a.st->inv_key, key);
+    return;
+  }
+  grad<DIM, D1, Q, NCG, DIM + 1, NT>(sB, sG, rA, rS, rA, rOut, tid);
+  double* eq = interp<DIM, DT, Q, 1, NT>(sBt, rTH, rTH + NQ, tid);
+  double* sq = (eq == rTH) ? rTH + NQ : rTH;
+  __syncthreads();
+
+  // per-point physics; the point owner rewrites its slots in place:
+  //   rOut[c][l][q] (c < DIM) <- D_F[c][l] * psi1_q  (F.1 components)
+  //   sq[q]                   <- sum_{a,l} D_F[a][l] dv_a/dxi_l  (F^T v integrand)
+  double rmin = __longlong_as_double(0x7ff0000000000000ll);
+  long long clamps = 0;
+  unsigned long long key = ~0ull;
+  for (int q = tid; q < NQ; q += NT) {
+    double J[DIM][DIM], dv[DIM][DIM], vq[DIM];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) {
+        J[c][b] = rOut[(c * (DIM + 1) + b) * NQ + q];
+        dv[c][b] = rOut[((DIM + c) * (DIM + 1) + b) * NQ + q];
+      }
+      vq[c] = rOut[((DIM + c) * (DIM + 1) + DIM) * NQ + q];
+    }
+    PointOut<DIM> po;
+    point_physics<DIM>(J, dv, vq, eq[q], a.qd0[e * NQ + q], a.gamma, a.q1, a.q2, po);
+    if (po.det <= 0.0) {
+      const unsigned long long k = (unsigned long long)q * a.ne + e;
+      key = k < key ? k : key;
+    }
+    clamps += po.clamped;
+    rmin = fmin(rmin, po.ratio);
+    double DF[DIM][DIM];
+    force_point<DIM>(po.sigma, po.jinv, a.tab.wnd[q] * po.det, DF);
+    const double p1 = a.tab.psi1[q];
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c)
+#pragma unroll
+      for (int l = 0; l < DIM; ++l) {
+        s += DF[c][l] * dv[c][l];
+        rOut[(c * (DIM + 1) + l) * NQ + q] = DF[c][l] * p1;
+      }
+    sq[q] = s;
+  }
+  publish_status<NT>(a.st, rmin, clamps, key, red);
+  __syncthreads();
+  // F.1 element vector: grad_t over the x-slots; result into the dead v-slots
+  double* fout = rOut + DIM * (DIM + 1) * NQ;
+  grad_t<DIM, D1, Q, DIM, (DIM + 1) * NQ, NT>(sB, sG, rOut, rA, rS, fout, tid);
+  // F^T v: thermodynamic transpose interpolation (operators.py:297)
+  double* fv = interp_t<DIM, DT, Q, 1, NT>(sBt, sq, eq, tid);
+  __syncthreads();
+  double* ev = a.evec + e * NL * DIM;
+  for (int i = tid; i < NL * DIM; i += NT) {
+    const int l = i / DIM, c = i - l * DIM;
+    ev[i] = fout[c * NL + l];
+  }
+  // de = M_e^{-1} (F^T v)_e   (einsum "eij,ej->ei", hydro.py:343)
+  const double* mi = a.minv + e * NTH * NTH;
+  for (int i = tid; i < NTH; i += NT) {
+    double s = 0.0;
+    for (int j = 0; j < NTH; ++j) s = fma(mi[i * NTH + j], fv[j], s);
+    a.de[e * NTH + i] = s;
+  }
+  (void)rMV;
+}
+
+// ---------------------------------------------------------------------------
+// K_mass: PA mass action, one warp per element (MassPA._apply_scalar operators.py:97-115).
+// CG mode fuses the direction update p = z + beta p_old, the wall mask of
+// _solve_momentum (hydro.py:323-327) and the element-wise p.Ap partial:
+//   p.Ap = sum_e sum_q D (B w_e)^2 + sum_{masked} p^2.
+
+struct CGDev {
+  double rz, norm0, alpha, beta, tol;
+  int it, active, code, iters, max_iter, nres;
+  unsigned int cnt[4];
+};
+
+struct MassArgs {
+  const double* x;      // apply: input (NN, NC); cg: z
+  const double* pold;   // cg: p_{k-1} buffers [2]
+  double* pbuf0;
+  double* pbuf1;
+  const uint8_t* mask;  // (NN, NC) or null
+  const uint8_t* own;   // (NE, nl)
+  const double* D;      // (NE, nq)
+  const int* emap;
+  const double* B;      // (Q, D1)
+  long long ne;
+  double* evec;         // (NE, nl, NC)
+  CGDev* cg;
+  double* partials;
+};
+
+template <int DIM, int P>
+struct MassCfg {
+  using D = Disc<DIM, P>;
+  static constexpr int WARPS = 4;
+  static constexpr int NT = 32 * WARPS;
+};
+
+template <int DIM, int P, int NC, bool CG>
+__global__ void __launch_bounds__(128) k_mass(MassArgs a) {
+  using D = Disc<DIM, P>;
+  constexpr int D1 = D::D1, Q = D::Q, NL = D::NL, NQ = D::NQ;
+  constexpr int WARPS = 4;
+  constexpr int BUF = NC * NQ;
+  extern __shared__ double smem[];
+  __shared__ double red[32];
+  __shared__ int sflag;
+  double* sB = smem;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* A = smem + Q * D1 + warp * 2 * BUF;
+  double* Bf = A + BUF;
+  if (CG && !a.cg->active) return;
+  for (int i = threadIdx.x; i < Q * D1; i += blockDim.x) sB[i] = a.B[i];
+  __syncthreads();
+  const long long e = (long long)blockIdx.x * WARPS + warp;
+  double acc = 0.0;
+  double beta = 0.0;
+  const double* pz = a.x;
+  const double* po = nullptr;
+  if constexpr (CG) {
+    beta = a.cg->beta;
+    po = (a.cg->it & 1) ? a.pbuf0 : a.pbuf1;  // p_{k-1} lives in pbuf[(k-1)&1]
+  }
+  if (e < a.ne) {
+    const int* em = a.emap + e * NL;
+    for (int i = lane; i < NL * NC; i += 32) {
+      const int l = i / NC, c = i - l * NC;
+      const long long n = em[l];
+      double val;
+      if constexpr (CG) {
+        const double p = __dadd_rn(pz[n * NC + c], __dmul_rn(beta, po[n * NC + c]));
+        const bool m = a.mask && a.mask[n * NC + c];
+        if (m && a.own[e * NL + l]) acc = fma(p, p, acc);
+        val = m ? 0.0 : p;
+      } else {
+        val = pz[n * NC + c];
+      }
+      A[c * NL + l] = val;
+    }
+    __syncwarp();
+    double* qv = interp<DIM, D1, Q, NC, 32>(sB, A, Bf, lane);
+    __syncwarp();
+    const double* De = a.D + e * NQ;
+    for (int i = lane; i < NQ * NC; i += 32) {
+      const int q = i % NQ;
+      const double u = qv[i];
+      const double du = u * De[q];
+      if constexpr (CG) acc = fma(du, u, acc);
+      qv[i] = du;
+    }
+    __syncwarp();
+    double* other = (qv == A) ? Bf : A;
+    double* r = interp_t<DIM, D1, Q, NC, 32>(sB, qv, other, lane);
+    __syncwarp();
+    double* ev = a.evec + e * NL * NC;
+    for (int i = lane; i < NL * NC; i += 32) {
+      const int l = i / NC, c = i - l * NC;
+      ev[i] = r[c * NL + l];
+    }
+  }
+  if constexpr (CG) {
+    const double bs = block_sum<128>(acc, red);
+    if (threadIdx.x == 0) a.partials[blockIdx.x] = bs;
+    if (grid_last_block(&a.cg->cnt[0], &sflag)) {
+      const double pAp = reduce_partials<128>(a.partials, gridDim.x, red);
+      if (threadIdx.x == 0) {
+        a.cg->cnt[0] = 0;
+        if (pAp <= 0.0) {
+          a.cg->code = 3;
+          a.cg->active = 0;
+        } else {
+          a.cg->alpha = a.cg->rz / pAp;
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// node-side kernels: deterministic G^T through the transpose map
+
+// L[n, c] = sum over entries of node n (ascending element) of E[idx, c]   (fespace.py:227-234)
+template <int NC>
+__device__ __forceinline__ void node_sum(const int* off, const int* idx, const double* E, long long n,
+                                         double (&s)[NC]) {
+#pragma unroll
+  for (int c = 0; c < NC; ++c) s[c] = 0.0;
+  const int b = off[n], f = off[n + 1];
+  for (int k = b; k < f; ++k) {
+    const long long j = idx[k];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) s[c] += E[j * NC + c];
+  }
+}
+
+struct NodeArgs {
+  const int* off;
+  const int* idx;
+  const double* evec;   // (NE, nl, NC)
+  const uint8_t* mask;
+  const double* invd;   // (NN, NC) 1/diag (masked rows -> 1)
+  double* x;
+  double* r;
+  double* z;
+  double* pbuf0;
+  double* pbuf1;
+  const double* rhs;    // cg_init from an explicit rhs (NN, NC) or null
+  double* out;          // scatter output
+  long long nn;
+  CGDev* cg;
+  double* partials;
+  double* hist;
+  int negate;           // cg_init from evec: rhs = -sum
+};
+
+// plain scatter: out = G^T evec (internal layout)
+template <int NC>
+__global__ void __launch_bounds__(256) k_scatter(NodeArgs a) {
+  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= a.nn) return;
+  double s[NC];
+  node_sum<NC>(a.off, a.idx, a.evec, n, s);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) a.out[n * NC + c] = s[c];
+}
+
+// CG start (cg_solve operators.py:340-350): r = b, z = D^{-1} r, x = 0, p_0 = 0,
+// rz = r.z, norm0 = sqrt(rz); b == 0 everywhere -> 0 iterations.
+// b is rhs, or -(G^T evec) masked (rhs_v = -F.1, hydro.py:351, 320).
+template <int NC>
+__global__ void __launch_bounds__(256) k_cg_init(NodeArgs a) {
+  __shared__ double red[32];
+  __shared__ int sflag;
+  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double rz = 0.0, nz = 0.0;
+  if (n < a.nn) {
+    double s[NC];
+    if (a.rhs) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) s[c] = a.rhs[n * NC + c];
+    } else {
+      node_sum<NC>(a.off, a.idx, a.evec, n, s);
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      double b = a.negate ? -s[c] : s[c];
+      if (a.mask && a.mask[n * NC + c]) b = 0.0;
+      const double z = a.invd[n * NC + c] * b;
+      a.r[n * NC + c] = b;
+      a.z[n * NC + c] = z;
+      a.x[n * NC + c] = 0.0;
+      a.pbuf0[n * NC + c] = 0.0;
+      rz = fma(b, z, rz);
+      if (b != 0.0 || b != b) nz += 1.0;
+    }
+  }
+  const double brz = block_sum<256>(rz, red);
+  const double bnz = block_sum<256>(nz, red);
+  if (threadIdx.x == 0) {
+    a.partials[2 * blockIdx.x] = brz;
+    a.partials[2 * blockIdx.x + 1] = bnz;
+  }
+  if (grid_last_block(&a.cg->cnt[2], &sflag)) {
+    double t = 0.0, anyb = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += 256) {
+      t += __ldcg(a.partials + 2 * i);
+      anyb += __ldcg(a.partials + 2 * i + 1);
+    }
+    t = block_sum<256>(t, red);
+    anyb = block_sum<256>(anyb, red);
+    if (threadIdx.x == 0) {
+      CGDev* g = a.cg;
+      g->cnt[2] = 0;
+      g->code = 0;
+      g->beta = 0.0;
+      g->it = 1;
+      g->iters = 0;
+      if (anyb == 0.0) {
+        g->active = 0;
+        g->nres = 0;
+      } else {
+        g->rz = t;
+        g->norm0 = sqrt(t);
+        if (a.hist) a.hist[0] = g->norm0;
+        g->nres = 1;
+        g->active = 1;
+      }
+    }
+  }
+}
+
+// CG iteration tail (operators.py:352-365): p_k = z + beta p_{k-1} (written),
+// Ap = G^T evec (identity on masked rows), x += alpha p, r -= alpha Ap, z = D^{-1} r,
+// rz_new = r.z; stop test sqrt(max(rz_new,0)) <= tol*norm0; beta = rz_new/rz.
+template <int NC>
+__global__ void __launch_bounds__(256) k_cg_node(NodeArgs a) {
+  __shared__ double red[32];
+  __shared__ int sflag;
+  CGDev* g = a.cg;
+  if (!g->active) return;
+  const int k = g->it;
+  const double alpha = g->alpha, beta = g->beta;
+  const double* po = (k & 1) ? a.pbuf0 : a.pbuf1;
+  double* pn = (k & 1) ? a.pbuf1 : a.pbuf0;
+  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double rz = 0.0;
+  if (n < a.nn) {
+    double s[NC];
+    node_sum<NC>(a.off, a.idx, a.evec, n, s);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const long long j = n * NC + c;
+      const double p = __dadd_rn(a.z[j], __dmul_rn(beta, po[j]));
+      pn[j] = p;
+      const double ap = (a.mask && a.mask[j]) ? p : s[c];
+      a.x[j] = __dadd_rn(a.x[j], __dmul_rn(alpha, p));
+      const double r = __dsub_rn(a.r[j], __dmul_rn(alpha, ap));
+      a.r[j] = r;
+      const double z = __dmul_rn(a.invd[j], r);
+      a.z[j] = z;
+      rz = fma(r, z, rz);
+    }
+  }
+  const double brz = block_sum<256>(rz, red);
+  if (threadIdx.x == 0) a.partials[blockIdx.x] = brz;
+  if (grid_last_block(&g->cnt[1], &sflag)) {
+    const double rzn = reduce_partials<256>(a.partials, gridDim.x, red);
+    if (threadIdx.x == 0) {
+      g->cnt[1] = 0;
+      const double res = sqrt(fmax(rzn, 0.0));
+      if (a.hist) a.hist[k] = res;
+      g->nres = k + 1;
+      if (res <= g->tol * g->norm0) {
+        g->iters = k;
+        g->active = 0;
+      } else if (k >= g->max_iter) {
+        g->code = 4;
+        g->iters = k;
+        g->active = 0;
+      } else {
+        g->beta = rzn / g->rz;
+        g->rz = rzn;
+        g->it = k + 1;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// state updates (rk2_step hydro.py:385-399)
+
+struct AxpyArgs {
+  const double* x;
+  const double* v;
+  const double* e;
+  const double* dxs;   // velocity used as dx (state.v for stage 1, mid.v for stage 2)
+  const double* dv;
+  const double* de;
+  double* xo;
+  double* vo;
+  double* eo;
+  const double* dtp;   // device attempt dt
+  double scale;        // 0.5 (midpoint) or 1.0
+  long long nv;        // NN*d
+  long long nte;       // NE*nt
+};
+
+__global__ void __launch_bounds__(256) k_axpy_state(AxpyArgs a) {
+  const double h = a.scale == 1.0 ? *a.dtp : (*a.dtp / 2.0);
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < a.nv) {
+    a.xo[i] = __dadd_rn(a.x[i], __dmul_rn(h, a.dxs[i]));
+    a.vo[i] = __dadd_rn(a.v[i], __dmul_rn(h, a.dv[i]));
+  }
+  if (i < a.nte) a.eo[i] = __dadd_rn(a.e[i], __dmul_rn(h, a.de[i]));
+}
+
+// dt = min(cfl*ratio, dt_max, t_final - t) / 2^retry  (timestep_estimate hydro.py:364-373)
+struct DtArgs {
+  const StatusDev* st;
+  double* dt;        // [0] = estimate, [1] = attempt
+  double cfl, dt_max, t_final, t;
+  double dt_fixed;   // >= 0: rk2_step(state, dt) with a caller-given dt
+  int retry;
+};
+__global__ void k_dt(DtArgs a) {
+  double dt;
+  if (a.dt_fixed >= 0.0) {
+    dt = a.dt_fixed;
+  } else {
+    dt = a.cfl * a.st->min_ratio;
+    dt = fmin(dt, a.dt_max);
+    dt = fmin(dt, a.t_final - a.t);
+  }
+  a.dt[0] = dt;
+  double att = dt;
+  for (int i = 0; i < a.retry; ++i) att /= 2.0;
+  a.dt[1] = att;
+}
+
+// ---------------------------------------------------------------------------
+// API-level kernels (reference layouts in, reference layouts out)
+
+// gather to the reference E-vector layout (nl, NE, ncomp)
+__global__ void k_gather_ref(const double* L, const int* emap, int nl, long long ne, int nc, double* E) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long tot = (long long)nl * ne * nc;
+  if (t >= tot) return;
+  const int c = (int)(t % nc);
+  const long long le = t / nc;  // l*NE + e
+  const long long e = le % ne, l = le / ne;
+  E[t] = L[(long long)emap[e * nl + l] * nc + c];
+}
+
+// scatter from the reference E-vector layout, ascending element per node (bit-exact np.add.at)
+__global__ void k_scatter_ref(const double* E, const int* off, const int* idx, int nl, long long ne,
+                              long long nn, int nc, double* L) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nn * nc) return;
+  const long long n = t / nc;
+  const int c = (int)(t % nc);
+  double s = 0.0;
+  for (int k = off[n]; k < off[n + 1]; ++k) {
+    const long long j = idx[k];
+    const long long e = j / nl, l = j % nl;
+    s += E[(l * ne + e) * nc + c];
+  }
+  L[t] = s;
+}
+
+// L2 space: E (nt, NE, nc) <-> L (NE*nt, nc) is a transpose
+__global__ void k_l2_gather(const double* L, int nt, long long ne, int nc, double* E, int transpose_back) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)nt * ne * nc) return;
+  const int c = (int)(t % nc);
+  const long long le = t / nc;
+  const long long e = le % ne, l = le / ne;
+  if (!transpose_back) E[t] = L[(e * nt + l) * nc + c];
+  else E[(e * nt + l) * nc + c] = L[t];
+}
+
+// (nq, NE) <-> (NE, nq) transposes and general point-data transposes
+__global__ void k_transpose(const double* in, long long rows, long long cols, double* out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= rows * cols) return;
+  const long long r = t / cols, c = t % cols;
+  out[c * rows + r] = in[t];
+}
+
+// geometry in reference layouts (compute_geometric_factors, fespace.py:326-346)
+struct GeomArgs {
+  const double* x;
+  const int* emap;
+  Tables tab;
+  long long ne;
+  double* jac;
+  double* detj;
+  double* jinv;
+  double* wdetj;
+  double* Dm_int;       // optional (NE, nq): (wdetj/detj)*qdata0 (hydro.py:223-224)
+  double* Dm_ref;       // optional (nq, NE)
+  const double* qdata0; // (nq, NE) ref layout
+  StatusDev* st;
+};
+
+template <int DIM, int P>
+struct GeomSmem {
+  using D = Disc<DIM, P>;
+  static constexpr int A = cmax(DIM * D::NL, DIM == 3 ? 3 * DIM * D::Q * D::Q * D::D1 : 0);
+  static constexpr int S = 2 * DIM * D::Q * ipow(D::D1, DIM - 1);
+  static constexpr int OUT = DIM * (DIM + 1) * D::NQ;
+  static constexpr int TOTAL = 2 * D::Q * D::D1 + D::Q * D::DT + A + S + OUT;
+  static constexpr size_t bytes = sizeof(double) * TOTAL;
+};
+
+template <int DIM, int P, int NT>
+__global__ void __launch_bounds__(NT) k_geom(GeomArgs a) {
+  using D = Disc<DIM, P>;
+  using SM = GeomSmem<DIM, P>;
+  constexpr int D1 = D::D1, Q = D::Q, DT = D::DT, NL = D::NL, NQ = D::NQ;
+  extern __shared__ double smem[];
+  double* sB = smem;
+  double* sG = sB + Q * D1;
+  double* sBt = sG + Q * D1;
+  double* rA = sBt + Q * DT;
+  double* rS = rA + SM::A;
+  double* rOut = rS + SM::S;
+  const int tid = threadIdx.x;
+  const long long e = blockIdx.x;
+  const long long ne = a.ne;
+  load_tables<Q, D1, DT>(a.tab, sB, sG, sBt);
+  const int* em = a.emap + e * NL;
+  for (int i = tid; i < NL * DIM; i += NT) {
+    const int l = i / DIM, c = i - l * DIM;
+    rA[c * NL + l] = a.x[(long long)em[l] * DIM + c];
+  }
+  __syncthreads();
+  grad<DIM, D1, Q, DIM, DIM + 1, NT>(sB, sG, rA, rS, rA, rOut, tid);
+  __syncthreads();
+  unsigned long long key = ~0ull;
+  for (int q = tid; q < NQ; q += NT) {
+    double J[DIM][DIM], inv[DIM][DIM];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c)
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) J[c][b] = rOut[(c * (DIM + 1) + b) * NQ + q];
+    const double det = det_inv<DIM>(J, inv);
+    if (det <= 0.0) {
+      const unsigned long long k = (unsigned long long)q * ne + e;
+      key = k < key ? k : key;
+    }
+    const long long pe = (long long)q * ne + e;
+    const double wd = a.tab.wnd[q] * det;
+#pragma unroll
+    for (int r = 0; r < DIM; ++r)
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) {
+        if (a.jac) a.jac[(long long)(r * DIM + c) * NQ * ne + pe] = J[r][c];
+        if (a.jinv) a.jinv[(long long)(r * DIM + c) * NQ * ne + pe] = inv[r][c];
+      }
+    if (a.detj) a.detj[pe] = det;
+    if (a.wdetj) a.wdetj[pe] = wd;
+    if (a.Dm_int || a.Dm_ref) {
+      const double dm = (wd / det) * a.qdata0[pe];
+      if (a.Dm_int) a.Dm_int[e * NQ + q] = dm;
+      if (a.Dm_ref) a.Dm_ref[pe] = dm;
+    }
+  }
+  if (key != ~0ull && a.st) atomicMin(&a.st->inv_key, key);
+}
+
+// stress_qdata in reference layout (hydro.py:254-315), geometry recomputed from x
+struct StressArgs {
+  const double* x;
+  const double* v;
+  const double* e;
+  const double* qdata0;  // (nq, NE)
+  const int* emap;
+  Tables tab;
+  double gamma, q1, q2;
+  long long ne;
+  double* sigma;         // (d,d,nq,NE) or null
+  StatusDev* st;
+};
+
+template <int DIM, int P, int NT>
+__global__ void __launch_bounds__(NT) k_stress(StressArgs a) {
+  using D = Disc<DIM, P>;
+  using SM = RatesSmem<DIM, P>;
+  constexpr int D1 = D::D1, Q = D::Q, DT = D::DT, NL = D::NL, NQ = D::NQ, NTH = D::NT;
+  constexpr int NCG = SM::NCG;
+  extern __shared__ double smem[];
+  double* sB = smem;
+  double* sG = sB + Q * D1;
+  double* sBt = sG + Q * D1;
+  double* rA = sBt + Q * DT;
+  double* rS = rA + SM::A;
+  double* rOut = rS + SM::S;
+  double* rTH = rOut + SM::OUT;
+  double* red = rTH + SM::TH + NTH;
+  const int tid = threadIdx.x;
+  const long long e = blockIdx.x, ne = a.ne;
+  load_tables<Q, D1, DT>(a.tab, sB, sG, sBt);
+  const int* em = a.emap + e * NL;
+  for (int i = tid; i < NL * DIM; i += NT) {
+    const int l = i / DIM, c = i - l * DIM;
+    const long long n = em[l];
+    rA[c * NL + l] = a.x[n * DIM + c];
+    rA[(DIM + c) * NL + l] = a.v[n * DIM + c];
+  }
+  for (int i = tid; i < NTH; i += NT) rTH[i] = a.e[e * NTH + i];
+  __syncthreads();
+  grad<DIM, D1, Q, NCG, DIM + 1, NT>(sB, sG, rA, rS, rA, rOut, tid);
+  double* eq = interp<DIM, DT, Q, 1, NT>(sBt, rTH, rTH + NQ, tid);
+  __syncthreads();
+  double rmin = __longlong_as_double(0x7ff0000000000000ll);
+  long long clamps = 0;
+  unsigned long long key = ~0ull;
+  for (int q = tid; q < NQ; q += NT) {
+    double J[DIM][DIM], dv[DIM][DIM], vq[DIM];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) {
+        J[c][b] = rOut[(c * (DIM + 1) + b) * NQ + q];
+        dv[c][b] = rOut[((DIM + c) * (DIM + 1) + b) * NQ + q];
+      }
+      vq[c] = rOut[((DIM + c) * (DIM + 1) + DIM) * NQ + q];
+    }
+    const long long pe = (long long)q * ne + e;
+    PointOut<DIM> po;
+    point_physics<DIM>(J, dv, vq, eq[q], a.qdata0[pe], a.gamma, a.q1, a.q2, po);
+    if (po.det <= 0.0) {
+      const unsigned long long k = (unsigned long long)q * ne + e;
+      key = k < key ? k : key;
+    }
+    clamps += po.clamped;
+    rmin = fmin(rmin, po.ratio);
+    if (a.sigma)
+#pragma unroll
+      for (int r = 0; r < DIM; ++r)
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) a.sigma[(long long)(r * DIM + c) * NQ * ne + pe] = po.sigma[r][c];
+  }
+  publish_status<NT>(a.st, rmin, clamps, key, red);
+}
+
+// D_F from reference-layout sigma, jinv, wdetj -> internal (NE, d*d, nq)
+template <int DIM>
+__global__ void k_force_D(const double* sigma, const double* jinv, const double* wdetj, long long ne,
+                          int nq, double* DFint, double* DFref) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ne * nq) return;
+  const long long q = t / ne, e = t % ne;  // t = q*NE + e
+  const long long P = (long long)nq * ne;
+  double sg[DIM][DIM], ji[DIM][DIM], DF[DIM][DIM];
+#pragma unroll
+  for (int r = 0; r < DIM; ++r)
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+      sg[r][c] = sigma[(r * DIM + c) * P + t];
+      ji[r][c] = jinv[(r * DIM + c) * P + t];
+    }
+  force_point<DIM>(sg, ji, wdetj[t], DF);
+#pragma unroll
+  for (int r = 0; r < DIM; ++r)
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+      DFint[(e * DIM * DIM + r * DIM + c) * nq + q] = DF[r][c];
+      if (DFref) DFref[(r * DIM + c) * P + t] = DF[r][c];
+    }
+}
+
+// ForcePA.apply (operators.py:264-280) / apply_transpose (:282-300), one CTA per element
+struct ForceArgs {
+  const double* in;     // apply: e (NE*nt); apply_t: v (NN, d)
+  const double* DF;     // (NE, d*d, nq)
+  const int* emap;
+  Tables tab;
+  long long ne;
+  double* evec;         // apply: (NE, nl, d)
+  double* out;          // apply_t: (NE*nt)
+};
+
+template <int DIM, int P>
+struct ForceSmem {
+  using D = Disc<DIM, P>;
+  static constexpr int A = cmax(DIM * D::NL, DIM == 3 ? 3 * DIM * D::Q * D::Q * D::D1 : 0);
+  static constexpr int S = 2 * DIM * D::Q * ipow(D::D1, DIM - 1);
+  static constexpr int OUT = DIM * (DIM + 1) * D::NQ;
+  static constexpr int TH = 2 * D::NQ;
+  static constexpr int TOTAL = 2 * D::Q * D::D1 + D::Q * D::DT + A + S + OUT + TH + DIM * D::NL;
+  static constexpr size_t bytes = sizeof(double) * TOTAL;
+};
+
+template <int DIM, int P, int NT, bool TRANS>
+__global__ void __launch_bounds__(NT) k_force(ForceArgs a) {
+  using D = Disc<DIM, P>;
+  using SM = ForceSmem<DIM, P>;
+  constexpr int D1 = D::D1, Q = D::Q, DT = D::DT, NL = D::NL, NQ = D::NQ, NTH = D::NT;
+  extern __shared__ double smem[];
+  double* sB = smem;
+  double* sG = sB + Q * D1;
+  double* sBt = sG + Q * D1;
+  double* rA = sBt + Q * DT;
+  double* rS = rA + SM::A;
+  double* rOut = rS + SM::S;
+  double* rTH = rOut + SM::OUT;
+  double* rF = rTH + SM::TH;
+  const int tid = threadIdx.x;
+  const long long e = blockIdx.x;
+  load_tables<Q, D1, DT>(a.tab, sB, sG, sBt);
+  const double* DFe = a.DF + e * DIM * DIM * NQ;
+  if constexpr (!TRANS) {
+    for (int i = tid; i < NTH; i += NT) rTH[i] = a.in[e * NTH + i];
+    __syncthreads();
+    double* eq = interp<DIM, DT, Q, 1, NT>(sBt, rTH, rTH + NQ, tid);
+    __syncthreads();
+    for (int i = tid; i < DIM * DIM * NQ; i += NT) {
+      const int q = i % NQ, al = i / NQ, c = al / DIM, l = al % DIM;
+      rOut[(c * (DIM + 1) + l) * NQ + q] = DFe[i] * eq[q];
+    }
+    __syncthreads();
+    grad_t<DIM, D1, Q, DIM, (DIM + 1) * NQ, NT>(sB, sG, rOut, rA, rS, rF, tid);
+    __syncthreads();
+    double* ev = a.evec + e * NL * DIM;
+    for (int i = tid; i < NL * DIM; i += NT) {
+      const int l = i / DIM, c = i - l * DIM;
+      ev[i] = rF[c * NL + l];
+    }
+  } else {
+    const int* em = a.emap + e * NL;
+    for (int i = tid; i < NL * DIM; i += NT) {
+      const int l = i / DIM, c = i - l * DIM;
+      rA[c * NL + l] = a.in[(long long)em[l] * DIM + c];
+    }
+    __syncthreads();
+    grad<DIM, D1, Q, DIM, DIM + 1, NT>(sB, sG, rA, rS, rA, rOut, tid);
+    __syncthreads();
+    for (int q = tid; q < NQ; q += NT) {
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < DIM; ++c)
+#pragma unroll
+        for (int l = 0; l < DIM; ++l) s += DFe[(c * DIM + l) * NQ + q] * rOut[(c * (DIM + 1) + l) * NQ + q];
+      rTH[q] = s;
+    }
+    __syncthreads();
+    double* fv = interp_t<DIM, DT, Q, 1, NT>(sBt, rTH, rTH + NQ, tid);
+    __syncthreads();
+    for (int i = tid; i < NTH; i += NT) a.out[e * NTH + i] = fv[i];
+  }
+}
+
+// MassPA.diagonal (operators.py:117-124): contract D with (B*B)^T on every axis
+template <int DIM, int P>
+__global__ void __launch_bounds__(128) k_mass_diag(const double* D, const double* B, long long ne, double* evec) {
+  using Dd = Disc<DIM, P>;
+  constexpr int D1 = Dd::D1, Q = Dd::Q, NL = Dd::NL, NQ = Dd::NQ;
+  __shared__ double sB2[Q * D1];
+  __shared__ double buf[4][2][NQ];
+  for (int i = threadIdx.x; i < Q * D1; i += blockDim.x) sB2[i] = B[i] * B[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long e = (long long)blockIdx.x * 4 + warp;
+  if (e >= ne) return;
+  double* A = buf[warp][0];
+  double* Bf = buf[warp][1];
+  for (int i = lane; i < NQ; i += 32) A[i] = D[e * NQ + i];
+  __syncwarp();
+  double* r = interp_t<DIM, D1, Q, 1, 32>(sB2, A, Bf, lane);
+  __syncwarp();
+  for (int i = lane; i < NL; i += 32) evec[e * NL + i] = r[i];
+}
+
+// per-element thermodynamic mass blocks M_e = Bth^T diag(D) Bth and their inverse
+// (hydro.py:229-232): Gauss-Jordan with partial pivoting, one CTA per element.
+template <int DIM, int P>
+__global__ void __launch_bounds__(128) k_minv(const double* Dm /*(NE,nq)*/, const double* Bt, long long ne,
+                                             double* minv, double* minv_ref) {
+  using Dd = Disc<DIM, P>;
+  constexpr int Q = Dd::Q, DT = Dd::DT, NQ = Dd::NQ, N = Dd::NT;
+  extern __shared__ double smem[];
+  double* M = smem;              // N x 2N augmented
+  double* Bf = M + N * 2 * N;    // full thermo basis (NQ x N)
+  __shared__ int piv;
+  const long long e = blockIdx.x;
+  for (int i = threadIdx.x; i < NQ * N; i += blockDim.x) {
+    const int q = i / N, j = i % N;
+    // x-fastest point and node indices: q = (qz*Q + qy)*Q + qx
+    double b = 1.0;
+    int qq = q, jj = j;
+    for (int d = 0; d < DIM; ++d) {
+      b *= Bt[(qq % Q) * DT + (jj % DT)];
+      qq /= Q;
+      jj /= DT;
+    }
+    Bf[i] = b;
+  }
+  __syncthreads();
+  const double* De = Dm + e * NQ;
+  for (int i = threadIdx.x; i < N * N; i += blockDim.x) {
+    const int r = i / N, c = i % N;
+    double s = 0.0;
+    for (int q = 0; q < NQ; ++q) s += Bf[q * N + r] * De[q] * Bf[q * N + c];
+    M[r * 2 * N + c] = s;
+    M[r * 2 * N + N + c] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int col = 0; col < N; ++col) {
+    if (threadIdx.x == 0) {
+      int best = col;
+      double bv = fabs(M[col * 2 * N + col]);
+      for (int r = col + 1; r < N; ++r) {
+        const double v = fabs(M[r * 2 * N + col]);
+        if (v > bv) {
+          bv = v;
+          best = r;
+        }
+      }
+      piv = best;
+    }
+    __syncthreads();
+    const int pr = piv;
+    if (pr != col)
+      for (int c = threadIdx.x; c < 2 * N; c += blockDim.x) {
+        const double t = M[col * 2 * N + c];
+        M[col * 2 * N + c] = M[pr * 2 * N + c];
+        M[pr * 2 * N + c] = t;
+      }
+    __syncthreads();
+    const double d = M[col * 2 * N + col];
+    __syncthreads();
+    for (int c = threadIdx.x; c < 2 * N; c += blockDim.x) M[col * 2 * N + c] /= d;
+    __syncthreads();
+    for (int i = threadIdx.x; i < N * 2 * N; i += blockDim.x) {
+      const int r = i / (2 * N), c = i % (2 * N);
+      if (r != col) {
+        const double f = M[r * 2 * N + col];
+        if (c != col) M[i] -= f * M[col * 2 * N + c];
+      }
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < N; r += blockDim.x)
+      if (r != col) M[r * 2 * N + col] = 0.0;
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < N * N; i += blockDim.x) {
+    const int r = i / N, c = i % N;
+    const double v = M[r * 2 * N + N + c];
+    minv[e * N * N + i] = v;
+    if (minv_ref) minv_ref[e * N * N + i] = v;
+  }
+}
+
+// solve_energy: out[e,i] = sum_j minv[e,i,j] rhs[e,j]
+__global__ void k_energy_solve(const double* minv, const double* rhs, int nt, long long ne, double* out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ne * nt) return;
+  const long long e = t / nt;
+  const int i = (int)(t % nt);
+  const double* m = minv + (e * nt + i) * nt;
+  const double* r = rhs + e * nt;
+  double s = 0.0;
+  for (int j = 0; j < nt; ++j) s = fma(m[j], r[j], s);
+  out[t] = s;
+}
+
+// internal energy sum_q w_q qdata0 e_q (hydro.py:413-420) per element -> partials
+template <int DIM, int P>
+__global__ void __launch_bounds__(128) k_internal_energy(const double* e_field, const double* qd0 /*(NE,nq)*/,
+                                                        const double* Bt, const double* wnd, long long ne,
+                                                        double* per_elem) {
+  using Dd = Disc<DIM, P>;
+  constexpr int Q = Dd::Q, DT = Dd::DT, NQ = Dd::NQ, NT = Dd::NT;
+  __shared__ double sBt[Q * DT];
+  __shared__ double buf[4][2][NQ];
+  for (int i = threadIdx.x; i < Q * DT; i += blockDim.x) sBt[i] = Bt[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long e = (long long)blockIdx.x * 4 + warp;
+  if (e >= ne) return;
+  double* A = buf[warp][0];
+  for (int i = lane; i < NT; i += 32) A[i] = e_field[e * NT + i];
+  __syncwarp();
+  double* eq = interp<DIM, DT, Q, 1, 32>(sBt, A, buf[warp][1], lane);
+  __syncwarp();
+  double s = 0.0;
+  for (int q = lane; q < NQ; q += 32) s += wnd[q] * qd0[e * NQ + q] * eq[q];
+  s = warp_sum(s);
+  if (lane == 0) per_elem[e] = s;
+}
+
+// fixed-order sum of n values into out[0] (one block)
+__global__ void __launch_bounds__(256) k_sum(const double* v, long long n, double* out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (long long i = threadIdx.x; i < n; i += 256) acc += v[i];
+  const double s = block_sum<256>(acc, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// dot of two vectors, fixed order per thread then block tree
+__global__ void __launch_bounds__(256) k_dot(const double* a, const double* b, long long n, double* out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (long long i = threadIdx.x; i < n; i += 256) acc = fma(a[i], b[i], acc);
+  const double s = block_sum<256>(acc, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+}  // namespace hx

@@ -1,0 +1,191 @@
+"""GPU parity: the sm_100a path through the C-ABI against golden vectors from the
+real reference (tests/golden, made by make_golden.py) and the CPU oracle.
+
+Tolerances: restriction (gather/scatter on identical inputs) bit-exact;
+single operator applies 1e-13 relative (fp64, different summation order than
+numpy/OpenBLAS); CG solutions 1e-10 with the same iteration count; N-step
+states and energies 1e-10 relative (BASELINE.json north star), on configs whose
+reference noise floor (1e-15 input perturbation) is below 1.2e-11.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel
+
+pytestmark = pytest.mark.gpu
+
+CASES = [(d, p) for d in (2, 3) for p in (1, 2, 3, 4)]
+
+
+def _mesh_from(g, d, p):
+    from paper_2112_07075_b200.fespace import HighOrderMesh
+
+    return HighOrderMesh(d, p, g["dofmap"], g["coords"].copy())
+
+
+@pytest.mark.parametrize("d,p", CASES)
+def test_restriction_bitwise(d, p):
+    from paper_2112_07075_b200.fespace import FiniteElementSpace
+
+    g = golden(f"ops_{d}d_p{p}")
+    mesh = _mesh_from(g, d, p)
+    h1 = FiniteElementSpace(mesh, "H1")
+    assert np.array_equal(h1.gather(g["gather_in"]), g["gather_out"])
+    assert np.array_equal(h1.scatter_add(g["scatter_in"]), g["scatter_out"])
+    assert np.array_equal(h1.scatter_add(g["scatter1_in"]), g["scatter1_out"])
+    l2 = FiniteElementSpace(mesh, "L2", order=max(p - 1, 0))
+    v = np.random.default_rng(1).normal(size=l2.ndof)
+    e = l2.gather(v)
+    assert np.array_equal(l2.scatter_add(e), v + 0.0)
+
+
+@pytest.mark.parametrize("d,p", CASES)
+def test_geometry(d, p):
+    from paper_2112_07075_b200.fespace import compute_geometric_factors
+    from paper_2112_07075_b200.tensor_basis import gauss_legendre
+
+    g = golden(f"ops_{d}d_p{p}")
+    geom = compute_geometric_factors(_mesh_from(g, d, p), gauss_legendre(p + 2))
+    assert rel(geom.jac, g["jac"]) < 1e-14
+    assert rel(geom.detj, g["detj"]) < 1e-14
+    assert rel(geom.jinv, g["jinv"]) < 1e-14
+    assert rel(geom.wdetj, g["wdetj"]) < 1e-14
+
+
+@pytest.mark.parametrize("d,p", CASES)
+def test_mass_pa(d, p):
+    from paper_2112_07075_b200.fespace import FiniteElementSpace, compute_geometric_factors
+    from paper_2112_07075_b200.operators import MassPA, cg_solve
+    from paper_2112_07075_b200.tensor_basis import gauss_legendre
+
+    g = golden(f"ops_{d}d_p{p}")
+    mesh = _mesh_from(g, d, p)
+    geom = compute_geometric_factors(mesh, gauss_legendre(p + 2))
+    m = MassPA(FiniteElementSpace(mesh, "H1"), geom, coeff=g["mass_coeff"])
+    assert rel(m.D, g["mass_D"]) < 1e-15
+    assert rel(m.apply(g["mass_u1"]), g["mass_y1"]) < 1e-13
+    assert rel(m.apply(g["mass_u3"]), g["mass_y3"]) < 1e-13
+    assert rel(m.diagonal(), g["mass_diag"]) < 1e-13
+    x, it = cg_solve(m.apply, g["cg_b"], precond_diag=m.diagonal(), rel_tol=1e-8, max_iter=500)
+    assert it == int(g["cg_iters"])
+    assert rel(x, g["cg_x"]) < 1e-10
+
+
+@pytest.mark.parametrize("d,p", CASES)
+def test_force_pa(d, p):
+    from paper_2112_07075_b200.fespace import FiniteElementSpace, compute_geometric_factors
+    from paper_2112_07075_b200.operators import ForcePA
+    from paper_2112_07075_b200.tensor_basis import gauss_legendre
+
+    g = golden(f"ops_{d}d_p{p}")
+    mesh = _mesh_from(g, d, p)
+    geom = compute_geometric_factors(mesh, gauss_legendre(p + 2))
+    kin = FiniteElementSpace(mesh, "H1", vdim=d)
+    thermo = FiniteElementSpace(mesh, "L2", order=max(p - 1, 0))
+    f = ForcePA(kin, thermo, geom, g["force_sigma"])
+    assert rel(f.D, g["force_D"]) < 1e-14
+    assert rel(f.apply(g["force_e"]), g["force_Fe"]) < 1e-13
+    assert rel(f.apply(np.ones(thermo.ndof)), g["force_F1"]) < 1e-13
+    assert rel(f.apply_transpose(g["force_v"]), g["force_Ftv"]) < 1e-13
+    # adjointness (test_operators.py:195-203)
+    e, v = g["force_e"], g["force_v"]
+    assert np.vdot(f.apply(e), v) == pytest.approx(np.vdot(e, f.apply_transpose(v)), rel=1e-12)
+
+
+def _hydro_from(g, d, p):
+    from paper_2112_07075_b200.hydro import LagrangeHydro, MaterialModel, ViscosityModel
+    from paper_2112_07075_b200.tensor_basis import gauss_legendre
+
+    mesh = _mesh_from(g, d, p)
+    return LagrangeHydro(mesh, gauss_legendre(p + 2), MaterialModel(1.4), ViscosityModel(0.5, 2.0),
+                         bc_mask=g["bc_mask"])
+
+
+@pytest.mark.parametrize("d,p", CASES)
+def test_hydro_point_data_and_rates(d, p):
+    from paper_2112_07075_b200.fespace import compute_geometric_factors
+    from paper_2112_07075_b200.hydro import HydroState
+
+    g = golden(f"ops_{d}d_p{p}")
+    hy = _hydro_from(g, d, p)
+    st = HydroState(g["st_x"], g["st_v"], g["st_e"], g["st_qdata0"], 0.0)
+    hy.begin_phase(st)
+    assert rel(hy.mass_pa.D, g["mass_D_phase"]) < 1e-15
+    assert rel(hy._mass_diag, g["mdiag"]) < 1e-13
+    assert rel(hy._m_e_inv, g["minv"]) < 1e-11
+    geom = compute_geometric_factors(hy.mesh, hy.quad, x=st.x)
+    sig, ratio = hy.stress_qdata(st, geom)
+    assert rel(sig, g["stress_sigma"]) < 1e-13
+    assert ratio == pytest.approx(float(g["stress_ratio"]), rel=1e-13)
+    assert hy.clamp_warnings == int(g["stress_clamps"])
+    r = hy.rates(st)
+    assert rel(r.dv, g["rates_dv"]) < 1e-10
+    assert rel(r.de, g["rates_de"]) < 1e-11
+    assert r.min_h_over_speed == pytest.approx(float(g["rates_ratio"]), rel=1e-13)
+    assert r.clamped == int(g["rates_clamped"])
+    assert rel(hy.solve_energy(g["esolve_rhs"]), g["esolve_out"]) < 1e-11
+    assert hy.kinetic_energy(st) == pytest.approx(float(g["ke"]), rel=1e-12)
+    assert hy.internal_energy(st) == pytest.approx(float(g["ie"]), rel=1e-13)
+    assert hy.total_mass(st) == pytest.approx(float(g["mass_total"]), rel=1e-15)
+    new, info = hy.rk2_step(st, 1e-3)
+    assert info["dt"] == 1e-3
+    assert rel(new.x, g["step_x"]) < 1e-12
+    assert rel(new.v, g["step_v"]) < 1e-10
+    assert rel(new.e, g["step_e"]) < 1e-11
+
+
+RUNS = ["sedov2d_q2", "sedov3d_q3", "sedov3d_q2", "triple3d_q3", "tgv3d_q4"]
+
+
+def _problem(z):
+    from paper_2112_07075_b200 import problems
+
+    d = int(z["dim"])
+    prob = str(z["problem"])
+    if prob == "sedov":
+        return problems.sedov(d, tuple(z["extents"]), tuple(int(c) for c in z["counts"]))
+    if prob == "tgv":
+        return problems.taylor_green(d, float(z["gamma"]))
+    return problems.triple_point(d, float(z["gamma"]))
+
+
+@pytest.mark.parametrize("name", RUNS)
+@pytest.mark.parametrize("fused", [False, True])
+def test_nstep_run_matches_reference(name, fused):
+    """N Lagrange steps (timestep_estimate + rk2_step) vs the reference's final state."""
+    from paper_2112_07075_b200.fespace import cartesian_mesh
+    from paper_2112_07075_b200.hydro import (LagrangeHydro, MaterialModel, StepControls, ViscosityModel,
+                                             box_velocity_bc)
+    from paper_2112_07075_b200.tensor_basis import gauss_legendre
+
+    z = golden("run_" + name)
+    d, p = int(z["dim"]), int(z["p"])
+    assert float(z["noise_floor"]) < 1.2e-11
+    mesh = cartesian_mesh(d, tuple(z["extents"]), tuple(int(c) for c in z["counts"]), p)
+    hy = LagrangeHydro(mesh, gauss_legendre(p + 2), MaterialModel(float(z["gamma"])), ViscosityModel(0.5, 2.0),
+                       bc_mask=box_velocity_bc(mesh))
+    rho0, v0, e0 = _problem(z)
+    st = hy.initial_state(rho0, v0, e0)
+    ctl = StepControls(cfl=float(z["cfl"]), dt_max=1.0, t_final=10.0)
+    energies = [hy.total_energy(st)]
+    dts = []
+    if fused:
+        st = hy.to_device(st)
+    for _ in range(int(z["nsteps"])):
+        if fused:
+            st, info = hy.step(st, ctl)
+        else:
+            dt = hy.timestep_estimate(st, ctl)
+            st, info = hy.rk2_step(st, dt)
+        dts.append(info["dt"])
+        energies.append(hy.total_energy(st))
+    st = hy.to_host(st)
+    tol = 1e-10
+    assert rel(st.x, z["x"]) < tol
+    assert rel(st.v, z["v"]) < tol
+    assert rel(st.e, z["e"]) < tol
+    assert rel(dts, z["dts"]) < tol
+    assert abs(energies[-1] - float(z["energies"][-1])) <= tol * abs(float(z["energies"][-1]))
+    assert st.t == pytest.approx(float(z["t"]), rel=1e-12)
+    assert hy.clamp_warnings == int(z["clamps"])
