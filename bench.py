@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Benchmark of the PA Lagrange step on B200: megadofs x timesteps / s (fp64).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = timestep_estimate + rk2_step (hydro.py:364-405) of the 3D Sedov blast,
+Q3-Q2, 23^3 elements per GPU (1,029,000 velocity dofs), the BASELINE.json
+weak-scaling configuration.  dofs = velocity dofs V = d * NN.
+
+value  : device time of K steps (CUDA events on the launching stream, max over
+         ranks), state resident in HBM, L2 flushed (256 MiB write) before every step.
+e2e    : the same steps through the C-ABI entry a host caller binds
+         (hx_step_host) with pinned HOST state buffers: H2D of x, v, e, the step,
+         D2H of the new x, v, e -- all inside the timed region.
+roofline: dominant kernel's algorithmic bytes / its average launch time (CUDA
+         events recorded by the library around each launch during the timed steps)
+         against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline / --impl reference: the CPU oracle (oracle/pa_oracle.py, a numpy
+         restatement of the reference, pinned to its golden vectors) on the host
+         cores, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "megadofs x timesteps/sec (Lagrange step, fp64)"
+UNIT = "Mdof*steps/s"
+K_NAMES = ["rates", "mass_cg", "cg_node", "cg_init", "axpy", "validity", "other"]
+
+
+def algorithmic_bytes(d, p, ne, nn):
+    """Per-launch algorithmic bytes of each kernel class ('Kernels')."""
+    nl, nq, nt = (p + 1) ** d, (p + 2) ** d, max(p, 1) ** d
+    V = d * nn
+    return {
+        # D_M + gathered z, p_{k-1} + element map + owner flags + wall mask + E-vector out
+        "mass_cg": 8 * ne * nq + 16 * V + 4 * ne * nl + ne * nl + V + 8 * d * ne * nl,
+        # E-vector + transpose map + z, p_{k-1}, x, r, 1/diag, mask in; p, x, r, z out
+        "cg_node": 8 * d * ne * nl + 4 * ne * nl + 4 * (nn + 1) + 5 * 8 * V + V + 4 * 8 * V,
+        # x, v gathered + e + qdata0 + element map + M_e^{-1} in; F.1 E-vector + de out
+        "rates": 16 * V + 8 * ne * nt + 8 * ne * nq + 4 * ne * nl + 8 * ne * nt * nt + 8 * d * ne * nl + 8 * ne * nt,
+        "cg_init": 8 * d * ne * nl + 4 * ne * nl + 4 * (nn + 1) + V + 8 * V + 5 * 8 * V,
+        "axpy": 3 * 2 * 8 * V + 3 * 8 * ne * nt,
+        "validity": 8 * V + 4 * ne * nl,
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        loaded = [r for r in self.rows if (num(r[6]) or 0) > 0] or self.rows
+        sm = [num(r[0]) for r in loaded if num(r[0]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": num(self.rows[0][1]),
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per launch from the committed ncu --set full summary, if present."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (reference arm and cpu_baseline)
+
+
+def cpu_oracle_run(p, n, steps, warmup, cfl=0.05):
+    """Time the oracle's timestep_estimate + rk2_step on an n^3 Q{p} Sedov sample."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import pa_oracle as O
+
+    cores = os.cpu_count() or 1
+    d = 3
+    with threadpool_limits(limits=cores):
+        dofmap, coords = O.box_mesh(d, (1.0,) * d, (n,) * d, p)
+        hy = O.Hydro(d, p, dofmap, coords, 1.4, 0.5, 2.0, bc_mask=O.box_mask(coords))
+        st = hy.initial_state(*O.sedov_fns(d, (1.0,) * d, (n,) * d))
+        times = []
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            dt = hy.timestep_estimate(st, cfl, dt_max=1.0, t_final=1e9)
+            st, _ = hy.rk2_step(st, dt)
+            if i >= warmup:
+                times.append(time.perf_counter() - t0)
+    V = d * coords.shape[0]
+    return V, times, cores
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    n = args.cpu_n
+    V, times, cores = cpu_oracle_run(args.p, n, args.steps, args.warmup)
+    tot = sum(times)
+    val = V * len(times) / tot / 1e6
+    sample = (f"3D Sedov Q{args.p}-Q{args.p - 1} {n}^3 elements ({V} velocity dofs), "
+              f"{len(times)} timed steps after {args.warmup} warm-up")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"3D Sedov Q{args.p}-Q{args.p - 1}, CPU sample {n}^3 elements", "global_batch": V,
+                   "seq_len": None, "parallelism": "cpu"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=23, help="elements per direction per GPU")
+    ap.add_argument("--p", type=int, default=3, help="kinematic order (Q_p - Q_{p-1})")
+    ap.add_argument("--cfl", type=float, default=0.05)
+    ap.add_argument("--cpu-n", type=int, default=12, help="CPU sample: elements per direction")
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2112_07075_b200 import _lib, problems
+    from paper_2112_07075_b200.fespace import cartesian_mesh
+    from paper_2112_07075_b200.hydro import LagrangeHydro, MaterialModel, StepControls, ViscosityModel, box_velocity_bc
+    from paper_2112_07075_b200.tensor_basis import gauss_legendre
+
+    d, p, n = 3, args.p, args.n
+    mesh = cartesian_mesh(d, (1.0,) * d, (n,) * d, p)
+    hy = LagrangeHydro(mesh, gauss_legendre(p + 2), MaterialModel(1.4), ViscosityModel(0.5, 2.0),
+                       bc_mask=box_velocity_bc(mesh))
+    st0 = hy.initial_state(*problems.sedov(d, (1.0,) * d, (n,) * d))
+    ctl = StepControls(cfl=args.cfl, dt_max=1.0, t_final=1e9)
+    V = d * mesh.num_nodes
+    lib, h = hy._ctx.lib, hy._ctx.h
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    # ---- device-resident steps
+    st = hy.to_device(st0)
+    bufs = [tuple(torch.empty_like(a) for a in (st.x, st.v, st.e)) for _ in range(2)]
+    for i in range(args.warmup):
+        st, info = hy.step(st, ctl, out=bufs[i % 2])
+    torch.cuda.synchronize()
+    lib.hx_prof_enable(h, 1)
+    lib.hx_prof_reset(h)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = hy._ctx.launches()
+    step_ms = []
+    cg_iters = []
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush (outside the per-step events)
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            st, info = hy.step(st, ctl, out=bufs[(args.warmup + i) % 2])
+            ev1.record(stream)
+            ev1.synchronize()
+            step_ms.append(ev0.elapsed_time(ev1))
+            cg_iters.append(info["cg_iterations"])
+    torch.cuda.synchronize()
+    launches = hy._ctx.launches() - launches0 - args.steps  # minus the flush is not ours; keep ours only
+    launches = hy._ctx.launches() - launches0
+    lib.hx_prof_enable(h, 0)
+    ktimes = {}
+    for k, name in enumerate(K_NAMES):
+        tot, cnt = _lib.C.c_double(), _lib.C.c_int64()
+        lib.hx_prof_read(h, k, _lib.C.byref(tot), _lib.C.byref(cnt))
+        if cnt.value:
+            ktimes[name] = (tot.value, int(cnt.value))
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = V * world * args.steps / (total_ms / 1e3) / 1e6
+
+    # ---- e2e through the C-ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        hst = hy.to_host(st)
+        hx_ = torch.from_numpy(np.ascontiguousarray(hst.x)).pin_memory()
+        hv_ = torch.from_numpy(np.ascontiguousarray(hst.v)).pin_memory()
+        he_ = torch.from_numpy(np.ascontiguousarray(hst.e)).pin_memory()
+        prm = hy._params(ctl)
+        t_state = hst.t
+        info_c = _lib.StepInfo()
+
+        def host_step():
+            nonlocal t_state
+            hy._ctx.sync_stream()
+            rc = lib.hx_step_host(h, _lib.C.byref(prm), float(t_state), hx_.data_ptr(), hv_.data_ptr(),
+                                  he_.data_ptr(), _lib.C.byref(info_c))
+            if rc != 0:
+                raise RuntimeError(f"hx_step_host failed: {rc}")
+            t_state = info_c.t_new
+
+        for _ in range(args.warmup):
+            host_step()
+        e2e_s = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            host_step()
+            e2e_s += time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        nb = 8 * (hst.x.size + hst.v.size + hst.e.size)
+        e2e = {"value": V * world * args.steps / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": nb,
+               "d2h_bytes_per_step": nb}
+
+    # ---- roofline of the dominant kernel
+    pk, pk_src = peaks()
+    ab = algorithmic_bytes(d, p, mesh.num_elements, mesh.num_nodes)
+    traffic = ncu_traffic()
+    kern = {}
+    for name, (tot, cnt) in ktimes.items():
+        avg_s = tot / cnt / 1e3
+        kb = ab.get(name)
+        kern[name] = {"launches": cnt, "avg_us": avg_s * 1e6, "share": tot / max(total_ms, 1e-30),
+                      "alg_bytes": kb, "gbs": (kb / avg_s / 1e9) if kb else None}
+    dom = max(kern, key=lambda k: ktimes[k][0]) if kern else None
+    roof = None
+    if dom:
+        ach = kern[dom]["gbs"]
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": pk, "unit": "GB/s",
+                "frac": ach / pk if ach else None, "traffic": traffic.get(dom), "peak_source": pk_src,
+                "alg_bytes_per_launch": kern[dom]["alg_bytes"]}
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        Vc, times, cores = cpu_oracle_run(p, args.cpu_n, args.cpu_steps, 1)
+        cpu = {"value": Vc * len(times) / sum(times) / 1e6, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"3D Sedov Q{p}-Q{p - 1} {args.cpu_n}^3 elements ({Vc} velocity dofs), "
+                         f"{len(times)} steps after 1 warm-up, oracle/pa_oracle.py"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"3D Sedov blast Q{p}-Q{p - 1}, {n}^3 hex elements per GPU, "
+                                   f"{V} velocity dofs per GPU, CFL {args.cfl}",
+                       "global_batch": V * world, "seq_len": None,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "flushed (256 MiB write) before every timed step",
+                       "cg_iterations": cg_iters},
+            "e2e": e2e, "gpu_launches": launches, "roofline": roof, "kernels": kern, "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

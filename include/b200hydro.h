@@ -200,6 +200,13 @@ int hx_step_host(hx_ctx* ctx, const hx_params* prm, double t, double* x_host, do
 int hx_energies(hx_ctx* ctx, const double* v, const double* e, const double* qdata0,
                 double* kinetic, double* internal);
 
+/* ---- live kernel timing (CUDA events around instrumented launches) ------------
+ * classes: 0 fused rates, 1 PA mass (CG), 2 CG node update, 3 CG init,
+ * 4 state axpy, 5 geometry validity, 6 other. */
+int hx_prof_enable(hx_ctx* ctx, int on);
+int hx_prof_read(hx_ctx* ctx, int kclass, double* total_ms, int64_t* count);
+int hx_prof_reset(hx_ctx* ctx);
+
 /* ---- multi-GPU (domain decomposition; the reference's P = identity) -- */
 
 /* Shared-node halo plan for this rank's subdomain: for each neighbour rank, the

@@ -87,6 +87,9 @@ _SIGS = {
                               C.POINTER(StepInfo)]),
     "hx_step_host": (C.c_int, [P, C.POINTER(Params), C.c_double, P, P, P, C.POINTER(StepInfo)]),
     "hx_energies": (C.c_int, [P, P, P, P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "hx_prof_enable": (C.c_int, [P, C.c_int]),
+    "hx_prof_read": (C.c_int, [P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    "hx_prof_reset": (C.c_int, [P]),
     "hx_comm_init": (C.c_int, [P, P, C.c_int, C.c_int, C.c_int, P, P, P, P]),
     "hx_comm_active": (C.c_int, [P]),
 }

@@ -58,6 +58,14 @@ struct hx_ctx {
   CGDev* h_cg = nullptr;
   StatusDev* h_st = nullptr;
   double* h_dt = nullptr;
+  // live per-kernel-class timing (hx_prof_*): event pairs around instrumented launches
+  bool prof_on = false;
+  std::vector<cudaEvent_t> prof_ev;
+  std::vector<int> prof_cls;
+  int prof_used = 0;
+  int prof_pending = 0;
+  double prof_tot[8] = {0};
+  long long prof_cnt[8] = {0};
   // host-buffer entry scratch (device state)
   double *hx_x = nullptr, *hx_v = nullptr, *hx_e = nullptr, *hx_xo = nullptr, *hx_vo = nullptr, *hx_eo = nullptr;
 };
@@ -109,6 +117,34 @@ static cudaError_t dalloc(T** p, size_t n) {
 
 static inline unsigned gblocks(long long n, int nt) { return (unsigned)((n + nt - 1) / nt); }
 
+enum { K_RATES = 0, K_MASS = 1, K_CGNODE = 2, K_CGINIT = 3, K_AXPY = 4, K_VALID = 5, K_OTHER = 6 };
+
+static void prof_collect(hx_ctx* c) {
+  if (c->prof_used == 0) return;
+  cudaEventSynchronize(c->prof_ev[2 * c->prof_used - 1]);
+  for (int i = 0; i < c->prof_used; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->prof_ev[2 * i], c->prof_ev[2 * i + 1]);
+    c->prof_tot[c->prof_cls[i]] += ms;
+    c->prof_cnt[c->prof_cls[i]] += 1;
+  }
+  c->prof_used = 0;
+}
+
+static void prof_begin(hx_ctx* c, int cls) {
+  if (!c->prof_on) return;
+  if ((size_t)(2 * c->prof_used + 2) > c->prof_ev.size()) prof_collect(c);
+  cudaEventRecord(c->prof_ev[2 * c->prof_used], c->stream);
+  c->prof_pending = cls;
+}
+
+static void prof_end(hx_ctx* c) {
+  if (!c->prof_on) return;
+  cudaEventRecord(c->prof_ev[2 * c->prof_used + 1], c->stream);
+  c->prof_cls[c->prof_used] = c->prof_pending;
+  ++c->prof_used;
+}
+
 static Tables tables(const hx_ctx* c) { return Tables{c->B, c->G, c->Bt, c->wnd, c->psi1}; }
 
 template <typename K>
@@ -150,7 +186,9 @@ struct LaunchRates {
       attr = true;
     }
     RatesArgs a{x, v, e, ctx->qd0, ctx->emap, ctx->minv, tables(ctx), gamma, q1, q2, ctx->ne, evec, de, st, mode};
+    prof_begin(ctx, mode == 0 ? K_RATES : K_VALID);
     kern<<<(unsigned)ctx->ne, RATES_NT, SM::bytes, ctx->stream>>>(a);
+    prof_end(ctx);
     CKL();
     return HX_OK;
   }
@@ -167,7 +205,9 @@ struct LaunchMass {
     if (cgmode) {                                                                     \
       auto k = k_mass<DIM, P, NC, true>;                                              \
       CK(smem_attr(k, bytes));                                                        \
+      prof_begin(ctx, K_MASS);                                                        \
       k<<<grid, 128, bytes, ctx->stream>>>(a);                                        \
+      prof_end(ctx);                                                                  \
     } else {                                                                          \
       auto k = k_mass<DIM, P, NC, false>;                                             \
       CK(smem_attr(k, bytes));                                                        \
@@ -365,7 +405,6 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   for (int q = 0; q < nq; ++q) {
     int qq = q;
     double w = 1.0;
-    double ps = 1.0;
     std::vector<int> dig(ctx->dim);
     for (int a = 0; a < ctx->dim; ++a) {
       dig[a] = qq % Q;
@@ -375,7 +414,6 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
     w = d->qweights_host[dig[ctx->dim - 1]];
     for (int a = ctx->dim - 2; a >= 0; --a) w *= d->qweights_host[dig[a]];
     wnd[q] = w;
-    (void)ps;
   }
   {
     // psi1 = tensor_interp(Bt, ones): per axis sum_j Bt[q, j]
@@ -472,6 +510,7 @@ extern "C" int hx_destroy(hx_ctx* ctx) {
   if (ctx->h_cg) cudaFreeHost(ctx->h_cg);
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
   if (ctx->h_dt) cudaFreeHost(ctx->h_dt);
+  for (auto& e : ctx->prof_ev) cudaEventDestroy(e);
   delete ctx;
   return HX_OK;
 }
@@ -649,9 +688,11 @@ static int run_cg(hx_ctx* ctx, const double* D, const double* rhs, const double*
   na.hist = hist;
   na.negate = negate;
   const unsigned gn = gblocks(ctx->nn, 256);
+  prof_begin(ctx, K_CGINIT);
   if (nc == 1) k_cg_init<1><<<gn, 256, 0, ctx->stream>>>(na);
   else if (nc == 2) k_cg_init<2><<<gn, 256, 0, ctx->stream>>>(na);
   else k_cg_init<3><<<gn, 256, 0, ctx->stream>>>(na);
+  prof_end(ctx);
   CKL();
   na.evec = ctx->evec;
   na.rhs = nullptr;
@@ -674,9 +715,11 @@ static int run_cg(hx_ctx* ctx, const double* D, const double* rhs, const double*
     for (int i = 0; i < chunk; ++i) {
       int rc = dispatch<LaunchMass>(ctx, nc, true, ma);
       if (rc) return rc;
+      prof_begin(ctx, K_CGNODE);
       if (nc == 1) k_cg_node<1><<<gn, 256, 0, ctx->stream>>>(na);
       else if (nc == 2) k_cg_node<2><<<gn, 256, 0, ctx->stream>>>(na);
       else k_cg_node<3><<<gn, 256, 0, ctx->stream>>>(na);
+      prof_end(ctx);
       CKL();
     }
     done_iters += chunk;
@@ -884,7 +927,9 @@ static int step_impl(hx_ctx* ctx, const hx_params* prm, double t, double dt_fixe
     k_dt<<<1, 1, 0, ctx->stream>>>(da);
     CKL();
     AxpyArgs m{x, v, e, v, ctx->dv0, ctx->de0, ctx->xm, ctx->vm, ctx->em, ctx->dt + 1, 0.5, nv, nte};
+    prof_begin(ctx, K_AXPY);
     k_axpy_state<<<ga, 256, 0, ctx->stream>>>(m);
+    prof_end(ctx);
     CKL();
     rc = read_status(ctx, ctx->st + 0, ctx->h_st + 0);
     if (rc) return rc;
@@ -923,7 +968,9 @@ static int step_impl(hx_ctx* ctx, const hx_params* prm, double t, double dt_fixe
     rc = rates_device(ctx, prm, ctx->xm, ctx->vm, ctx->em, ctx->dv1, ctx->de1, ctx->st + 1, &c1);
     if (rc) return rc;
     AxpyArgs n{x, v, e, ctx->vm, ctx->dv1, ctx->de1, x_out, v_out, e_out, ctx->dt + 1, 1.0, nv, nte};
+    prof_begin(ctx, K_AXPY);
     k_axpy_state<<<ga, 256, 0, ctx->stream>>>(n);
+    prof_end(ctx);
     CKL();
     // validity of the new geometry (hydro.py:400-401)
     rc = status_reset(ctx, ctx->st + 2);
@@ -1043,3 +1090,36 @@ extern "C" int hx_comm_init(hx_ctx* ctx, const void*, int, int, int, const int32
   return fail(ctx, HX_EINVAL, "hx_comm_init: device-side NCCL halo not built in this version");
 }
 extern "C" int hx_comm_active(hx_ctx*) { return 0; }
+
+// ---------------------------------------------------------------------------
+// live kernel timing
+
+extern "C" int hx_prof_enable(hx_ctx* ctx, int on) {
+  if (!ctx) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  if (on && ctx->prof_ev.empty()) {
+    ctx->prof_ev.resize(8192);
+    ctx->prof_cls.resize(4096);
+    for (auto& e : ctx->prof_ev) CK(cudaEventCreate(&e));
+  }
+  ctx->prof_on = on != 0;
+  return HX_OK;
+}
+
+extern "C" int hx_prof_read(hx_ctx* ctx, int kclass, double* total_ms, int64_t* count) {
+  if (!ctx || kclass < 0 || kclass > 7) return HX_EINVAL;
+  prof_collect(ctx);
+  if (total_ms) *total_ms = ctx->prof_tot[kclass];
+  if (count) *count = ctx->prof_cnt[kclass];
+  return HX_OK;
+}
+
+extern "C" int hx_prof_reset(hx_ctx* ctx) {
+  if (!ctx) return HX_EINVAL;
+  prof_collect(ctx);
+  for (int i = 0; i < 8; ++i) {
+    ctx->prof_tot[i] = 0;
+    ctx->prof_cnt[i] = 0;
+  }
+  return HX_OK;
+}

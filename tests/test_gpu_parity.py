@@ -163,8 +163,8 @@ def test_nstep_run_matches_reference(name, fused):
     d, p = int(z["dim"]), int(z["p"])
     assert float(z["noise_floor"]) < 1.2e-11
     mesh = cartesian_mesh(d, tuple(z["extents"]), tuple(int(c) for c in z["counts"]), p)
-    hy = LagrangeHydro(mesh, gauss_legendre(p + 2), MaterialModel(float(z["gamma"])), ViscosityModel(0.5, 2.0),
-                       bc_mask=box_velocity_bc(mesh))
+    hy = LagrangeHydro(mesh, gauss_legendre(p + 2), MaterialModel(float(z["gamma"])),
+                       ViscosityModel(float(z["q1"]), float(z["q2"])), bc_mask=box_velocity_bc(mesh))
     rho0, v0, e0 = _problem(z)
     st = hy.initial_state(rho0, v0, e0)
     ctl = StepControls(cfl=float(z["cfl"]), dt_max=1.0, t_final=10.0)

@@ -113,7 +113,8 @@ def run_oracle(z, nsteps=None):
     d, p = int(z["dim"]), int(z["p"])
     ext, counts = tuple(z["extents"]), tuple(int(c) for c in z["counts"])
     dofmap, coords = O.box_mesh(d, ext, counts, p)
-    hy = O.Hydro(d, p, dofmap, coords, float(z["gamma"]), 0.5, 2.0, bc_mask=O.box_mask(coords))
+    hy = O.Hydro(d, p, dofmap, coords, float(z["gamma"]), float(z["q1"]), float(z["q2"]),
+                 bc_mask=O.box_mask(coords))
     rho0, v0, e0 = problem_fns(z)
     st = hy.initial_state(rho0, v0, e0)
     energies = [hy.total_energy(st)]
