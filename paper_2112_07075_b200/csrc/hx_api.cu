@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -29,7 +30,7 @@ struct hx_ctx {
   // tables
   double *B = nullptr, *G = nullptr, *Bt = nullptr, *wnd = nullptr, *psi1 = nullptr;
   // restriction
-  int *emap = nullptr, *off = nullptr, *idx = nullptr;
+  int *emap = nullptr, *off = nullptr, *idx = nullptr, *slot = nullptr;
   uint8_t* own = nullptr;
   // workspaces
   double* evec = nullptr;     // (NE, nl, d)
@@ -38,7 +39,7 @@ struct hx_ctx {
   double* partials = nullptr; // reduction partials
   double* hist = nullptr;     // CG residual history
   int hist_len = 0;
-  CGDev* cg = nullptr;
+  CGDev* cg = nullptr;        // [2]: stage-1 and stage-2 momentum solves
   StatusDev* st = nullptr;    // [4]: S, mid, new, scratch
   double* dt = nullptr;       // [2]
   double* scal = nullptr;     // small scalars
@@ -66,6 +67,18 @@ struct hx_ctx {
   int prof_pending = 0;
   double prof_tot[8] = {0};
   long long prof_cnt[8] = {0};
+  // CUDA-graph step path (one graph per buffer/parameter set)
+  struct StepGraph {
+    const void* key[6];
+    double dt_fixed;
+    hx_params prm;
+    int seen = 0;
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::vector<StepGraph> graphs;
+  cudaStream_t gstream = nullptr, gstream2 = nullptr;
+  double* t_dev = nullptr;
+  double* h_t = nullptr;
   // host-buffer entry scratch (device state)
   double *hx_x = nullptr, *hx_v = nullptr, *hx_e = nullptr, *hx_xo = nullptr, *hx_vo = nullptr, *hx_eo = nullptr;
 };
@@ -145,6 +158,17 @@ static void prof_end(hx_ctx* c) {
   ++c->prof_used;
 }
 
+// resident-capacity grid for persistent kernels (SMs x max resident blocks)
+template <typename K>
+static unsigned persistent_grid(K kernel, int threads, size_t smem, long long work_blocks) {
+  static int sms = 0;
+  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+  long long g = (long long)std::max(per, 1) * sms;
+  return (unsigned)std::max<long long>(1, std::min<long long>(g, work_blocks));
+}
+
 static Tables tables(const hx_ctx* c) { return Tables{c->B, c->G, c->Bt, c->wnd, c->psi1}; }
 
 template <typename K>
@@ -185,7 +209,7 @@ struct LaunchRates {
       CK(smem_attr(kern, SM::bytes));
       attr = true;
     }
-    RatesArgs a{x, v, e, ctx->qd0, ctx->emap, ctx->minv, tables(ctx), gamma, q1, q2, ctx->ne, evec, de, st, mode};
+    RatesArgs a{x, v, e, ctx->qd0, ctx->emap, ctx->slot, ctx->minv, tables(ctx), gamma, q1, q2, ctx->ne, evec, de, st, mode};
     prof_begin(ctx, mode == 0 ? K_RATES : K_VALID);
     kern<<<(unsigned)ctx->ne, RATES_NT, SM::bytes, ctx->stream>>>(a);
     prof_end(ctx);
@@ -194,10 +218,77 @@ struct LaunchRates {
   }
 };
 
+template <int P, int NC, int MINB>
+static int launch_mass3w_b(hx_ctx* ctx, bool cgmode, const MassArgs& a) {
+  using M = Mass3W<P, NC>;
+  if (cgmode) {
+    auto k = k_mass3w<P, NC, true, MINB>;
+    CK(smem_attr(k, M::bytes));
+    static unsigned grid = 0;
+    if (!grid) grid = persistent_grid(k, 32 * M::WPB, M::bytes, 1ll << 40);
+    prof_begin(ctx, K_MASS);
+    k<<<std::min<unsigned>(grid, gblocks(ctx->ne, M::WPB)), 32 * M::WPB, M::bytes, ctx->stream>>>(a);
+    prof_end(ctx);
+  } else {
+    auto k = k_mass3w<P, NC, false, MINB>;
+    CK(smem_attr(k, M::bytes));
+    static unsigned grid = 0;
+    if (!grid) grid = persistent_grid(k, 32 * M::WPB, M::bytes, 1ll << 40);
+    k<<<std::min<unsigned>(grid, gblocks(ctx->ne, M::WPB)), 32 * M::WPB, M::bytes, ctx->stream>>>(a);
+  }
+  CKL();
+  return HX_OK;
+}
+
+static int g_mass_minb = -1;  // HX_MASS_MINB: resident-block target of k_mass3w (register cap)
+
+template <int P, int NC>
+static int launch_mass3w(hx_ctx* ctx, bool cgmode, const MassArgs& a) {
+  if (g_mass_minb < 0) {
+    const char* v = getenv("HX_MASS_MINB");
+    g_mass_minb = v ? atoi(v) : 4;
+  }
+  if (g_mass_minb >= 5 && P <= 3) return launch_mass3w_b<P, NC, 5>(ctx, cgmode, a);
+  if (g_mass_minb <= 3 || P >= 4) return launch_mass3w_b<P, NC, 3>(ctx, cgmode, a);
+  return launch_mass3w_b<P, NC, 4>(ctx, cgmode, a);
+}
+
+static int g_mass_variant = -1;  // HX_MASS_KERNEL=column|line (default line)
+
+template <int P, int NC>
+static int launch_mass3d(hx_ctx* ctx, bool cgmode, const MassArgs& a) {
+  if (g_mass_variant < 0) {
+    const char* v = getenv("HX_MASS_KERNEL");
+    g_mass_variant = (v && strcmp(v, "column") == 0) ? 0 : 1;
+  }
+  if (g_mass_variant == 1) return launch_mass3w<P, NC>(ctx, cgmode, a);
+  constexpr int Q = P + 2, D1 = P + 1, EPB = 128 / (Q * Q);
+  const size_t bytes = sizeof(double) * EPB * NC * (D1 * D1 * D1 + D1 * D1 * Q + D1 * Q * Q);
+  const unsigned grid = gblocks(ctx->ne, EPB);
+  if (cgmode) {
+    auto k = k_mass3d<P, NC, true>;
+    CK(smem_attr(k, bytes));
+    prof_begin(ctx, K_MASS);
+    k<<<grid, 128, bytes, ctx->stream>>>(a);
+    prof_end(ctx);
+  } else {
+    auto k = k_mass3d<P, NC, false>;
+    CK(smem_attr(k, bytes));
+    k<<<grid, 128, bytes, ctx->stream>>>(a);
+  }
+  CKL();
+  return HX_OK;
+}
+
 template <int DIM, int P>
 struct LaunchMass {
   static int run(hx_ctx* ctx, int nc, bool cgmode, const MassArgs& a) {
     using D = Disc<DIM, P>;
+    if constexpr (DIM == 3) {
+      if (nc == 1) return launch_mass3d<P, 1>(ctx, cgmode, a);
+      if (nc == 2) return launch_mass3d<P, 2>(ctx, cgmode, a);
+      if (nc == 3) return launch_mass3d<P, 3>(ctx, cgmode, a);
+    }
     const unsigned grid = gblocks(ctx->ne, 4);
     const size_t bytes = sizeof(double) * (D::Q * D::D1 + 4 * 2 * nc * D::NQ);
 #define HX_MASS_CASE(NC)                                                              \
@@ -227,7 +318,7 @@ struct LaunchMass {
 template <int DIM, int P>
 struct LaunchMassDiag {
   static int run(hx_ctx* ctx, const double* D, double* evec) {
-    k_mass_diag<DIM, P><<<gblocks(ctx->ne, 4), 128, 0, ctx->stream>>>(D, ctx->B, ctx->ne, evec);
+    k_mass_diag<DIM, P><<<gblocks(ctx->ne, 4), 128, 0, ctx->stream>>>(D, ctx->B, ctx->slot, ctx->ne, evec);
     CKL();
     return HX_OK;
   }
@@ -314,13 +405,9 @@ static int launch_scatter(hx_ctx* ctx, const double* evec, int nc, double* out) 
   return HX_OK;
 }
 
-static int status_reset(hx_ctx* ctx, StatusDev* st) {
-  StatusDev h;
-  h.inv_key = ~0ull;
-  h.clamps = 0;
-  h.min_ratio = __builtin_inf();
-  h.pad = 0;
-  CK(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, ctx->stream));
+static int status_reset(hx_ctx* ctx, StatusDev* st, int n = 1) {
+  k_status_reset<<<1, 32, 0, ctx->stream>>>(st, n);
+  CKL();
   return HX_OK;
 }
 
@@ -394,10 +481,12 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   std::vector<int> fill(off.begin(), off.end() - 1);
   std::vector<int> idx((size_t)ne * nl);
   std::vector<uint8_t> own((size_t)ne * nl, 0);
+  std::vector<int> slot((size_t)ne * nl);
   for (long long e = 0; e < ne; ++e)  // ascending element => deterministic accumulation order
     for (int l = 0; l < nl; ++l) {
       const int n = emap[e * nl + l];
       if (fill[n] == off[n]) own[e * nl + l] = 1;
+      slot[e * nl + l] = fill[n];
       idx[fill[n]++] = (int)(e * nl + l);
     }
   // tables: tensor weights (x fastest) and the thermodynamic interpolant of 1
@@ -445,14 +534,19 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   ok &= dalloc(&ctx->off, nn + 1) == cudaSuccess;
   ok &= dalloc(&ctx->idx, (size_t)ne * nl) == cudaSuccess;
   ok &= dalloc(&ctx->own, (size_t)ne * nl) == cudaSuccess;
+  ok &= dalloc(&ctx->slot, (size_t)ne * nl) == cudaSuccess;
   ok &= dalloc(&ctx->evec, (size_t)ne * nl * dd) == cudaSuccess;
   ok &= dalloc(&ctx->evec2, (size_t)ne * std::max(nl * dd, nq)) == cudaSuccess;
   ok &= dalloc(&ctx->r, nv) == cudaSuccess;
   ok &= dalloc(&ctx->z, nv) == cudaSuccess;
   ok &= dalloc(&ctx->p0, nv) == cudaSuccess;
   ok &= dalloc(&ctx->p1, nv) == cudaSuccess;
-  ok &= dalloc(&ctx->partials, 2 * (size_t)std::max<long long>(gblocks(nn, 256), gblocks(ne, 4)) + 64) == cudaSuccess;
-  ok &= dalloc(&ctx->cg, 1) == cudaSuccess;
+  ok &= dalloc(&ctx->partials, 2 * (size_t)std::max<long long>(gblocks(3 * nn, 256), gblocks(ne, 1)) + 64) == cudaSuccess;
+  ok &= dalloc(&ctx->cg, 2) == cudaSuccess;
+  ok &= dalloc(&ctx->t_dev, 1) == cudaSuccess;
+  ok &= cudaMallocHost((void**)&ctx->h_t, sizeof(double)) == cudaSuccess;
+  ok &= cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking) == cudaSuccess;
+  ok &= cudaStreamCreateWithFlags(&ctx->gstream2, cudaStreamNonBlocking) == cudaSuccess;
   ok &= dalloc(&ctx->st, 4) == cudaSuccess;
   ok &= dalloc(&ctx->dt, 2) == cudaSuccess;
   ok &= dalloc(&ctx->scal, 16) == cudaSuccess;
@@ -469,7 +563,7 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   ok &= dalloc(&ctx->dv1, nv) == cudaSuccess;
   ok &= dalloc(&ctx->de0, (size_t)ne * ctx->nt) == cudaSuccess;
   ok &= dalloc(&ctx->de1, (size_t)ne * ctx->nt) == cudaSuccess;
-  ok &= cudaMallocHost((void**)&ctx->h_cg, sizeof(CGDev)) == cudaSuccess;
+  ok &= cudaMallocHost((void**)&ctx->h_cg, 2 * sizeof(CGDev)) == cudaSuccess;
   ok &= cudaMallocHost((void**)&ctx->h_st, 4 * sizeof(StatusDev)) == cudaSuccess;
   ok &= cudaMallocHost((void**)&ctx->h_dt, 2 * sizeof(double)) == cudaSuccess;
   if (!ok) {
@@ -486,8 +580,25 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   ok &= cudaMemcpy(ctx->off, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice) == cudaSuccess;
   ok &= cudaMemcpy(ctx->idx, idx.data(), sizeof(int) * idx.size(), cudaMemcpyHostToDevice) == cudaSuccess;
   ok &= cudaMemcpy(ctx->own, own.data(), own.size(), cudaMemcpyHostToDevice) == cudaSuccess;
-  ok &= cudaMemset(ctx->cg, 0, sizeof(CGDev)) == cudaSuccess;
+  ok &= cudaMemcpy(ctx->slot, slot.data(), sizeof(int) * slot.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemset(ctx->cg, 0, 2 * sizeof(CGDev)) == cudaSuccess;
   ok &= cudaMemset(ctx->mask, 0, nv) == cudaSuccess;
+  {
+    // fixed per-order tables in the constant bank (k_mass3d); all contexts of one
+    // order must agree on them
+    static std::vector<double> seen[4];
+    std::vector<double> tb(d->B_host, d->B_host + Q * D1);
+    if (!seen[ctx->p - 1].empty() && seen[ctx->p - 1] != tb) {
+      int rc = fail(ctx, HX_EINVAL, "basis tables for order %d differ from an existing context", ctx->p);
+      hx_destroy(ctx);
+      return rc;
+    }
+    seen[ctx->p - 1] = tb;
+    ok &= cudaMemcpyToSymbol(c_B, tb.data(), sizeof(double) * tb.size(), sizeof(double) * 30 * (ctx->p - 1)) ==
+          cudaSuccess;
+    ok &= cudaMemcpyToSymbol(c_G, d->G_host, sizeof(double) * Q * D1, sizeof(double) * 30 * (ctx->p - 1)) ==
+          cudaSuccess;
+  }
   if (!ok) {
     int rc = fail(ctx, HX_ECUDA, "device upload failed");
     hx_destroy(ctx);
@@ -501,7 +612,7 @@ extern "C" int hx_destroy(hx_ctx* ctx) {
   if (!ctx) return HX_OK;
   cudaSetDevice(ctx->device);
   void* dev[] = {ctx->B,  ctx->G,    ctx->Bt,   ctx->wnd,  ctx->psi1, ctx->emap, ctx->off,   ctx->idx,
-                 ctx->own, ctx->evec, ctx->evec2, ctx->r,   ctx->z,    ctx->p0,   ctx->p1,    ctx->partials,
+                 ctx->own, ctx->slot, ctx->evec, ctx->evec2, ctx->r,   ctx->z,    ctx->p0,   ctx->p1,    ctx->partials,
                  ctx->hist, ctx->cg,  ctx->st,   ctx->dt,   ctx->scal, ctx->Dm,   ctx->qd0,   ctx->minv,
                  ctx->mdiag, ctx->invd, ctx->mask, ctx->xm, ctx->vm,   ctx->em,   ctx->dv0,   ctx->dv1,
                  ctx->de0, ctx->de1, ctx->hx_x, ctx->hx_v, ctx->hx_e, ctx->hx_xo, ctx->hx_vo, ctx->hx_eo};
@@ -510,6 +621,12 @@ extern "C" int hx_destroy(hx_ctx* ctx) {
   if (ctx->h_cg) cudaFreeHost(ctx->h_cg);
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
   if (ctx->h_dt) cudaFreeHost(ctx->h_dt);
+  if (ctx->h_t) cudaFreeHost(ctx->h_t);
+  if (ctx->t_dev) cudaFree(ctx->t_dev);
+  for (auto& g : ctx->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
+  if (ctx->gstream2) cudaStreamDestroy(ctx->gstream2);
   for (auto& e : ctx->prof_ev) cudaEventDestroy(e);
   delete ctx;
   return HX_OK;
@@ -626,6 +743,7 @@ static int mass_evec(hx_ctx* ctx, const double* D, const double* x, int nc, doub
   a.x = x;
   a.D = D;
   a.emap = ctx->emap;
+  a.slot = ctx->slot;
   a.B = ctx->B;
   a.ne = ctx->ne;
   a.evec = evec;
@@ -651,12 +769,21 @@ extern "C" int hx_mass_diagonal(hx_mass* m, double* diag) {
   return launch_scatter(ctx, ctx->evec2, 1, diag);
 }
 
-// Device CG on the PA mass: init + chunks of (mass, node) iterations.  The stop
-// test runs on device (k_cg_node's last block); the host polls a pinned copy of the
-// CG state once per chunk and launches no-op-guarded kernels past convergence.
-static int run_cg(hx_ctx* ctx, const double* D, const double* rhs, const double* evec_rhs, int negate,
-                  const uint8_t* mask, const double* invd, double rel_tol, int max_iter, double* x, int nc,
-                  double* hist, hx_cg_info* info) {
+// Device CG on the PA mass.  k_cg_init, then iterations of (k_mass*, k_cg_node);
+// the stop test runs on the device (k_cg_node's last block).  Outside a graph the
+// host polls a pinned copy of the CG state once per chunk of iterations (kernels
+// past convergence exit at once); inside a graph the iterations sit in a
+// conditional WHILE node driven by the same flag (cudaGraphSetConditional).
+struct CGLaunch {
+  NodeArgs na;
+  MassArgs ma;
+  unsigned gn, gnc;
+  int nc;
+};
+
+static int cg_prepare(hx_ctx* ctx, CGDev* cg, const double* D, const double* rhs, const double* evec_rhs, int negate,
+                      const uint8_t* mask, const double* invd, double rel_tol, int max_iter, double* x, int nc,
+                      double* hist, CGLaunch& L) {
   if (hist == nullptr) {
     if (ctx->hist_len < max_iter + 1) {
       if (ctx->hist) cudaFree(ctx->hist);
@@ -666,11 +793,8 @@ static int run_cg(hx_ctx* ctx, const double* D, const double* rhs, const double*
     }
     hist = ctx->hist;
   }
-  CGDev h{};
-  h.tol = rel_tol;
-  h.max_iter = max_iter;
-  CK(cudaMemcpyAsync(ctx->cg, &h, sizeof h, cudaMemcpyHostToDevice, ctx->stream));
-  NodeArgs na{};
+  NodeArgs& na = L.na;
+  na = NodeArgs{};
   na.off = ctx->off;
   na.idx = ctx->idx;
   na.evec = evec_rhs ? evec_rhs : ctx->evec;
@@ -683,20 +807,14 @@ static int run_cg(hx_ctx* ctx, const double* D, const double* rhs, const double*
   na.pbuf1 = ctx->p1;
   na.rhs = rhs;
   na.nn = ctx->nn;
-  na.cg = ctx->cg;
+  na.cg = cg;
   na.partials = ctx->partials;
   na.hist = hist;
   na.negate = negate;
-  const unsigned gn = gblocks(ctx->nn, 256);
-  prof_begin(ctx, K_CGINIT);
-  if (nc == 1) k_cg_init<1><<<gn, 256, 0, ctx->stream>>>(na);
-  else if (nc == 2) k_cg_init<2><<<gn, 256, 0, ctx->stream>>>(na);
-  else k_cg_init<3><<<gn, 256, 0, ctx->stream>>>(na);
-  prof_end(ctx);
-  CKL();
-  na.evec = ctx->evec;
-  na.rhs = nullptr;
-  MassArgs ma{};
+  na.tol = rel_tol;
+  na.max_iter = max_iter;
+  MassArgs& ma = L.ma;
+  ma = MassArgs{};
   ma.x = ctx->z;
   ma.pbuf0 = ctx->p0;
   ma.pbuf1 = ctx->p1;
@@ -704,37 +822,119 @@ static int run_cg(hx_ctx* ctx, const double* D, const double* rhs, const double*
   ma.own = ctx->own;
   ma.D = D;
   ma.emap = ctx->emap;
+  ma.slot = ctx->slot;
   ma.B = ctx->B;
   ma.ne = ctx->ne;
   ma.evec = ctx->evec;
-  ma.cg = ctx->cg;
+  ma.cg = cg;
   ma.partials = ctx->partials;
+  L.nc = nc;
+  static unsigned cap_node[4] = {0, 0, 0, 0}, cap_init[4] = {0, 0, 0, 0};
+  if (!cap_node[nc]) {
+    if (nc == 1) {
+      cap_node[nc] = persistent_grid(k_cg_node<1>, 256, 0, 1ll << 40);
+      cap_init[nc] = persistent_grid(k_cg_init<1>, 256, 0, 1ll << 40);
+    } else if (nc == 2) {
+      cap_node[nc] = persistent_grid(k_cg_node<2>, 256, 0, 1ll << 40);
+      cap_init[nc] = persistent_grid(k_cg_init<2>, 256, 0, 1ll << 40);
+    } else {
+      cap_node[nc] = persistent_grid(k_cg_node<3>, 256, 0, 1ll << 40);
+      cap_init[nc] = persistent_grid(k_cg_init<3>, 256, 0, 1ll << 40);
+    }
+  }
+  L.gnc = std::min(gblocks(ctx->nn * nc, 256), cap_node[nc]);
+  L.gn = std::min(gblocks(ctx->nn * nc, 256), cap_init[nc]);
+  return HX_OK;
+}
+
+static int cg_launch_init(hx_ctx* ctx, CGLaunch& L) {
+  prof_begin(ctx, K_CGINIT);
+  if (L.nc == 1) k_cg_init<1><<<L.gn, 256, 0, ctx->stream>>>(L.na);
+  else if (L.nc == 2) k_cg_init<2><<<L.gn, 256, 0, ctx->stream>>>(L.na);
+  else k_cg_init<3><<<L.gn, 256, 0, ctx->stream>>>(L.na);
+  prof_end(ctx);
+  CKL();
+  L.na.evec = ctx->evec;
+  L.na.rhs = nullptr;
+  return HX_OK;
+}
+
+static int cg_launch_iter(hx_ctx* ctx, CGLaunch& L) {
+  int rc = dispatch<LaunchMass>(ctx, L.nc, true, L.ma);
+  if (rc) return rc;
+  prof_begin(ctx, K_CGNODE);
+  if (L.nc == 1) k_cg_node<1><<<L.gnc, 256, 0, ctx->stream>>>(L.na);
+  else if (L.nc == 2) k_cg_node<2><<<L.gnc, 256, 0, ctx->stream>>>(L.na);
+  else k_cg_node<3><<<L.gnc, 256, 0, ctx->stream>>>(L.na);
+  prof_end(ctx);
+  CKL();
+  return HX_OK;
+}
+
+static void cg_info_from(const CGDev& g, hx_cg_info* info) {
+  if (!info) return;
+  info->code = g.code == 0 ? HX_OK : (g.code == 3 ? HX_ECG_BREAKDOWN : HX_ECG_MAXITER);
+  info->iterations = g.iters;
+  info->n_residuals = g.nres;
+}
+
+static int run_cg(hx_ctx* ctx, const double* D, const double* rhs, const double* evec_rhs, int negate,
+                  const uint8_t* mask, const double* invd, double rel_tol, int max_iter, double* x, int nc,
+                  double* hist, hx_cg_info* info, CGDev* cg = nullptr) {
+  if (!cg) cg = ctx->cg;
+  CGLaunch L;
+  int rc = cg_prepare(ctx, cg, D, rhs, evec_rhs, negate, mask, invd, rel_tol, max_iter, x, nc, hist, L);
+  if (rc) return rc;
+  rc = cg_launch_init(ctx, L);
+  if (rc) return rc;
   int done_iters = 0;
   int chunk = 8;
   while (true) {
     for (int i = 0; i < chunk; ++i) {
-      int rc = dispatch<LaunchMass>(ctx, nc, true, ma);
+      rc = cg_launch_iter(ctx, L);
       if (rc) return rc;
-      prof_begin(ctx, K_CGNODE);
-      if (nc == 1) k_cg_node<1><<<gn, 256, 0, ctx->stream>>>(na);
-      else if (nc == 2) k_cg_node<2><<<gn, 256, 0, ctx->stream>>>(na);
-      else k_cg_node<3><<<gn, 256, 0, ctx->stream>>>(na);
-      prof_end(ctx);
-      CKL();
     }
     done_iters += chunk;
-    CK(cudaMemcpyAsync(ctx->h_cg, ctx->cg, sizeof(CGDev), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_cg, cg, sizeof(CGDev), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (!ctx->h_cg->active) break;
     if (done_iters > max_iter + 1) break;
     chunk = std::min(chunk * 2, 64);
   }
-  const CGDev& g = *ctx->h_cg;
-  if (info) {
-    info->code = g.code == 0 ? HX_OK : (g.code == 3 ? HX_ECG_BREAKDOWN : HX_ECG_MAXITER);
-    info->iterations = g.iters;
-    info->n_residuals = g.nres;
-  }
+  cg_info_from(*ctx->h_cg, info);
+  return HX_OK;
+}
+
+// capture the CG of one stage into the graph being captured on ctx->stream
+static int cg_capture(hx_ctx* ctx, CGLaunch& L) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CK(cudaStreamGetCaptureInfo(ctx->stream, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  L.na.cond = (unsigned long long)h;
+  L.na.use_cond = 1;
+  int rc = cg_launch_init(ctx, L);
+  if (rc) return rc;
+  CK(cudaStreamGetCaptureInfo(ctx->stream, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, deps, nd, &p));
+  CK(cudaStreamUpdateCaptureDependencies(ctx->stream, &node, 1, cudaStreamSetCaptureDependencies));
+  cudaGraph_t body = p.conditional.phGraph_out[0];
+  cudaStream_t outer = ctx->stream;
+  CK(cudaStreamBeginCaptureToGraph(ctx->gstream2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  ctx->stream = ctx->gstream2;
+  rc = cg_launch_iter(ctx, L);
+  ctx->stream = outer;
+  if (rc) return rc;
+  CK(cudaStreamEndCapture(ctx->gstream2, &body));
   return HX_OK;
 }
 
@@ -756,7 +956,7 @@ extern "C" int hx_mass_cg(hx_mass* m, const double* rhs, int ncomp, const uint8_
   k_recip<<<gblocks(nv, 256), 256, 0, ctx->stream>>>(precond_diag, nv, invd);
   CKL();
   hx_cg_info ci{};
-  int rc = run_cg(ctx, m->D, rhs, nullptr, 0, bcmask, invd, rel_tol, max_iter, x, ncomp, residuals, &ci);
+  int rc = run_cg(ctx, m->D, rhs, nullptr, 0, bcmask, invd, rel_tol, max_iter, x, ncomp, residuals, &ci, ctx->cg);
   if (rc) return rc;
   CK(cudaStreamSynchronize(ctx->stream));
   if (info) *info = ci;
@@ -794,7 +994,7 @@ extern "C" int hx_force_apply(hx_force* f, const double* e, double* y) {
   if (!f || !e || !y) return HX_EINVAL;
   hx_ctx* ctx = f->ctx;
   CK(cudaSetDevice(ctx->device));
-  ForceArgs a{e, f->DF, ctx->emap, tables(ctx), ctx->ne, ctx->evec2, nullptr};
+  ForceArgs a{e, f->DF, ctx->emap, ctx->slot, tables(ctx), ctx->ne, ctx->evec2, nullptr};
   int rc = dispatch<LaunchForce>(ctx, a, false);
   if (rc) return rc;
   return launch_scatter(ctx, ctx->evec2, ctx->dim, y);
@@ -804,7 +1004,7 @@ extern "C" int hx_force_apply_t(hx_force* f, const double* v, double* y) {
   if (!f || !v || !y) return HX_EINVAL;
   hx_ctx* ctx = f->ctx;
   CK(cudaSetDevice(ctx->device));
-  ForceArgs a{v, f->DF, ctx->emap, tables(ctx), ctx->ne, nullptr, y};
+  ForceArgs a{v, f->DF, ctx->emap, ctx->slot, tables(ctx), ctx->ne, nullptr, y};
   return dispatch<LaunchForce>(ctx, a, true);
 }
 
@@ -876,14 +1076,14 @@ extern "C" int hx_energy_solve(hx_ctx* ctx, const double* rhs, double* out) {
 // One rates() evaluation on device: fused qpoint/force kernel then the masked CG.
 // Status lands in st; CG info in *cgi.  No host sync except inside the CG poll.
 static int rates_device(hx_ctx* ctx, const hx_params* prm, const double* x, const double* v, const double* e,
-                        double* dv, double* de, StatusDev* st, hx_cg_info* cgi) {
+                        double* dv, double* de, StatusDev* st, hx_cg_info* cgi, CGDev* cg = nullptr) {
   int rc = status_reset(ctx, st);
   if (rc) return rc;
   rc = dispatch<LaunchRates>(ctx, x, v, e, ctx->evec, de, st, 0, prm->gamma, prm->q1, prm->q2);
   if (rc) return rc;
   // rhs = where(mask, 0, -F.1) built inside k_cg_init from the element vectors
   return run_cg(ctx, ctx->Dm, nullptr, ctx->evec, 1, ctx->has_mask ? ctx->mask : nullptr, ctx->invd,
-                prm->rel_tol, prm->max_iter, dv, ctx->dim, nullptr, cgi);
+                prm->rel_tol, prm->max_iter, dv, ctx->dim, nullptr, cgi, cg);
 }
 
 extern "C" int hx_rates(hx_ctx* ctx, const hx_params* prm, const double* x, const double* v, const double* e,
@@ -910,20 +1110,21 @@ extern "C" int hx_rates(hx_ctx* ctx, const hx_params* prm, const double* x, cons
 // timestep_estimate (dt_fixed < 0) + rk2_step on device (hydro.py:364-405)
 static int step_impl(hx_ctx* ctx, const hx_params* prm, double t, double dt_fixed, const double* x,
                      const double* v, const double* e, double* x_out, double* v_out, double* e_out,
-                     hx_step_info* info) {
+                     hx_step_info* info, int attempt0 = 0, const hx_step_info* carry = nullptr) {
   if (!ctx || !prm || !x || !v || !e || !x_out || !v_out || !e_out || !ctx->phase) return HX_EINVAL;
   CK(cudaSetDevice(ctx->device));
   const bool estimate = dt_fixed < 0.0;
   hx_step_info out{};
+  if (carry) out = *carry;
   const long long nv = ctx->nn * ctx->dim, nte = ctx->ne * ctx->nt;
   const unsigned ga = gblocks(std::max(nv, nte), 256);
-  long long clamps_total = 0;
-  for (int attempt = 0; attempt <= prm->max_retries; ++attempt) {
+  long long clamps_total = carry ? carry->clamped : 0;
+  for (int attempt = attempt0; attempt <= prm->max_retries; ++attempt) {
     // stage 1: rates(S) -- its ratio is also timestep_estimate's (same state)
     hx_cg_info c0{}, c1{};
-    int rc = rates_device(ctx, prm, x, v, e, ctx->dv0, ctx->de0, ctx->st + 0, &c0);
+    int rc = rates_device(ctx, prm, x, v, e, ctx->dv0, ctx->de0, ctx->st + 0, &c0, ctx->cg);
     if (rc) return rc;
-    DtArgs da{ctx->st + 0, ctx->dt, prm->cfl, prm->dt_max, prm->t_final, t, dt_fixed, attempt};
+    DtArgs da{ctx->st + 0, ctx->dt, prm->cfl, prm->dt_max, prm->t_final, t, dt_fixed, attempt, nullptr};
     k_dt<<<1, 1, 0, ctx->stream>>>(da);
     CKL();
     AxpyArgs m{x, v, e, v, ctx->dv0, ctx->de0, ctx->xm, ctx->vm, ctx->em, ctx->dt + 1, 0.5, nv, nte};
@@ -965,7 +1166,7 @@ static int step_impl(hx_ctx* ctx, const hx_params* prm, double t, double dt_fixe
       return out.code;
     }
     // stage 2: rates(mid)
-    rc = rates_device(ctx, prm, ctx->xm, ctx->vm, ctx->em, ctx->dv1, ctx->de1, ctx->st + 1, &c1);
+    rc = rates_device(ctx, prm, ctx->xm, ctx->vm, ctx->em, ctx->dv1, ctx->de1, ctx->st + 1, &c1, ctx->cg + 1);
     if (rc) return rc;
     AxpyArgs n{x, v, e, ctx->vm, ctx->dv1, ctx->de1, x_out, v_out, e_out, ctx->dt + 1, 1.0, nv, nte};
     prof_begin(ctx, K_AXPY);
@@ -1017,16 +1218,202 @@ static int step_impl(hx_ctx* ctx, const hx_params* prm, double t, double dt_fixe
   return out.code;
 }
 
+// ---- the same step as ONE CUDA graph (attempt 0; retries fall back to step_impl)
+
+static bool same_params(const hx_params& a, const hx_params& b) { return memcmp(&a, &b, sizeof a) == 0; }
+
+static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, const double* x, const double* v,
+                        const double* e, double* x_out, double* v_out, double* e_out, cudaGraphExec_t* exec) {
+  const long long nv = ctx->nn * ctx->dim, nte = ctx->ne * ctx->nt;
+  const unsigned ga = gblocks(std::max(nv, nte), 256);
+  cudaStream_t user = ctx->stream;
+  const bool prof = ctx->prof_on;
+  const long long launches = ctx->launches;
+  ctx->prof_on = false;
+  ctx->stream = ctx->gstream;
+  cudaGraph_t graph = nullptr;
+  int rc = HX_OK;
+  auto body = [&]() -> int {
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    int r = status_reset(ctx, ctx->st, 3);
+    if (r) return r;
+    const uint8_t* mask = ctx->has_mask ? ctx->mask : nullptr;
+    // stage 1: rates(S); its CFL ratio is timestep_estimate's
+    r = dispatch<LaunchRates>(ctx, x, v, e, ctx->evec, ctx->de0, ctx->st + 0, 0, prm->gamma, prm->q1, prm->q2);
+    if (r) return r;
+    CGLaunch L0;
+    r = cg_prepare(ctx, ctx->cg, ctx->Dm, nullptr, ctx->evec, 1, mask, ctx->invd, prm->rel_tol, prm->max_iter,
+                   ctx->dv0, ctx->dim, nullptr, L0);
+    if (r) return r;
+    r = cg_capture(ctx, L0);
+    if (r) return r;
+    DtArgs da{ctx->st + 0, ctx->dt, prm->cfl, prm->dt_max, prm->t_final, 0.0, dt_fixed, 0, ctx->t_dev};
+    k_dt<<<1, 1, 0, ctx->stream>>>(da);
+    CKL();
+    AxpyArgs m{x, v, e, v, ctx->dv0, ctx->de0, ctx->xm, ctx->vm, ctx->em, ctx->dt + 1, 0.5, nv, nte};
+    k_axpy_state<<<ga, 256, 0, ctx->stream>>>(m);
+    CKL();
+    // stage 2: rates(mid)
+    r = dispatch<LaunchRates>(ctx, (const double*)ctx->xm, (const double*)ctx->vm, (const double*)ctx->em,
+                              ctx->evec, ctx->de1, ctx->st + 1, 0, prm->gamma, prm->q1, prm->q2);
+    if (r) return r;
+    CGLaunch L1;
+    r = cg_prepare(ctx, ctx->cg + 1, ctx->Dm, nullptr, ctx->evec, 1, mask, ctx->invd, prm->rel_tol,
+                   prm->max_iter, ctx->dv1, ctx->dim, nullptr, L1);
+    if (r) return r;
+    r = cg_capture(ctx, L1);
+    if (r) return r;
+    AxpyArgs n{x, v, e, ctx->vm, ctx->dv1, ctx->de1, x_out, v_out, e_out, ctx->dt + 1, 1.0, nv, nte};
+    k_axpy_state<<<ga, 256, 0, ctx->stream>>>(n);
+    CKL();
+    // validity of the new geometry
+    r = dispatch<LaunchRates>(ctx, (const double*)x_out, (const double*)nullptr, (const double*)nullptr,
+                              (double*)nullptr, (double*)nullptr, ctx->st + 2, 1, 0.0, 0.0, 0.0);
+    if (r) return r;
+    CK(cudaMemcpyAsync(ctx->h_st, ctx->st, 3 * sizeof(StatusDev), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_cg, ctx->cg, 2 * sizeof(CGDev), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_dt, ctx->dt, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamEndCapture(ctx->stream, &graph));
+    return HX_OK;
+  };
+  rc = body();
+  if (rc) {
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(ctx->stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+      cudaGraph_t junk;
+      cudaStreamEndCapture(ctx->stream, &junk);
+      if (junk) cudaGraphDestroy(junk);
+    }
+    cudaGetLastError();
+  }
+  ctx->stream = user;
+  ctx->prof_on = prof;
+  ctx->launches = launches;
+  if (rc) return rc;
+  cudaError_t ce = cudaGraphInstantiate(exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ce != cudaSuccess) return fail(ctx, HX_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(ce));
+  return HX_OK;
+}
+
+static int g_use_graph = -1;  // HX_GRAPH=0 disables the graph path
+
+static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_fixed, const double* x,
+                         const double* v, const double* e, double* x_out, double* v_out, double* e_out,
+                         hx_step_info* info) {
+  if (!ctx || !prm || !x || !v || !e || !x_out || !v_out || !e_out || !ctx->phase) return HX_EINVAL;
+  if (g_use_graph < 0) {
+    const char* s = getenv("HX_GRAPH");
+    g_use_graph = (s && s[0] == '0') ? 0 : 1;
+  }
+  if (!g_use_graph || ctx->prof_on) return step_impl(ctx, prm, t, dt_fixed, x, v, e, x_out, v_out, e_out, info);
+  CK(cudaSetDevice(ctx->device));
+  const void* key[6] = {x, v, e, x_out, v_out, e_out};
+  hx_ctx::StepGraph* sg = nullptr;
+  for (auto& g : ctx->graphs)
+    if (!memcmp(g.key, key, sizeof key) && g.dt_fixed == dt_fixed && same_params(g.prm, *prm)) sg = &g;
+  if (!sg) {
+    if (ctx->graphs.size() >= 8) {
+      for (auto& g : ctx->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+      ctx->graphs.clear();
+    }
+    ctx->graphs.emplace_back();
+    sg = &ctx->graphs.back();
+    memcpy(sg->key, key, sizeof key);
+    sg->dt_fixed = dt_fixed;
+    sg->prm = *prm;
+  }
+  if (sg->seen++ == 0)  // first use of a buffer set: plain launches (warms every lazy init)
+    return step_impl(ctx, prm, t, dt_fixed, x, v, e, x_out, v_out, e_out, info);
+  if (!sg->exec) {
+    int rc = capture_step(ctx, prm, dt_fixed, x, v, e, x_out, v_out, e_out, &sg->exec);
+    if (rc) return rc;
+  }
+  *ctx->h_t = t;
+  CK(cudaMemcpyAsync(ctx->t_dev, ctx->h_t, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaGraphLaunch(sg->exec, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const StatusDev s0 = ctx->h_st[0], s1 = ctx->h_st[1], s2 = ctx->h_st[2];
+  const CGDev c0 = ctx->h_cg[0], c1 = ctx->h_cg[1];
+  ctx->launches += 9 + 2 * (long long)(c0.iters + c1.iters);
+  hx_step_info out{};
+  const bool estimate = dt_fixed < 0.0;
+  long long clamps = 0;
+  out.cg_iterations[0] = c0.iters;
+  out.cg_iterations[1] = c1.iters;
+  // interpretation identical to step_impl's first attempt
+  if (s0.inv_key != ~0ull) {
+    if (estimate) {
+      out.code = HX_EINVERTED;
+      out.failed_stage = 0;
+      decode_inv(ctx, s0.inv_key, &out.inv);
+      if (info) *info = out;
+      return out.code;
+    }
+    out.failed_stage = 0;
+    decode_inv(ctx, s0.inv_key, &out.inv);
+    out.retries = 1;
+    return step_impl(ctx, prm, t, dt_fixed, x, v, e, x_out, v_out, e_out, info, 1, &out);
+  }
+  if (estimate) {
+    clamps += (long long)s0.clamps;
+    out.dt = ctx->h_dt[0];
+    if (ctx->h_dt[0] < prm->dt_min) {
+      out.code = HX_EUNDERFLOW;
+      out.failed_stage = 0;
+      out.clamped = clamps;
+      if (info) *info = out;
+      return out.code;
+    }
+  }
+  clamps += (long long)s0.clamps;
+  if (c0.code) {
+    out.code = c0.code == 3 ? HX_ECG_BREAKDOWN : HX_ECG_MAXITER;
+    if (info) *info = out;
+    return out.code;
+  }
+  if (s1.inv_key != ~0ull) {
+    out.failed_stage = 1;
+    decode_inv(ctx, s1.inv_key, &out.inv);
+    out.retries = 1;
+    out.clamped = clamps;
+    return step_impl(ctx, prm, t, dt_fixed, x, v, e, x_out, v_out, e_out, info, 1, &out);
+  }
+  clamps += (long long)s1.clamps;
+  if (c1.code) {
+    out.code = c1.code == 3 ? HX_ECG_BREAKDOWN : HX_ECG_MAXITER;
+    if (info) *info = out;
+    return out.code;
+  }
+  if (s2.inv_key != ~0ull) {
+    out.failed_stage = 2;
+    decode_inv(ctx, s2.inv_key, &out.inv);
+    out.retries = 1;
+    out.clamped = clamps;
+    return step_impl(ctx, prm, t, dt_fixed, x, v, e, x_out, v_out, e_out, info, 1, &out);
+  }
+  out.code = HX_OK;
+  out.retries = 0;
+  out.dt = ctx->h_dt[1];
+  out.min_h_over_speed = s1.min_ratio;
+  out.t_new = t + ctx->h_dt[1];
+  out.clamped = clamps;
+  out.inv.inverted = 0;
+  if (info) *info = out;
+  return HX_OK;
+}
+
 extern "C" int hx_step(hx_ctx* ctx, const hx_params* prm, double t, const double* x, const double* v,
                        const double* e, double* x_out, double* v_out, double* e_out, hx_step_info* info) {
-  return step_impl(ctx, prm, t, -1.0, x, v, e, x_out, v_out, e_out, info);
+  return step_dispatch(ctx, prm, t, -1.0, x, v, e, x_out, v_out, e_out, info);
 }
 
 extern "C" int hx_rk2_step(hx_ctx* ctx, const hx_params* prm, double t, double dt, const double* x,
                            const double* v, const double* e, double* x_out, double* v_out, double* e_out,
                            hx_step_info* info) {
   if (!(dt >= 0.0)) return fail(ctx, HX_EINVAL, "dt must be >= 0");
-  return step_impl(ctx, prm, t, dt, x, v, e, x_out, v_out, e_out, info);
+  return step_dispatch(ctx, prm, t, dt, x, v, e, x_out, v_out, e_out, info);
 }
 
 extern "C" int hx_step_host(hx_ctx* ctx, const hx_params* prm, double t, double* x_host, double* v_host,

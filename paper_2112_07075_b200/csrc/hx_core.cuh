@@ -408,19 +408,21 @@ __device__ __forceinline__ double block_sum(double v, double* sbuf) {
   return r;
 }
 
-// "last block" detection for single-pass grid reductions: every block calls it
-// after publishing its partial; returns true in exactly one block (all threads).
+// "last block" detection for single-pass grid reductions.  Thread 0 of every block
+// has already written the block's partial; only it fences and bumps the counter
+// (a fence in every thread costs an L1 invalidation per thread).  Returns true in
+// exactly one block (all its threads), after an acquire fence.
 __device__ __forceinline__ bool grid_last_block(unsigned int* counter, int* sflag) {
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence();
     const unsigned int prev = atomicAdd(counter, 1u);
-    *sflag = (prev == gridDim.x - 1) ? 1 : 0;
+    const int last = (prev == gridDim.x - 1) ? 1 : 0;
+    if (last) __threadfence();
+    *sflag = last;
   }
   __syncthreads();
-  const bool last = *sflag != 0;
-  if (last) __threadfence();
-  return last;
+  return *sflag != 0;
 }
 
 // fixed-order sum of n partials by one block of NT threads; result in thread 0

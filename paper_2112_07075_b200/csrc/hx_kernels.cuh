@@ -169,6 +169,7 @@ struct RatesArgs {
   const double* e;     // (NE*nt)
   const double* qd0;   // (NE, nq)
   const int* emap;     // (NE, nl)
+  const int* slot;     // (NE, nl) position of (e, l) in the node-sorted E-vector
   const double* minv;  // (NE, nt, nt)
   Tables tab;
   double gamma, q1, q2;
@@ -294,10 +295,9 @@ __global__ void __launch_bounds__(NT) k_rates(RatesArgs a) {
   // F^T v: thermodynamic transpose interpolation (operators.py:297)
   double* fv = interp_t<DIM, DT, Q, 1, NT>(sBt, sq, eq, tid);
   __syncthreads();
-  double* ev = a.evec + e * NL * DIM;
   for (int i = tid; i < NL * DIM; i += NT) {
     const int l = i / DIM, c = i - l * DIM;
-    ev[i] = fout[c * NL + l];
+    a.evec[(long long)a.slot[e * NL + l] * DIM + c] = fout[c * NL + l];
   }
   // de = M_e^{-1} (F^T v)_e   (einsum "eij,ej->ei", hydro.py:343)
   const double* mi = a.minv + e * NTH * NTH;
@@ -319,7 +319,14 @@ struct CGDev {
   double rz, norm0, alpha, beta, tol;
   int it, active, code, iters, max_iter, nres;
   unsigned int cnt[4];
+  unsigned long long cond;  // cudaGraphConditionalHandle of the WHILE node (graph mode)
+  int use_cond;
 };
+
+// publish the CG "continue" flag to the enclosing WHILE graph node
+__device__ __forceinline__ void cg_publish(const CGDev* g) {
+  if (g->use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)g->cond, g->active ? 1u : 0u);
+}
 
 struct MassArgs {
   const double* x;      // apply: input (NN, NC); cg: z
@@ -330,6 +337,7 @@ struct MassArgs {
   const uint8_t* own;   // (NE, nl)
   const double* D;      // (NE, nq)
   const int* emap;
+  const int* slot;      // (NE, nl) node-sorted E-vector position
   const double* B;      // (Q, D1)
   long long ne;
   double* evec;         // (NE, nl, NC)
@@ -400,10 +408,211 @@ __global__ void __launch_bounds__(128) k_mass(MassArgs a) {
     double* other = (qv == A) ? Bf : A;
     double* r = interp_t<DIM, D1, Q, NC, 32>(sB, qv, other, lane);
     __syncwarp();
-    double* ev = a.evec + e * NL * NC;
     for (int i = lane; i < NL * NC; i += 32) {
       const int l = i / NC, c = i - l * NC;
-      ev[i] = r[c * NL + l];
+      a.evec[(long long)a.slot[e * NL + l] * NC + c] = r[c * NL + l];
+    }
+  }
+  if constexpr (CG) {
+    const double bs = block_sum<128>(acc, red);
+    if (threadIdx.x == 0) a.partials[blockIdx.x] = bs;
+    if (grid_last_block(&a.cg->cnt[0], &sflag)) {
+      const double pAp = reduce_partials<128>(a.partials, gridDim.x, red);
+      if (threadIdx.x == 0) {
+        a.cg->cnt[0] = 0;
+        if (pAp <= 0.0) {
+          a.cg->code = 3;
+          a.cg->active = 0;
+        } else {
+          a.cg->alpha = a.cg->rz / pAp;
+        }
+      }
+    }
+  }
+}
+
+// Fixed 1D tables per order p, in the constant bank: the z-direction stages read
+// them with warp-uniform addresses, so DFMA takes them as c[][] operands (no
+// register or shared-memory traffic).  hx_create uploads them and refuses a
+// context whose tables differ (they depend only on p: Lobatto nodes, p+2 Gauss points).
+__constant__ double c_B[4][30];
+
+// 3D PA mass with a (qx, qy) column per thread (the z direction lives in registers).
+// A CTA of 128 threads holds EPB = 128 / Q^2 elements.  Same CG fusion as k_mass.
+//   X:  A[dz][dy][qx] = sum_dx B[qx][dx] X[dz][dy][dx]      threads (qx, dy<D1)
+//   Y:  S[dz][qy][qx] = sum_dy B[qy][dy] A[dz][dy][qx]      threads (qx, qy)
+//   Z:  u[qz] = sum_dz B[qz][dz] S[dz][qy][qx]; u *= D; S[dz][qy][qx] = sum_qz B[qz][dz] u[qz]
+//   Y^T: A[dz][dy][qx] = sum_qy B[qy][dy] S[dz][qy][qx]    threads (qx, dy<D1)
+//   X^T: out[dz][dy][dx] = sum_qx B[qx][dx] A[dz][dy][qx]  threads (dx<D1, dy<D1)
+// Latency hiding: the point data D and every gathered value are requested before
+// the first use (all loads of a thread in flight at once).
+template <int P, int NC, bool CG>
+__global__ void __launch_bounds__(128, 5) k_mass3d(MassArgs a) {
+  constexpr int D1 = P + 1, Q = P + 2, Q2 = Q * Q, NL = D1 * D1 * D1, NQ = Q * Q * Q;
+  constexpr int EPB = 128 / Q2;
+  constexpr int SX = NL, SA = D1 * D1 * Q, SB = D1 * Q * Q;
+  constexpr int PER = NC * (SX + SA + SB);
+  constexpr int GR = (NL + Q2 - 1) / Q2;  // gather rounds (nodes per thread)
+  const double* cB = c_B[P - 1];
+  extern __shared__ double smem[];
+  __shared__ double red[32];
+  __shared__ int sflag;
+  if (CG && !a.cg->active) return;
+  const int t = threadIdx.x;
+  const int el = t / Q2, w = t - el * Q2, tx = w % Q, ty = w / Q;
+  const long long e = (long long)blockIdx.x * EPB + el;
+  const bool active = el < EPB && e < a.ne;
+  double* sX = smem + (el < EPB ? el : 0) * PER;
+  double* sA = sX + NC * SX;
+  double* sS = sA + NC * SA;
+  // point data first (independent of everything else)
+  double Dq[Q];
+  if (active) {
+    const double* De = a.D + e * NQ + ty * Q + tx;
+#pragma unroll
+    for (int qz = 0; qz < Q; ++qz) Dq[qz] = __ldg(De + qz * Q2);
+  }
+  double acc = 0.0;
+  if (active) {
+    double beta = 0.0;
+    const double* po = nullptr;
+    if constexpr (CG) {
+      beta = a.cg->beta;
+      po = (a.cg->it & 1) ? a.pbuf0 : a.pbuf1;
+    }
+    const int* em = a.emap + e * NL;
+    long long nd[GR];
+#pragma unroll
+    for (int k = 0; k < GR; ++k) {
+      const int l = w + k * Q2;
+      nd[k] = l < NL ? (long long)__ldg(em + l) : -1;
+    }
+    double zv[GR][NC], pv[GR][NC];
+    uint8_t mk[GR][NC], ow[GR];
+#pragma unroll
+    for (int k = 0; k < GR; ++k) {
+      const int l = w + k * Q2;
+      if (nd[k] >= 0) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          zv[k][c] = __ldcg(a.x + nd[k] * NC + c);
+          if constexpr (CG) {
+            pv[k][c] = __ldcg(po + nd[k] * NC + c);
+            mk[k][c] = a.mask ? a.mask[nd[k] * NC + c] : 0;
+          }
+        }
+        if constexpr (CG) ow[k] = a.own[e * NL + l];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < GR; ++k) {
+      const int l = w + k * Q2;
+      if (nd[k] >= 0) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          double val = zv[k][c];
+          if constexpr (CG) {
+            const double p = __dadd_rn(zv[k][c], __dmul_rn(beta, pv[k][c]));
+            if (mk[k][c] && ow[k]) acc = fma(p, p, acc);
+            val = mk[k][c] ? 0.0 : p;
+          }
+          sX[c * SX + l] = val;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (active && ty < D1) {  // X
+    double rowx[D1];
+#pragma unroll
+    for (int d = 0; d < D1; ++d) rowx[d] = cB[tx * D1 + d];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int dz = 0; dz < D1; ++dz) {
+        const double* src = sX + c * SX + (dz * D1 + ty) * D1;
+        double s = 0.0;
+#pragma unroll
+        for (int dx = 0; dx < D1; ++dx) s = fma(rowx[dx], src[dx], s);
+        sA[c * SA + (dz * D1 + ty) * Q + tx] = s;
+      }
+  }
+  __syncthreads();
+  if (active) {  // Y
+    double rowy[D1];
+#pragma unroll
+    for (int d = 0; d < D1; ++d) rowy[d] = cB[ty * D1 + d];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int dz = 0; dz < D1; ++dz) {
+        double s = 0.0;
+#pragma unroll
+        for (int dy = 0; dy < D1; ++dy) s = fma(rowy[dy], sA[c * SA + (dz * D1 + dy) * Q + tx], s);
+        sS[c * SB + (dz * Q + ty) * Q + tx] = s;
+      }
+  }
+  __syncthreads();
+  if (active) {  // Z, D, Z^T in registers; B from the constant bank
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      double col[D1];
+#pragma unroll
+      for (int dz = 0; dz < D1; ++dz) col[dz] = sS[c * SB + (dz * Q + ty) * Q + tx];
+      double u[Q];
+#pragma unroll
+      for (int qz = 0; qz < Q; ++qz) {
+        double s = 0.0;
+#pragma unroll
+        for (int dz = 0; dz < D1; ++dz) s = fma(cB[qz * D1 + dz], col[dz], s);
+        const double du = s * Dq[qz];
+        if constexpr (CG) acc = fma(du, s, acc);
+        u[qz] = du;
+      }
+#pragma unroll
+      for (int dz = 0; dz < D1; ++dz) {
+        double s = 0.0;
+#pragma unroll
+        for (int qz = 0; qz < Q; ++qz) s = fma(cB[qz * D1 + dz], u[qz], s);
+        sS[c * SB + (dz * Q + ty) * Q + tx] = s;
+      }
+    }
+  }
+  __syncthreads();
+  if (active && ty < D1) {  // Y^T
+    double coly[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) coly[q] = cB[q * D1 + ty];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int dz = 0; dz < D1; ++dz) {
+        double s = 0.0;
+#pragma unroll
+        for (int qy = 0; qy < Q; ++qy) s = fma(coly[qy], sS[c * SB + (dz * Q + qy) * Q + tx], s);
+        sA[c * SA + (dz * D1 + ty) * Q + tx] = s;
+      }
+  }
+  __syncthreads();
+  if (active && ty < D1 && tx < D1) {  // X^T -> node-sorted E-vector
+    double colx[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) colx[q] = cB[q * D1 + tx];
+    const int* sl = a.slot + e * NL;
+    int so[D1];
+#pragma unroll
+    for (int dz = 0; dz < D1; ++dz) so[dz] = __ldg(sl + (dz * D1 + ty) * D1 + tx);
+#pragma unroll
+    for (int dz = 0; dz < D1; ++dz) {
+      const long long o = (long long)so[dz] * NC;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double* src = sA + c * SA + (dz * D1 + ty) * Q;
+        double s = 0.0;
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx) s = fma(colx[qx], src[qx], s);
+        a.evec[o + c] = s;
+      }
     }
   }
   if constexpr (CG) {
@@ -425,20 +634,256 @@ __global__ void __launch_bounds__(128) k_mass(MassArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Warp-per-element 3D PA mass ("line" mapping).  Each lane owns whole tensor
+// lines of a 1D contraction (MI inputs -> MO outputs), so all lanes read the same
+// basis entry at the same time: the basis is a constant-bank operand of DFMA
+// (c_B, warp-uniform) and every shared-memory load feeds MO FMAs.  Tensors use an
+// odd x-pitch so line-strided accesses are bank-conflict free.  Only __syncwarp
+// between stages.  CG fusion as in k_mass (direction update, wall mask, p.Ap).
+
+__constant__ double c_G[4][30];
+
+template <int P, int TAB>
+__device__ __forceinline__ double cmat(int i) {
+  if constexpr (TAB == 0) return c_B[P - 1][i];
+  else return c_G[P - 1][i];
+}
+
+__host__ __device__ constexpr int oddp(int n) { return n | 1; }
+
+// out = M.in along axis AX; M is the (Q x D1) table TAB, applied D1->Q (TR=false)
+// or transposed Q->D1 (TR=true).  in: (N0,N1,N2) with x-pitch P0; out x-pitch oddp(O0).
+template <int P, int TAB, bool TR, int N0, int N1, int N2, int AX, int NC>
+__device__ __forceinline__ void wline(const double* in, double* out, int lane) {
+  constexpr int D1 = P + 1;
+  constexpr int MI = AX == 0 ? N0 : (AX == 1 ? N1 : N2);
+  constexpr int MO = TR ? D1 : P + 2;
+  constexpr int O0 = AX == 0 ? MO : N0, O1 = AX == 1 ? MO : N1, O2 = AX == 2 ? MO : N2;
+  constexpr int P0 = oddp(N0), Q0 = oddp(O0);
+  constexpr int CSI = N2 * N1 * P0, CSO = O2 * O1 * Q0;
+  constexpr int NLN = N0 * N1 * N2 / MI;
+  constexpr int ROUNDS = (NLN * NC + 31) / 32;
+  constexpr int IST = AX == 0 ? 1 : (AX == 1 ? P0 : N1 * P0);
+  constexpr int OST = AX == 0 ? 1 : (AX == 1 ? Q0 : O1 * Q0);
+#pragma unroll
+  for (int r = 0; r < ROUNDS; ++r) {
+    const int w = lane + 32 * r;
+    if (w < NLN * NC) {
+      const int c = w / NLN, l = w - c * NLN;
+      int ib, ob;
+      if constexpr (AX == 0) {
+        ib = l * P0;  // l = i2*N1 + i1
+        ob = l * Q0;
+      } else if constexpr (AX == 1) {
+        const int i0 = l % N0, i2 = l / N0;
+        ib = i2 * N1 * P0 + i0;
+        ob = i2 * O1 * Q0 + i0;
+      } else {
+        const int i0 = l % N0, i1 = l / N0;
+        ib = i1 * P0 + i0;
+        ob = i1 * Q0 + i0;
+      }
+      const double* src = in + c * CSI + ib;
+      double* dst = out + c * CSO + ob;
+      double x[MI];
+#pragma unroll
+      for (int j = 0; j < MI; ++j) x[j] = src[j * IST];
+#pragma unroll
+      for (int k = 0; k < MO; ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < MI; ++j) s = fma(cmat<P, TAB>(TR ? j * D1 + k : k * D1 + j), x[j], s);
+        dst[k * OST] = s;
+      }
+    }
+  }
+}
+
+template <int P, int NC>
+struct Mass3W {
+  static constexpr int D1 = P + 1, Q = P + 2;
+  static constexpr int BUF = NC * Q * Q * oddp(Q);  // largest stage tensor
+  static constexpr int WPB = 4;
+  static constexpr size_t bytes = sizeof(double) * WPB * 2 * BUF;
+};
+
+template <int P, int NC, bool CG, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_mass3w(MassArgs a) {
+  constexpr int D1 = P + 1, Q = P + 2, NL = D1 * D1 * D1, NQ = Q * Q * Q, Q2 = Q * Q;
+  constexpr int WPB = Mass3W<P, NC>::WPB, BUF = Mass3W<P, NC>::BUF;
+  constexpr int PD = oddp(D1), PQ = oddp(Q);
+  constexpr int GR = (NL + 31) / 32;          // gather rounds (nodes per lane)
+  constexpr int ZR = (Q2 * NC + 31) / 32;     // z-stage rounds (columns per lane)
+  extern __shared__ double smem[];
+  __shared__ double red[32];
+  __shared__ int sflag;
+  if (CG && !a.cg->active) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* A = smem + warp * 2 * BUF;
+  double* Bb = A + BUF;
+  double acc = 0.0;
+  // persistent: the grid covers the resident capacity, warps stride over elements
+  for (long long e = (long long)blockIdx.x * WPB + warp; e < a.ne; e += (long long)gridDim.x * WPB) {
+    // gather: lane owns nodes lane, lane+32, ... (all loads issued before use)
+    double beta = 0.0;
+    const double* po = nullptr;
+    if constexpr (CG) {
+      beta = a.cg->beta;
+      po = (a.cg->it & 1) ? a.pbuf0 : a.pbuf1;
+    }
+    const int* em = a.emap + e * NL;
+    long long nd[GR];
+#pragma unroll
+    for (int k = 0; k < GR; ++k) {
+      const int l = lane + 32 * k;
+      nd[k] = l < NL ? (long long)__ldg(em + l) : -1;
+    }
+    double zv[GR][NC], pv[GR][NC];
+    uint8_t mk[GR][NC], ow[GR];
+#pragma unroll
+    for (int k = 0; k < GR; ++k) {
+      if (nd[k] >= 0) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          zv[k][c] = __ldcg(a.x + nd[k] * NC + c);
+          if constexpr (CG) {
+            pv[k][c] = __ldcg(po + nd[k] * NC + c);
+            mk[k][c] = a.mask ? a.mask[nd[k] * NC + c] : 0;
+          }
+        }
+        if constexpr (CG) ow[k] = a.own[e * NL + lane + 32 * k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < GR; ++k) {
+      const int l = lane + 32 * k;
+      if (nd[k] >= 0) {
+        const int dx = l % D1, dy = (l / D1) % D1, dz = l / (D1 * D1);
+        const int si = (dz * D1 + dy) * PD + dx;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          double val = zv[k][c];
+          if constexpr (CG) {
+            const double p = __dadd_rn(zv[k][c], __dmul_rn(beta, pv[k][c]));
+            if (mk[k][c] && ow[k]) acc = fma(p, p, acc);
+            val = mk[k][c] ? 0.0 : p;
+          }
+          A[c * D1 * D1 * PD + si] = val;
+        }
+      }
+    }
+    __syncwarp();
+    wline<P, 0, false, D1, D1, D1, 0, NC>(A, Bb, lane);  // (Q, D1, D1)
+    __syncwarp();
+    // point data of this lane's z columns, in flight during the y stage
+    double Dq[ZR][Q];
+#pragma unroll
+    for (int r = 0; r < ZR; ++r) {
+      const int w = lane + 32 * r;
+      const int l = (w < Q2 * NC) ? w % Q2 : 0;
+#pragma unroll
+      for (int qz = 0; qz < Q; ++qz) Dq[r][qz] = __ldg(a.D + e * NQ + qz * Q2 + l);
+    }
+    wline<P, 0, false, Q, D1, D1, 1, NC>(Bb, A, lane);   // (Q, Q, D1)
+    __syncwarp();
+    // z stage: B, D, B^T on each (qx, qy) column in registers; in place in A
+#pragma unroll
+    for (int r = 0; r < ZR; ++r) {
+      const int w = lane + 32 * r;
+      if (w < Q2 * NC) {
+        const int c = w / Q2, l = w - c * Q2;
+        const int qx = l % Q, qy = l / Q;
+        double* col = A + c * D1 * Q * PQ + qy * PQ + qx;  // (Q,Q,D1) tensor, z stride Q*PQ
+        double xin[D1];
+#pragma unroll
+        for (int dz = 0; dz < D1; ++dz) xin[dz] = col[dz * Q * PQ];
+        double u[Q];
+#pragma unroll
+        for (int qz = 0; qz < Q; ++qz) {
+          double s = 0.0;
+#pragma unroll
+          for (int dz = 0; dz < D1; ++dz) s = fma(cmat<P, 0>(qz * D1 + dz), xin[dz], s);
+          const double du = s * Dq[r][qz];
+          if constexpr (CG) acc = fma(du, s, acc);
+          u[qz] = du;
+        }
+#pragma unroll
+        for (int dz = 0; dz < D1; ++dz) {
+          double s = 0.0;
+#pragma unroll
+          for (int qz = 0; qz < Q; ++qz) s = fma(cmat<P, 0>(qz * D1 + dz), u[qz], s);
+          col[dz * Q * PQ] = s;
+        }
+      }
+    }
+    __syncwarp();
+    wline<P, 0, true, Q, Q, D1, 1, NC>(A, Bb, lane);     // (Q, D1, D1)
+    __syncwarp();
+    wline<P, 0, true, Q, D1, D1, 0, NC>(Bb, A, lane);    // (D1, D1, D1)
+    __syncwarp();
+    // node-sorted E-vector: lanes over (node, component), 24 contiguous bytes per node
+    const int* sl = a.slot + e * NL;
+#pragma unroll
+    for (int k = 0; k < GR; ++k) {
+      const int l = lane + 32 * k;
+      if (l < NL) {
+        const int dx = l % D1, dy = (l / D1) % D1, dz = l / (D1 * D1);
+        const int si = (dz * D1 + dy) * PD + dx;
+        const long long o = (long long)__ldg(sl + l) * NC;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) a.evec[o + c] = A[c * D1 * D1 * PD + si];
+      }
+    }
+    __syncwarp();
+  }
+  if constexpr (CG) {
+    const double bs = block_sum<32 * WPB>(acc, red);
+    if (threadIdx.x == 0) a.partials[blockIdx.x] = bs;
+    if (grid_last_block(&a.cg->cnt[0], &sflag)) {
+      const double pAp = reduce_partials<32 * WPB>(a.partials, gridDim.x, red);
+      if (threadIdx.x == 0) {
+        a.cg->cnt[0] = 0;
+        if (pAp <= 0.0) {
+          a.cg->code = 3;
+          a.cg->active = 0;
+        } else {
+          a.cg->alpha = a.cg->rz / pAp;
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // node-side kernels: deterministic G^T through the transpose map
 
-// L[n, c] = sum over entries of node n (ascending element) of E[idx, c]   (fespace.py:227-234)
+// E is node-sorted: the entries of node n are E[off[n]..off[n+1]) in ascending element
+// order.  Up to MAXDEG entries are requested at once (absent ones read as +0.0,
+// which never changes a sum that starts from 0.0), then added in order: the result
+// is bit-identical to the sequential ascending-element accumulation (fespace.py:227-234).
+template <int NC>
+__device__ __forceinline__ double node_sum1(const int* off, const double* E, long long n, int c) {
+  constexpr int MAXDEG = 8;
+  const int b = __ldg(off + n), f = __ldg(off + n + 1);
+  double s = 0.0;
+  if (f - b <= MAXDEG) {
+    double v[MAXDEG];
+#pragma unroll
+    for (int j = 0; j < MAXDEG; ++j) v[j] = (b + j < f) ? __ldcg(E + (long long)(b + j) * NC + c) : 0.0;
+#pragma unroll
+    for (int j = 0; j < MAXDEG; ++j) s += v[j];
+  } else {
+    for (long long k = b; k < f; ++k) s += __ldcg(E + k * NC + c);
+  }
+  return s;
+}
+
 template <int NC>
 __device__ __forceinline__ void node_sum(const int* off, const int* idx, const double* E, long long n,
                                          double (&s)[NC]) {
 #pragma unroll
-  for (int c = 0; c < NC; ++c) s[c] = 0.0;
-  const int b = off[n], f = off[n + 1];
-  for (int k = b; k < f; ++k) {
-    const long long j = idx[k];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) s[c] += E[j * NC + c];
-  }
+  for (int c = 0; c < NC; ++c) s[c] = node_sum1<NC>(off, E, n, c);
+  (void)idx;
 }
 
 struct NodeArgs {
@@ -459,6 +904,10 @@ struct NodeArgs {
   double* partials;
   double* hist;
   int negate;           // cg_init from evec: rhs = -sum
+  double tol;           // cg_init: stop tolerance and iteration cap
+  int max_iter;
+  unsigned long long cond;
+  int use_cond;
 };
 
 // plain scatter: out = G^T evec (internal layout)
@@ -474,33 +923,27 @@ __global__ void __launch_bounds__(256) k_scatter(NodeArgs a) {
 
 // CG start (cg_solve operators.py:340-350): r = b, z = D^{-1} r, x = 0, p_0 = 0,
 // rz = r.z, norm0 = sqrt(rz); b == 0 everywhere -> 0 iterations.
-// b is rhs, or -(G^T evec) masked (rhs_v = -F.1, hydro.py:351, 320).
+// b is rhs, or -(G^T evec) masked (rhs_v = -F.1, hydro.py:351, 320).  Persistent
+// grid-stride over (node, component).
 template <int NC>
 __global__ void __launch_bounds__(256) k_cg_init(NodeArgs a) {
   __shared__ double red[32];
   __shared__ int sflag;
-  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   double rz = 0.0, nz = 0.0;
-  if (n < a.nn) {
-    double s[NC];
-    if (a.rhs) {
-#pragma unroll
-      for (int c = 0; c < NC; ++c) s[c] = a.rhs[n * NC + c];
-    } else {
-      node_sum<NC>(a.off, a.idx, a.evec, n, s);
-    }
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      double b = a.negate ? -s[c] : s[c];
-      if (a.mask && a.mask[n * NC + c]) b = 0.0;
-      const double z = a.invd[n * NC + c] * b;
-      a.r[n * NC + c] = b;
-      a.z[n * NC + c] = z;
-      a.x[n * NC + c] = 0.0;
-      a.pbuf0[n * NC + c] = 0.0;
-      rz = fma(b, z, rz);
-      if (b != 0.0 || b != b) nz += 1.0;
-    }
+  const long long N = a.nn * NC;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += (long long)gridDim.x * blockDim.x) {
+    const long long n = j / NC;
+    const int c = (int)(j - n * NC);
+    const double s = a.rhs ? a.rhs[j] : node_sum1<NC>(a.off, a.evec, n, c);
+    double b = a.negate ? -s : s;
+    if (a.mask && a.mask[j]) b = 0.0;
+    const double z = a.invd[j] * b;
+    a.r[j] = b;
+    a.z[j] = z;
+    a.x[j] = 0.0;
+    a.pbuf0[j] = 0.0;
+    rz = fma(b, z, rz);
+    if (b != 0.0 || b != b) nz += 1.0;
   }
   const double brz = block_sum<256>(rz, red);
   const double bnz = block_sum<256>(nz, red);
@@ -523,9 +966,18 @@ __global__ void __launch_bounds__(256) k_cg_init(NodeArgs a) {
       g->beta = 0.0;
       g->it = 1;
       g->iters = 0;
-      if (anyb == 0.0) {
+      g->tol = a.tol;
+      g->max_iter = a.max_iter;
+      g->cond = a.cond;
+      g->use_cond = a.use_cond;
+      if (anyb == 0.0 || a.max_iter <= 0) {
         g->active = 0;
-        g->nres = 0;
+        g->nres = anyb == 0.0 ? 0 : 1;
+        if (anyb != 0.0) {
+          g->norm0 = sqrt(t);
+          if (a.hist) a.hist[0] = g->norm0;
+          g->code = 4;
+        }
       } else {
         g->rz = t;
         g->norm0 = sqrt(t);
@@ -533,6 +985,7 @@ __global__ void __launch_bounds__(256) k_cg_init(NodeArgs a) {
         g->nres = 1;
         g->active = 1;
       }
+      cg_publish(g);
     }
   }
 }
@@ -541,7 +994,7 @@ __global__ void __launch_bounds__(256) k_cg_init(NodeArgs a) {
 // Ap = G^T evec (identity on masked rows), x += alpha p, r -= alpha Ap, z = D^{-1} r,
 // rz_new = r.z; stop test sqrt(max(rz_new,0)) <= tol*norm0; beta = rz_new/rz.
 template <int NC>
-__global__ void __launch_bounds__(256) k_cg_node(NodeArgs a) {
+__global__ void __launch_bounds__(256, 4) k_cg_node(NodeArgs a) {
   __shared__ double red[32];
   __shared__ int sflag;
   CGDev* g = a.cg;
@@ -550,23 +1003,44 @@ __global__ void __launch_bounds__(256) k_cg_node(NodeArgs a) {
   const double alpha = g->alpha, beta = g->beta;
   const double* po = (k & 1) ? a.pbuf0 : a.pbuf1;
   double* pn = (k & 1) ? a.pbuf1 : a.pbuf0;
-  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   double rz = 0.0;
-  if (n < a.nn) {
-    double s[NC];
-    node_sum<NC>(a.off, a.idx, a.evec, n, s);
+  // grid-stride over (node, component), U items per thread per trip so that all
+  // their loads are in flight together
+  constexpr int U = 2;
+  const long long N = a.nn * NC;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long j0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; j0 < N; j0 += U * stride) {
+    double zj[U], pj[U], xj[U], rj[U], dj[U], s[U];
+    bool m[U];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const long long j = n * NC + c;
-      const double p = __dadd_rn(a.z[j], __dmul_rn(beta, po[j]));
-      pn[j] = p;
-      const double ap = (a.mask && a.mask[j]) ? p : s[c];
-      a.x[j] = __dadd_rn(a.x[j], __dmul_rn(alpha, p));
-      const double r = __dsub_rn(a.r[j], __dmul_rn(alpha, ap));
-      a.r[j] = r;
-      const double z = __dmul_rn(a.invd[j], r);
-      a.z[j] = z;
-      rz = fma(r, z, rz);
+    for (int u = 0; u < U; ++u) {
+      const long long j = j0 + u * stride;
+      if (j < N) {
+        const long long n = j / NC;
+        const int c = (int)(j - n * NC);
+        zj[u] = __ldcg(a.z + j);
+        pj[u] = __ldcg(po + j);
+        xj[u] = __ldcg(a.x + j);
+        rj[u] = __ldcg(a.r + j);
+        dj[u] = __ldg(a.invd + j);
+        m[u] = a.mask && a.mask[j];
+        s[u] = node_sum1<NC>(a.off, a.evec, n, c);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long j = j0 + u * stride;
+      if (j < N) {
+        const double p = __dadd_rn(zj[u], __dmul_rn(beta, pj[u]));
+        pn[j] = p;
+        const double ap = m[u] ? p : s[u];
+        a.x[j] = __dadd_rn(xj[u], __dmul_rn(alpha, p));
+        const double r = __dsub_rn(rj[u], __dmul_rn(alpha, ap));
+        a.r[j] = r;
+        const double z = __dmul_rn(dj[u], r);
+        a.z[j] = z;
+        rz = fma(r, z, rz);
+      }
     }
   }
   const double brz = block_sum<256>(rz, red);
@@ -590,6 +1064,7 @@ __global__ void __launch_bounds__(256) k_cg_node(NodeArgs a) {
         g->rz = rzn;
         g->it = k + 1;
       }
+      cg_publish(g);
     }
   }
 }
@@ -630,20 +1105,32 @@ struct DtArgs {
   double cfl, dt_max, t_final, t;
   double dt_fixed;   // >= 0: rk2_step(state, dt) with a caller-given dt
   int retry;
+  const double* tptr;  // state time on the device (graph mode) or null (use t)
 };
 __global__ void k_dt(DtArgs a) {
   double dt;
   if (a.dt_fixed >= 0.0) {
     dt = a.dt_fixed;
   } else {
+    const double t = a.tptr ? *a.tptr : a.t;
     dt = a.cfl * a.st->min_ratio;
     dt = fmin(dt, a.dt_max);
-    dt = fmin(dt, a.t_final - a.t);
+    dt = fmin(dt, a.t_final - t);
   }
   a.dt[0] = dt;
   double att = dt;
   for (int i = 0; i < a.retry; ++i) att /= 2.0;
   a.dt[1] = att;
+}
+
+__global__ void k_status_reset(StatusDev* st, int n) {
+  const int i = threadIdx.x;
+  if (i < n) {
+    st[i].inv_key = ~0ull;
+    st[i].clamps = 0;
+    st[i].min_ratio = __longlong_as_double(0x7ff0000000000000ll);
+    st[i].pad = 0;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -884,6 +1371,7 @@ struct ForceArgs {
   const double* in;     // apply: e (NE*nt); apply_t: v (NN, d)
   const double* DF;     // (NE, d*d, nq)
   const int* emap;
+  const int* slot;
   Tables tab;
   long long ne;
   double* evec;         // apply: (NE, nl, d)
@@ -931,10 +1419,9 @@ __global__ void __launch_bounds__(NT) k_force(ForceArgs a) {
     __syncthreads();
     grad_t<DIM, D1, Q, DIM, (DIM + 1) * NQ, NT>(sB, sG, rOut, rA, rS, rF, tid);
     __syncthreads();
-    double* ev = a.evec + e * NL * DIM;
     for (int i = tid; i < NL * DIM; i += NT) {
       const int l = i / DIM, c = i - l * DIM;
-      ev[i] = rF[c * NL + l];
+      a.evec[(long long)a.slot[e * NL + l] * DIM + c] = rF[c * NL + l];
     }
   } else {
     const int* em = a.emap + e * NL;
@@ -962,7 +1449,8 @@ __global__ void __launch_bounds__(NT) k_force(ForceArgs a) {
 
 // MassPA.diagonal (operators.py:117-124): contract D with (B*B)^T on every axis
 template <int DIM, int P>
-__global__ void __launch_bounds__(128) k_mass_diag(const double* D, const double* B, long long ne, double* evec) {
+__global__ void __launch_bounds__(128) k_mass_diag(const double* D, const double* B, const int* slot, long long ne,
+                                                   double* evec) {
   using Dd = Disc<DIM, P>;
   constexpr int D1 = Dd::D1, Q = Dd::Q, NL = Dd::NL, NQ = Dd::NQ;
   __shared__ double sB2[Q * D1];
@@ -978,7 +1466,7 @@ __global__ void __launch_bounds__(128) k_mass_diag(const double* D, const double
   __syncwarp();
   double* r = interp_t<DIM, D1, Q, 1, 32>(sB2, A, Bf, lane);
   __syncwarp();
-  for (int i = lane; i < NL; i += 32) evec[e * NL + i] = r[i];
+  for (int i = lane; i < NL; i += 32) evec[slot[e * NL + i]] = r[i];
 }
 
 // per-element thermodynamic mass blocks M_e = Bth^T diag(D) Bth and their inverse
