@@ -253,14 +253,66 @@ static int launch_mass3w(hx_ctx* ctx, bool cgmode, const MassArgs& a) {
   return launch_mass3w_b<P, NC, 4>(ctx, cgmode, a);
 }
 
-static int g_mass_variant = -1;  // HX_MASS_KERNEL=column|line (default line)
+template <int P, int NC>
+static int launch_mass_pc(hx_ctx* ctx, bool cgmode, const MassArgs& a) {
+  using M = MassPC<P, NC>;
+  const unsigned work = gblocks(ctx->ne, M::EPC);
+  if (cgmode) {
+    auto k = k_mass_pc<P, NC, true>;
+    CK(smem_attr(k, M::bytes));
+    static unsigned grid = 0;
+    if (!grid) grid = persistent_grid(k, 128, M::bytes, 1ll << 40);
+    prof_begin(ctx, K_MASS);
+    k<<<std::min(grid, work), 128, M::bytes, ctx->stream>>>(a);
+    prof_end(ctx);
+  } else {
+    auto k = k_mass_pc<P, NC, false>;
+    CK(smem_attr(k, M::bytes));
+    static unsigned grid = 0;
+    if (!grid) grid = persistent_grid(k, 128, M::bytes, 1ll << 40);
+    k<<<std::min(grid, work), 128, M::bytes, ctx->stream>>>(a);
+  }
+  CKL();
+  return HX_OK;
+}
+
+template <int P, int NC>
+static int launch_mass_pc2(hx_ctx* ctx, bool cgmode, const MassArgs& a) {
+  using M = MassPC2<P, NC>;
+  const unsigned work = gblocks(ctx->ne, M::EPC);
+  if (cgmode) {
+    auto k = k_mass_pc2<P, NC, true>;
+    CK(smem_attr(k, M::bytes));
+    static unsigned grid = 0;
+    if (!grid) grid = persistent_grid(k, 128, M::bytes, 1ll << 40);
+    prof_begin(ctx, K_MASS);
+    k<<<std::min(grid, work), 128, M::bytes, ctx->stream>>>(a);
+    prof_end(ctx);
+  } else {
+    auto k = k_mass_pc2<P, NC, false>;
+    CK(smem_attr(k, M::bytes));
+    static unsigned grid = 0;
+    if (!grid) grid = persistent_grid(k, 128, M::bytes, 1ll << 40);
+    k<<<std::min(grid, work), 128, M::bytes, ctx->stream>>>(a);
+  }
+  CKL();
+  return HX_OK;
+}
+
+static int g_mass_variant = -1;  // HX_MASS_KERNEL=column|line|pc|pc2 (default pc2)
 
 template <int P, int NC>
 static int launch_mass3d(hx_ctx* ctx, bool cgmode, const MassArgs& a) {
   if (g_mass_variant < 0) {
     const char* v = getenv("HX_MASS_KERNEL");
-    g_mass_variant = (v && strcmp(v, "column") == 0) ? 0 : 1;
+    g_mass_variant = 2;
+    if (v && strcmp(v, "pc2") == 0) g_mass_variant = 3;
+    if (v && strcmp(v, "column") == 0) g_mass_variant = 0;
+    if (v && strcmp(v, "line") == 0) g_mass_variant = 1;
+    if (v && strcmp(v, "pc") == 0) g_mass_variant = 2;
   }
+  if (g_mass_variant == 3 && P <= 3) return launch_mass_pc2<P, NC>(ctx, cgmode, a);
+  if (g_mass_variant == 2 && P <= 3) return launch_mass_pc<P, NC>(ctx, cgmode, a);
   if (g_mass_variant == 1) return launch_mass3w<P, NC>(ctx, cgmode, a);
   constexpr int Q = P + 2, D1 = P + 1, EPB = 128 / (Q * Q);
   const size_t bytes = sizeof(double) * EPB * NC * (D1 * D1 * D1 + D1 * D1 * Q + D1 * Q * Q);

@@ -855,6 +855,386 @@ __global__ void __launch_bounds__(128, MINB) k_mass3w(MassArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// 3D PA mass, "plane + column" decomposition.  A thread owns one (component,
+// z-plane) of an element and runs the x and y contractions of that plane in
+// registers (basis entries are warp-uniform constant-bank operands); threads
+// owning (qx, qy) columns then run z, the point scaling D and z^T on all
+// components at once (one D column load serves NC components).  Shared memory only
+// carries the (Q x Q) plane images between the two phases: 4 * NC * D1 * Q^2
+// doubles per element, odd plane stride -> conflict-free.  Persistent CTAs.
+template <int P, int NC>
+struct MassPC {
+  static constexpr int D1 = P + 1, Q = P + 2, QQ = Q * Q;
+  static constexpr int PLN = NC * D1;       // planes per element
+  static constexpr int EPC = 128 / PLN;     // elements per CTA pass
+  static constexpr int TS = NC * D1 * QQ;   // smem doubles per element (plane stride QQ is odd for odd Q...)
+  static constexpr size_t bytes = sizeof(double) * EPC * TS;
+};
+
+template <int P, int NC, bool CG>
+__global__ void __launch_bounds__(128, 4) k_mass_pc(MassArgs a) {
+  using M = MassPC<P, NC>;
+  constexpr int D1 = P + 1, Q = P + 2, NL = D1 * D1 * D1, NQ = Q * Q * Q, QQ = Q * Q, DD = D1 * D1;
+  constexpr int PLN = M::PLN, EPC = M::EPC, TS = M::TS;
+  const double* cB = c_B[P - 1];
+  extern __shared__ double smem[];
+  __shared__ double red[32];
+  __shared__ int sflag;
+  if (CG && !a.cg->active) return;
+  const int t = threadIdx.x;
+  double acc = 0.0;
+  double beta = 0.0;
+  const double* po = nullptr;
+  if constexpr (CG) {
+    beta = a.cg->beta;
+    po = (a.cg->it & 1) ? a.pbuf0 : a.pbuf1;
+  }
+  const int pe = t / PLN, pr = t - pe * PLN;
+  const int pc = pr / D1, pz = pr - pc * D1;  // plane: component pc, z index pz
+  for (long long e0 = (long long)blockIdx.x * EPC; e0 < a.ne; e0 += (long long)gridDim.x * EPC) {
+    const long long e = e0 + pe;
+    const bool pact = pe < EPC && e < a.ne;
+    double* T = smem + pe * TS + pr * QQ;
+    // ---- phase 1 (planes): gather, x and y contractions in registers
+    if (pact) {
+      const int* em = a.emap + e * NL + pz * DD;
+      long long nd[DD];
+#pragma unroll
+      for (int k = 0; k < DD; ++k) nd[k] = __ldg(em + k);
+      double u[DD];
+      if constexpr (CG) {
+        double zv[DD], pv[DD];
+        uint8_t mk[DD], ow[DD];
+#pragma unroll
+        for (int k = 0; k < DD; ++k) {
+          zv[k] = __ldcg(a.x + nd[k] * NC + pc);
+          pv[k] = __ldcg(po + nd[k] * NC + pc);
+          mk[k] = a.mask ? a.mask[nd[k] * NC + pc] : 0;
+          ow[k] = a.own[e * NL + pz * DD + k];
+        }
+#pragma unroll
+        for (int k = 0; k < DD; ++k) {
+          const double p = __dadd_rn(zv[k], __dmul_rn(beta, pv[k]));
+          if (mk[k] && ow[k]) acc = fma(p, p, acc);
+          u[k] = mk[k] ? 0.0 : p;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < DD; ++k) u[k] = a.x[nd[k] * NC + pc];
+      }
+      double v[D1][Q];  // after x: v[dy][qx]
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx) {
+          double s = 0.0;
+#pragma unroll
+          for (int dx = 0; dx < D1; ++dx) s = fma(cB[qx * D1 + dx], u[dy * D1 + dx], s);
+          v[dy][qx] = s;
+        }
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy)
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx) {
+          double s = 0.0;
+#pragma unroll
+          for (int dy = 0; dy < D1; ++dy) s = fma(cB[qy * D1 + dy], v[dy][qx], s);
+          T[qy * Q + qx] = s;
+        }
+    }
+    __syncthreads();
+    // ---- phase 2 (columns): z, D, z^T for all components of a (qx, qy) column
+    for (int it = t; it < EPC * QQ; it += 128) {
+      const int ce = it / QQ, l = it - ce * QQ;
+      const long long ee = e0 + ce;
+      if (ee >= a.ne) continue;
+      double Dq[Q];
+#pragma unroll
+      for (int qz = 0; qz < Q; ++qz) Dq[qz] = __ldg(a.D + ee * NQ + qz * QQ + l);
+      double* base = smem + ce * TS + l;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        double col[D1];
+#pragma unroll
+        for (int dz = 0; dz < D1; ++dz) col[dz] = base[(c * D1 + dz) * QQ];
+        double w[Q];
+#pragma unroll
+        for (int qz = 0; qz < Q; ++qz) {
+          double s = 0.0;
+#pragma unroll
+          for (int dz = 0; dz < D1; ++dz) s = fma(cB[qz * D1 + dz], col[dz], s);
+          const double du = s * Dq[qz];
+          if constexpr (CG) acc = fma(du, s, acc);
+          w[qz] = du;
+        }
+#pragma unroll
+        for (int dz = 0; dz < D1; ++dz) {
+          double s = 0.0;
+#pragma unroll
+          for (int qz = 0; qz < Q; ++qz) s = fma(cB[qz * D1 + dz], w[qz], s);
+          base[(c * D1 + dz) * QQ] = s;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- phase 3 (planes): y^T, x^T in registers, node-sorted E-vector out
+    if (pact) {
+      double Tq[QQ];
+#pragma unroll
+      for (int k = 0; k < QQ; ++k) Tq[k] = T[k];
+      double v[D1][Q];  // after y^T: v[dy][qx]
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx) {
+          double s = 0.0;
+#pragma unroll
+          for (int qy = 0; qy < Q; ++qy) s = fma(cB[qy * D1 + dy], Tq[qy * Q + qx], s);
+          v[dy][qx] = s;
+        }
+      const int* sl = a.slot + e * NL + pz * DD;
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < D1; ++dx) {
+          double s = 0.0;
+#pragma unroll
+          for (int qx = 0; qx < Q; ++qx) s = fma(cB[qx * D1 + dx], v[dy][qx], s);
+          a.evec[(long long)__ldg(sl + dy * D1 + dx) * NC + pc] = s;
+        }
+    }
+    __syncthreads();
+  }
+  if constexpr (CG) {
+    const double bs = block_sum<128>(acc, red);
+    if (threadIdx.x == 0) a.partials[blockIdx.x] = bs;
+    if (grid_last_block(&a.cg->cnt[0], &sflag)) {
+      const double pAp = reduce_partials<128>(a.partials, gridDim.x, red);
+      if (threadIdx.x == 0) {
+        a.cg->cnt[0] = 0;
+        if (pAp <= 0.0) {
+          a.cg->code = 3;
+          a.cg->active = 0;
+        } else {
+          a.cg->alpha = a.cg->rz / pAp;
+        }
+      }
+    }
+  }
+}
+
+// Same plane + column decomposition with coalesced global I/O: the gather and the
+// E-vector scatter are done cooperatively by the whole CTA with lanes over
+// (node, component) -- x-adjacent nodes of an element are adjacent in memory on
+// structured meshes -- and staged through a padded shared-memory image
+// (plane stride DD+1, odd).
+template <int P, int NC>
+struct MassPC2 {
+  static constexpr int D1 = P + 1, Q = P + 2, QQ = Q * Q, DD = D1 * D1, NL = D1 * DD;
+  static constexpr int PLN = NC * D1;
+  static constexpr int EPC = 128 / PLN;
+  static constexpr int GS = PLN * (DD + 1);   // staged nodal image per element
+  static constexpr int TS = PLN * QQ;         // plane images per element
+  static constexpr size_t bytes = sizeof(double) * EPC * (GS + TS);
+};
+
+template <int P, int NC, bool CG>
+__global__ void __launch_bounds__(128, 4) k_mass_pc2(MassArgs a) {
+  using M = MassPC2<P, NC>;
+  constexpr int D1 = P + 1, Q = P + 2, NL = D1 * D1 * D1, NQ = Q * Q * Q, QQ = Q * Q, DD = D1 * D1;
+  constexpr int PLN = M::PLN, EPC = M::EPC, TS = M::TS, GS = M::GS;
+  const double* cB = c_B[P - 1];
+  extern __shared__ double smem[];
+  double* sG = smem;              // [EPC][PLN][DD+1]
+  double* sT = smem + EPC * GS;   // [EPC][PLN][QQ]
+  __shared__ double red[32];
+  __shared__ int sflag;
+  if (CG && !a.cg->active) return;
+  const int t = threadIdx.x;
+  double acc = 0.0;
+  double beta = 0.0;
+  const double* po = nullptr;
+  if constexpr (CG) {
+    beta = a.cg->beta;
+    po = (a.cg->it & 1) ? a.pbuf0 : a.pbuf1;
+  }
+  const int pe = t / PLN, pr = t - pe * PLN;  // plane pr = c * D1 + dz
+  for (long long e0 = (long long)blockIdx.x * EPC; e0 < a.ne; e0 += (long long)gridDim.x * EPC) {
+    const int nel = (int)((a.ne - e0) < EPC ? (a.ne - e0) : EPC);
+    // ---- phase 0: cooperative gather -> sG.  Items (el, c, l) with l fastest (x-adjacent
+    // nodes are adjacent in memory; conflict-free smem writes); all index loads, then
+    // all value loads are issued before any use.
+    constexpr int GI = EPC * NC * NL, GR = (GI + 127) / 128;
+    {
+      int nd[GR];
+#pragma unroll
+      for (int r = 0; r < GR; ++r) {
+        const int it = t + 128 * r;
+        const int el = it / (NC * NL), q = it - el * (NC * NL), l = q % NL;
+        nd[r] = (it < GI && el < nel) ? __ldg(a.emap + (e0 + el) * NL + l) : -1;
+      }
+      double zv[GR], pv[GR];
+      uint8_t mk[GR], ow[GR];
+#pragma unroll
+      for (int r = 0; r < GR; ++r) {
+        const int it = t + 128 * r;
+        const int el = it / (NC * NL), q = it - el * (NC * NL), c = q / NL, l = q - c * NL;
+        if (nd[r] >= 0) {
+          zv[r] = __ldcg(a.x + (long long)nd[r] * NC + c);
+          if constexpr (CG) {
+            pv[r] = __ldcg(po + (long long)nd[r] * NC + c);
+            mk[r] = a.mask ? a.mask[(long long)nd[r] * NC + c] : 0;
+            ow[r] = a.own[(e0 + el) * NL + l];
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < GR; ++r) {
+        const int it = t + 128 * r;
+        const int el = it / (NC * NL), q = it - el * (NC * NL), c = q / NL, l = q - c * NL;
+        if (nd[r] >= 0) {
+          double val = zv[r];
+          if constexpr (CG) {
+            const double p = __dadd_rn(zv[r], __dmul_rn(beta, pv[r]));
+            if (mk[r] && ow[r]) acc = fma(p, p, acc);
+            val = mk[r] ? 0.0 : p;
+          }
+          const int dz = l / DD, k = l - dz * DD;
+          sG[el * GS + (c * D1 + dz) * (DD + 1) + k] = val;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- phase 1 (planes): x and y contractions in registers -> sT
+    const bool pact = pe < nel;
+    if (pact) {
+      const double* g = sG + pe * GS + pr * (DD + 1);
+      double u[DD];
+#pragma unroll
+      for (int k = 0; k < DD; ++k) u[k] = g[k];
+      double v[D1][Q];
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx) {
+          double s = 0.0;
+#pragma unroll
+          for (int dx = 0; dx < D1; ++dx) s = fma(cB[qx * D1 + dx], u[dy * D1 + dx], s);
+          v[dy][qx] = s;
+        }
+      double* T = sT + pe * TS + pr * QQ;
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy)
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx) {
+          double s = 0.0;
+#pragma unroll
+          for (int dy = 0; dy < D1; ++dy) s = fma(cB[qy * D1 + dy], v[dy][qx], s);
+          T[qy * Q + qx] = s;
+        }
+    }
+    __syncthreads();
+    // ---- phase 2 (columns): z, D, z^T for all components of a (qx, qy) column
+    for (int it = t; it < nel * QQ; it += 128) {
+      const int ce = it / QQ, l = it - ce * QQ;
+      const long long ee = e0 + ce;
+      double Dq[Q];
+#pragma unroll
+      for (int qz = 0; qz < Q; ++qz) Dq[qz] = __ldg(a.D + ee * NQ + qz * QQ + l);
+      double* base = sT + ce * TS + l;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        double col[D1];
+#pragma unroll
+        for (int dz = 0; dz < D1; ++dz) col[dz] = base[(c * D1 + dz) * QQ];
+        double w[Q];
+#pragma unroll
+        for (int qz = 0; qz < Q; ++qz) {
+          double s = 0.0;
+#pragma unroll
+          for (int dz = 0; dz < D1; ++dz) s = fma(cB[qz * D1 + dz], col[dz], s);
+          const double du = s * Dq[qz];
+          if constexpr (CG) acc = fma(du, s, acc);
+          w[qz] = du;
+        }
+#pragma unroll
+        for (int dz = 0; dz < D1; ++dz) {
+          double s = 0.0;
+#pragma unroll
+          for (int qz = 0; qz < Q; ++qz) s = fma(cB[qz * D1 + dz], w[qz], s);
+          base[(c * D1 + dz) * QQ] = s;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- phase 3 (planes): y^T, x^T in registers -> sG (reused as the output image)
+    if (pact) {
+      const double* T = sT + pe * TS + pr * QQ;
+      double Tq[QQ];
+#pragma unroll
+      for (int k = 0; k < QQ; ++k) Tq[k] = T[k];
+      double v[D1][Q];
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx) {
+          double s = 0.0;
+#pragma unroll
+          for (int qy = 0; qy < Q; ++qy) s = fma(cB[qy * D1 + dy], Tq[qy * Q + qx], s);
+          v[dy][qx] = s;
+        }
+      double* g = sG + pe * GS + pr * (DD + 1);
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < D1; ++dx) {
+          double s = 0.0;
+#pragma unroll
+          for (int qx = 0; qx < Q; ++qx) s = fma(cB[qx * D1 + dx], v[dy][qx], s);
+          g[dy * D1 + dx] = s;
+        }
+    }
+    __syncthreads();
+    // ---- phase 4: cooperative node-sorted E-vector write (slot loads first)
+    {
+      int so[GR];
+#pragma unroll
+      for (int r = 0; r < GR; ++r) {
+        const int it = t + 128 * r;
+        const int el = it / (NC * NL), q = it - el * (NC * NL), l = q % NL;
+        so[r] = (it < GI && el < nel) ? __ldg(a.slot + (e0 + el) * NL + l) : -1;
+      }
+#pragma unroll
+      for (int r = 0; r < GR; ++r) {
+        const int it = t + 128 * r;
+        const int el = it / (NC * NL), q = it - el * (NC * NL), c = q / NL, l = q - c * NL;
+        if (so[r] >= 0) {
+          const int dz = l / DD, k = l - dz * DD;
+          a.evec[(long long)so[r] * NC + c] = sG[el * GS + (c * D1 + dz) * (DD + 1) + k];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if constexpr (CG) {
+    const double bs = block_sum<128>(acc, red);
+    if (threadIdx.x == 0) a.partials[blockIdx.x] = bs;
+    if (grid_last_block(&a.cg->cnt[0], &sflag)) {
+      const double pAp = reduce_partials<128>(a.partials, gridDim.x, red);
+      if (threadIdx.x == 0) {
+        a.cg->cnt[0] = 0;
+        if (pAp <= 0.0) {
+          a.cg->code = 3;
+          a.cg->active = 0;
+        } else {
+          a.cg->alpha = a.cg->rz / pAp;
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // node-side kernels: deterministic G^T through the transpose map
 
 // E is node-sorted: the entries of node n are E[off[n]..off[n+1]) in ascending element
