@@ -183,6 +183,86 @@ def run_reference(args, rank):
 # B200 arm
 
 
+def run_distributed(args, world, rank, local):
+    """N>1: one brick of n^3 elements per rank (weak scaling) of a global Sedov mesh;
+    element work on the device, shared-node halo sums and CG/CFL scalars over NCCL
+    (paper_2112_07075_b200.distributed)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2112_07075_b200 import problems
+    from paper_2112_07075_b200.distributed import DeviceOps, DistributedLagrange
+    from paper_2112_07075_b200.fespace import cartesian_mesh
+    from paper_2112_07075_b200.hydro import LagrangeHydro, MaterialModel, ViscosityModel, box_velocity_bc
+    from paper_2112_07075_b200.partition import brick_partition, rank_grid
+    from paper_2112_07075_b200.tensor_basis import gauss_legendre
+
+    d, p, n = 3, args.p, args.n
+    # choose global counts so that every brick is n^3
+    counts = [n, n, n]
+    gg = [1, 1, 1]
+    f = world
+    ax = 0
+    while f > 1:
+        gg[ax % 3] *= 2
+        f //= 2
+        ax += 1
+    counts = [n * gg[a] for a in range(3)]
+    gmesh = cartesian_mesh(d, (1.0,) * d, counts, p)
+    mask = box_velocity_bc(gmesh)
+    ghy = LagrangeHydro(gmesh, gauss_legendre(p + 2), MaterialModel(1.4), ViscosityModel(0.5, 2.0), bc_mask=mask)
+    st0 = ghy.initial_state(*problems.sedov(d, (1.0,) * d, counts))
+    _, subs = brick_partition(d, (1.0,) * d, counts, p, world, bc_mask_global=mask)
+    sub = subs[rank]
+    nt = max(p, 1) ** d
+    T = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+    x, v = T(st0.x[sub.l2g]), T(st0.v[sub.l2g])
+    e = T(np.asarray(st0.e).reshape(-1, nt)[sub.g_elems].reshape(-1))
+    q0 = T(np.asarray(st0.qdata0)[:, sub.g_elems])
+    dl = DistributedLagrange(sub, DeviceOps(sub, 1.4, 0.5, 2.0), 1.4, device="cuda")
+    dl.begin_phase(x, q0)
+    t = 0.0
+    V_global = d * gmesh.num_nodes
+
+    def step():
+        nonlocal x, v, e, t
+        dt = dl.timestep_estimate(x, v, e, q0, t, args.cfl, dt_max=1.0, t_final=1e9)
+        (x, v, e, t), _ = dl.rk2_step(x, v, e, q0, t, dt)
+
+    for _ in range(args.warmup):
+        step()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    dist.barrier()
+    torch.cuda.synchronize()
+    tot = 0.0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            step()
+            ev1.record(stream)
+            ev1.synchronize()
+            tot += ev0.elapsed_time(ev1)
+    tt = torch.tensor([tot], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    tot = float(tt.item())
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": V_global * args.steps / (tot / 1e3) / 1e6, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"3D Sedov blast Q{p}-Q{p - 1}, {n}^3 hex elements per GPU, global {counts}, "
+                                   f"CFL {args.cfl}", "global_batch": V_global, "seq_len": None,
+                       "parallelism": f"domain decomposition {list(sub.grid)} (NCCL halo + allreduce, "
+                                      "host-driven CG)", "l2": "flushed before every timed step"},
+            "e2e": None, "gpu_launches": None, "roofline": None, "cpu_baseline": None, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -215,6 +295,10 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    if world > 1:
+        run_distributed(args, world, rank, local)
+        return
 
     from paper_2112_07075_b200 import _lib, problems
     from paper_2112_07075_b200.fespace import cartesian_mesh
