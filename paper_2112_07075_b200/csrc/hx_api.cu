@@ -31,6 +31,8 @@ struct hx_ctx {
   double *B = nullptr, *G = nullptr, *Bt = nullptr, *wnd = nullptr, *psi1 = nullptr;
   // restriction
   int *emap = nullptr, *off = nullptr, *idx = nullptr, *slot = nullptr;
+  int* emapf = nullptr;      // packed CG element map (node | owner | mask) of the phase mask
+  int* emapf_api = nullptr;  // the same for hx_mass_cg calls (rebuilt per call)
   uint8_t* own = nullptr;
   // workspaces
   double* evec = nullptr;     // (NE, nl, d)
@@ -277,59 +279,32 @@ static int launch_mass_pc(hx_ctx* ctx, bool cgmode, const MassArgs& a) {
 }
 
 template <int P, int NC>
-static int launch_mass_pc2(hx_ctx* ctx, bool cgmode, const MassArgs& a) {
-  using M = MassPC2<P, NC>;
-  const unsigned work = gblocks(ctx->ne, M::EPC);
-  if (cgmode) {
-    auto k = k_mass_pc2<P, NC, true>;
-    CK(smem_attr(k, M::bytes));
-    static unsigned grid = 0;
-    if (!grid) grid = persistent_grid(k, 128, M::bytes, 1ll << 40);
-    prof_begin(ctx, K_MASS);
-    k<<<std::min(grid, work), 128, M::bytes, ctx->stream>>>(a);
-    prof_end(ctx);
-  } else {
-    auto k = k_mass_pc2<P, NC, false>;
-    CK(smem_attr(k, M::bytes));
-    static unsigned grid = 0;
-    if (!grid) grid = persistent_grid(k, 128, M::bytes, 1ll << 40);
-    k<<<std::min(grid, work), 128, M::bytes, ctx->stream>>>(a);
-  }
+static int launch_mass_tma(hx_ctx* ctx, const MassArgs& a) {
+  using M = MassTMA<P, NC>;
+  auto k = k_mass_tma<P, NC>;
+  CK(smem_attr(k, M::bytes));
+  static unsigned grid = 0;
+  if (!grid) grid = persistent_grid(k, 128, M::bytes, 1ll << 40);
+  prof_begin(ctx, K_MASS);
+  k<<<std::min(grid, gblocks(ctx->ne, M::EPC)), 128, M::bytes, ctx->stream>>>(a);
+  prof_end(ctx);
   CKL();
   return HX_OK;
 }
 
-static int g_mass_variant = -1;  // HX_MASS_KERNEL=column|line|pc|pc2 (default pc2)
+static int g_mass_variant = -1;  // HX_MASS_KERNEL=line|pc|tma (default pc for p<=3; tma: async-pipelined CG variant)
 
 template <int P, int NC>
 static int launch_mass3d(hx_ctx* ctx, bool cgmode, const MassArgs& a) {
   if (g_mass_variant < 0) {
     const char* v = getenv("HX_MASS_KERNEL");
     g_mass_variant = 2;
-    if (v && strcmp(v, "pc2") == 0) g_mass_variant = 3;
-    if (v && strcmp(v, "column") == 0) g_mass_variant = 0;
     if (v && strcmp(v, "line") == 0) g_mass_variant = 1;
-    if (v && strcmp(v, "pc") == 0) g_mass_variant = 2;
+    if (v && strcmp(v, "tma") == 0) g_mass_variant = 3;
   }
-  if (g_mass_variant == 3 && P <= 3) return launch_mass_pc2<P, NC>(ctx, cgmode, a);
-  if (g_mass_variant == 2 && P <= 3) return launch_mass_pc<P, NC>(ctx, cgmode, a);
-  if (g_mass_variant == 1) return launch_mass3w<P, NC>(ctx, cgmode, a);
-  constexpr int Q = P + 2, D1 = P + 1, EPB = 128 / (Q * Q);
-  const size_t bytes = sizeof(double) * EPB * NC * (D1 * D1 * D1 + D1 * D1 * Q + D1 * Q * Q);
-  const unsigned grid = gblocks(ctx->ne, EPB);
-  if (cgmode) {
-    auto k = k_mass3d<P, NC, true>;
-    CK(smem_attr(k, bytes));
-    prof_begin(ctx, K_MASS);
-    k<<<grid, 128, bytes, ctx->stream>>>(a);
-    prof_end(ctx);
-  } else {
-    auto k = k_mass3d<P, NC, false>;
-    CK(smem_attr(k, bytes));
-    k<<<grid, 128, bytes, ctx->stream>>>(a);
-  }
-  CKL();
-  return HX_OK;
+  if (g_mass_variant == 3 && P <= 3 && cgmode) return launch_mass_tma<P, NC>(ctx, a);
+  if (g_mass_variant >= 2 && P <= 3) return launch_mass_pc<P, NC>(ctx, cgmode, a);
+  return launch_mass3w<P, NC>(ctx, cgmode, a);
 }
 
 template <int DIM, int P>
@@ -502,8 +477,8 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   ctx->ne = d->num_elements;
   ctx->nn = d->num_nodes;
   ctx->device = d->device;
-  if ((long long)ctx->ne * ctx->nl >= (1ll << 31)) {
-    int rc = fail(ctx, HX_EINVAL, "mesh too large for 32-bit E-vector indices");
+  if (ctx->nn >= (1ll << 27) || (long long)ctx->ne * ctx->nl >= (1ll << 31)) {
+    int rc = fail(ctx, HX_EINVAL, "mesh too large for 27-bit node ids / 32-bit E-vector indices (split it across ranks)");
     delete ctx;
     return rc;
   }
@@ -586,13 +561,15 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   ok &= dalloc(&ctx->off, nn + 1) == cudaSuccess;
   ok &= dalloc(&ctx->idx, (size_t)ne * nl) == cudaSuccess;
   ok &= dalloc(&ctx->own, (size_t)ne * nl) == cudaSuccess;
-  ok &= dalloc(&ctx->slot, (size_t)ne * nl) == cudaSuccess;
+  ok &= dalloc(&ctx->slot, (size_t)ne * nl + 8) == cudaSuccess;
   ok &= dalloc(&ctx->evec, (size_t)ne * nl * dd) == cudaSuccess;
   ok &= dalloc(&ctx->evec2, (size_t)ne * std::max(nl * dd, nq)) == cudaSuccess;
   ok &= dalloc(&ctx->r, nv) == cudaSuccess;
   ok &= dalloc(&ctx->z, nv) == cudaSuccess;
-  ok &= dalloc(&ctx->p0, nv) == cudaSuccess;
-  ok &= dalloc(&ctx->p1, nv) == cudaSuccess;
+  ok &= dalloc(&ctx->p0, 2 * nv) == cudaSuccess;  // interleaved (z, p) pairs
+  ok &= dalloc(&ctx->p1, 2 * nv) == cudaSuccess;
+  ok &= dalloc(&ctx->emapf, (size_t)ne * nl + 8) == cudaSuccess;
+  ok &= dalloc(&ctx->emapf_api, (size_t)ne * nl + 8) == cudaSuccess;
   ok &= dalloc(&ctx->partials, 2 * (size_t)std::max<long long>(gblocks(3 * nn, 256), gblocks(ne, 1)) + 64) == cudaSuccess;
   ok &= dalloc(&ctx->cg, 2) == cudaSuccess;
   ok &= dalloc(&ctx->t_dev, 1) == cudaSuccess;
@@ -602,7 +579,7 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   ok &= dalloc(&ctx->st, 4) == cudaSuccess;
   ok &= dalloc(&ctx->dt, 2) == cudaSuccess;
   ok &= dalloc(&ctx->scal, 16) == cudaSuccess;
-  ok &= dalloc(&ctx->Dm, (size_t)ne * nq) == cudaSuccess;
+  ok &= dalloc(&ctx->Dm, (size_t)ne * nq + 8) == cudaSuccess;
   ok &= dalloc(&ctx->qd0, (size_t)ne * nq) == cudaSuccess;
   ok &= dalloc(&ctx->minv, (size_t)ne * ctx->nt * ctx->nt) == cudaSuccess;
   ok &= dalloc(&ctx->mdiag, nn) == cudaSuccess;
@@ -664,7 +641,7 @@ extern "C" int hx_destroy(hx_ctx* ctx) {
   if (!ctx) return HX_OK;
   cudaSetDevice(ctx->device);
   void* dev[] = {ctx->B,  ctx->G,    ctx->Bt,   ctx->wnd,  ctx->psi1, ctx->emap, ctx->off,   ctx->idx,
-                 ctx->own, ctx->slot, ctx->evec, ctx->evec2, ctx->r,   ctx->z,    ctx->p0,   ctx->p1,    ctx->partials,
+                 ctx->own, ctx->slot, ctx->emapf, ctx->emapf_api, ctx->evec, ctx->evec2, ctx->r,   ctx->z,    ctx->p0,   ctx->p1,    ctx->partials,
                  ctx->hist, ctx->cg,  ctx->st,   ctx->dt,   ctx->scal, ctx->Dm,   ctx->qd0,   ctx->minv,
                  ctx->mdiag, ctx->invd, ctx->mask, ctx->xm, ctx->vm,   ctx->em,   ctx->dv0,   ctx->dv1,
                  ctx->de0, ctx->de1, ctx->hx_x, ctx->hx_v, ctx->hx_e, ctx->hx_xo, ctx->hx_vo, ctx->hx_eo};
@@ -772,7 +749,7 @@ extern "C" int hx_mass_create(hx_ctx* ctx, const double* D, hx_mass** out) {
   if (!ctx || !D || !out) return HX_EINVAL;
   CK(cudaSetDevice(ctx->device));
   hx_mass* m = new hx_mass{ctx, nullptr};
-  if (dalloc(&m->D, (size_t)ctx->ne * ctx->nq) != cudaSuccess) {
+  if (dalloc(&m->D, (size_t)ctx->ne * ctx->nq + 8) != cudaSuccess) {  // +pad: bulk copies read 16-B spans
     delete m;
     return fail(ctx, HX_ECUDA, "alloc");
   }
@@ -833,9 +810,16 @@ struct CGLaunch {
   int nc;
 };
 
+static int build_emapf(hx_ctx* ctx, const uint8_t* mask, int nc, int* out) {
+  const long long n = ctx->ne * ctx->nl;
+  k_build_emapf<<<gblocks(n, 256), 256, 0, ctx->stream>>>(ctx->emap, ctx->own, mask, nc, n, out);
+  CKL();
+  return HX_OK;
+}
+
 static int cg_prepare(hx_ctx* ctx, CGDev* cg, const double* D, const double* rhs, const double* evec_rhs, int negate,
                       const uint8_t* mask, const double* invd, double rel_tol, int max_iter, double* x, int nc,
-                      double* hist, CGLaunch& L) {
+                      double* hist, CGLaunch& L, const int* emapf) {
   if (hist == nullptr) {
     if (ctx->hist_len < max_iter + 1) {
       if (ctx->hist) cudaFree(ctx->hist);
@@ -874,6 +858,7 @@ static int cg_prepare(hx_ctx* ctx, CGDev* cg, const double* D, const double* rhs
   ma.own = ctx->own;
   ma.D = D;
   ma.emap = ctx->emap;
+  ma.emapf = emapf;
   ma.slot = ctx->slot;
   ma.B = ctx->B;
   ma.ne = ctx->ne;
@@ -932,10 +917,11 @@ static void cg_info_from(const CGDev& g, hx_cg_info* info) {
 
 static int run_cg(hx_ctx* ctx, const double* D, const double* rhs, const double* evec_rhs, int negate,
                   const uint8_t* mask, const double* invd, double rel_tol, int max_iter, double* x, int nc,
-                  double* hist, hx_cg_info* info, CGDev* cg = nullptr) {
+                  double* hist, hx_cg_info* info, CGDev* cg = nullptr, const int* emapf = nullptr) {
   if (!cg) cg = ctx->cg;
+  if (!emapf) emapf = ctx->emapf;
   CGLaunch L;
-  int rc = cg_prepare(ctx, cg, D, rhs, evec_rhs, negate, mask, invd, rel_tol, max_iter, x, nc, hist, L);
+  int rc = cg_prepare(ctx, cg, D, rhs, evec_rhs, negate, mask, invd, rel_tol, max_iter, x, nc, hist, L, emapf);
   if (rc) return rc;
   rc = cg_launch_init(ctx, L);
   if (rc) return rc;
@@ -1007,8 +993,11 @@ extern "C" int hx_mass_cg(hx_mass* m, const double* rhs, int ncomp, const uint8_
   const long long nv = ctx->nn * ncomp;
   k_recip<<<gblocks(nv, 256), 256, 0, ctx->stream>>>(precond_diag, nv, invd);
   CKL();
+  int rc = build_emapf(ctx, bcmask, ncomp, ctx->emapf_api);
+  if (rc) return rc;
   hx_cg_info ci{};
-  int rc = run_cg(ctx, m->D, rhs, nullptr, 0, bcmask, invd, rel_tol, max_iter, x, ncomp, residuals, &ci, ctx->cg);
+  rc = run_cg(ctx, m->D, rhs, nullptr, 0, bcmask, invd, rel_tol, max_iter, x, ncomp, residuals, &ci, ctx->cg,
+              ctx->emapf_api);
   if (rc) return rc;
   CK(cudaStreamSynchronize(ctx->stream));
   if (info) *info = ci;
@@ -1086,6 +1075,11 @@ extern "C" int hx_phase_begin(hx_ctx* ctx, const double* x, const double* qdata0
   ctx->has_mask = bcmask != nullptr;
   k_invdiag<<<gblocks(nv, 256), 256, 0, ctx->stream>>>(ctx->mdiag, ctx->mask, ctx->dim, ctx->nn, ctx->invd);
   CKL();
+  rc = build_emapf(ctx, ctx->has_mask ? ctx->mask : nullptr, ctx->dim, ctx->emapf);
+  if (rc) return rc;
+  for (auto& g : ctx->graphs)  // graphs captured against the previous phase are stale
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  ctx->graphs.clear();
   rc = dispatch<LaunchMinv>(ctx, minv_out);
   if (rc) return rc;
   if (mass_diag_out) CK(cudaMemcpyAsync(mass_diag_out, ctx->mdiag, sizeof(double) * ctx->nn, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1295,7 +1289,7 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
     if (r) return r;
     CGLaunch L0;
     r = cg_prepare(ctx, ctx->cg, ctx->Dm, nullptr, ctx->evec, 1, mask, ctx->invd, prm->rel_tol, prm->max_iter,
-                   ctx->dv0, ctx->dim, nullptr, L0);
+                   ctx->dv0, ctx->dim, nullptr, L0, ctx->emapf);
     if (r) return r;
     r = cg_capture(ctx, L0);
     if (r) return r;
@@ -1311,7 +1305,7 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
     if (r) return r;
     CGLaunch L1;
     r = cg_prepare(ctx, ctx->cg + 1, ctx->Dm, nullptr, ctx->evec, 1, mask, ctx->invd, prm->rel_tol,
-                   prm->max_iter, ctx->dv1, ctx->dim, nullptr, L1);
+                   prm->max_iter, ctx->dv1, ctx->dim, nullptr, L1, ctx->emapf);
     if (r) return r;
     r = cg_capture(ctx, L1);
     if (r) return r;

@@ -323,18 +323,31 @@ struct CGDev {
   int use_cond;
 };
 
+// Packed element map used by the CG kernels: node id | owner<<27 | wall-mask(c)<<(28+c)
+// (one load per local node instead of node id + owner byte + mask byte).
+__device__ __forceinline__ long long emf_node(int w) { return (long long)(w & 0x07ffffff); }
+__device__ __forceinline__ bool emf_own(int w) { return (w >> 27) & 1; }
+__device__ __forceinline__ bool emf_mask(int w, int c) { return (w >> (28 + c)) & 1; }
+
+// CG direction p_k = z_{k-1} + beta p_{k-1} from the interleaved (z, p) pair
+__device__ __forceinline__ double cg_dir(const double* zp, long long j, double beta) {
+  const double2 q = __ldcg(reinterpret_cast<const double2*>(zp) + j);
+  return __dadd_rn(q.x, __dmul_rn(beta, q.y));
+}
+
 // publish the CG "continue" flag to the enclosing WHILE graph node
 __device__ __forceinline__ void cg_publish(const CGDev* g) {
   if (g->use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)g->cond, g->active ? 1u : 0u);
 }
 
 struct MassArgs {
-  const double* x;      // apply: input (NN, NC); cg: z
-  const double* pold;   // cg: p_{k-1} buffers [2]
-  double* pbuf0;
+  const double* x;      // apply: input (NN, NC)
+  const double* pold;   // unused
+  double* pbuf0;        // cg: interleaved (z, p) pairs, ping-pong: iteration k reads pbuf[(k-1)&1]
   double* pbuf1;
   const uint8_t* mask;  // (NN, NC) or null
   const uint8_t* own;   // (NE, nl)
+  const int* emapf;     // cg: packed element map (node | owner | wall mask)
   const double* D;      // (NE, nq)
   const int* emap;
   const int* slot;      // (NE, nl) node-sorted E-vector position
@@ -375,20 +388,22 @@ __global__ void __launch_bounds__(128) k_mass(MassArgs a) {
   const double* po = nullptr;
   if constexpr (CG) {
     beta = a.cg->beta;
-    po = (a.cg->it & 1) ? a.pbuf0 : a.pbuf1;  // p_{k-1} lives in pbuf[(k-1)&1]
+    po = (a.cg->it & 1) ? a.pbuf0 : a.pbuf1;  // (z, p)_{k-1} lives in pbuf[(k-1)&1]
   }
   if (e < a.ne) {
     const int* em = a.emap + e * NL;
     for (int i = lane; i < NL * NC; i += 32) {
       const int l = i / NC, c = i - l * NC;
-      const long long n = em[l];
       double val;
       if constexpr (CG) {
-        const double p = __dadd_rn(pz[n * NC + c], __dmul_rn(beta, po[n * NC + c]));
-        const bool m = a.mask && a.mask[n * NC + c];
-        if (m && a.own[e * NL + l]) acc = fma(p, p, acc);
+        const int w = a.emapf[e * NL + l];
+        const long long n = emf_node(w);
+        const double p = cg_dir(po, n * NC + c, beta);
+        const bool m = emf_mask(w, c);
+        if (m && emf_own(w)) acc = fma(p, p, acc);
         val = m ? 0.0 : p;
       } else {
+        const long long n = em[l];
         val = pz[n * NC + c];
       }
       A[c * NL + l] = val;
@@ -436,202 +451,6 @@ __global__ void __launch_bounds__(128) k_mass(MassArgs a) {
 // register or shared-memory traffic).  hx_create uploads them and refuses a
 // context whose tables differ (they depend only on p: Lobatto nodes, p+2 Gauss points).
 __constant__ double c_B[4][30];
-
-// 3D PA mass with a (qx, qy) column per thread (the z direction lives in registers).
-// A CTA of 128 threads holds EPB = 128 / Q^2 elements.  Same CG fusion as k_mass.
-//   X:  A[dz][dy][qx] = sum_dx B[qx][dx] X[dz][dy][dx]      threads (qx, dy<D1)
-//   Y:  S[dz][qy][qx] = sum_dy B[qy][dy] A[dz][dy][qx]      threads (qx, qy)
-//   Z:  u[qz] = sum_dz B[qz][dz] S[dz][qy][qx]; u *= D; S[dz][qy][qx] = sum_qz B[qz][dz] u[qz]
-//   Y^T: A[dz][dy][qx] = sum_qy B[qy][dy] S[dz][qy][qx]    threads (qx, dy<D1)
-//   X^T: out[dz][dy][dx] = sum_qx B[qx][dx] A[dz][dy][qx]  threads (dx<D1, dy<D1)
-// Latency hiding: the point data D and every gathered value are requested before
-// the first use (all loads of a thread in flight at once).
-template <int P, int NC, bool CG>
-__global__ void __launch_bounds__(128, 5) k_mass3d(MassArgs a) {
-  constexpr int D1 = P + 1, Q = P + 2, Q2 = Q * Q, NL = D1 * D1 * D1, NQ = Q * Q * Q;
-  constexpr int EPB = 128 / Q2;
-  constexpr int SX = NL, SA = D1 * D1 * Q, SB = D1 * Q * Q;
-  constexpr int PER = NC * (SX + SA + SB);
-  constexpr int GR = (NL + Q2 - 1) / Q2;  // gather rounds (nodes per thread)
-  const double* cB = c_B[P - 1];
-  extern __shared__ double smem[];
-  __shared__ double red[32];
-  __shared__ int sflag;
-  if (CG && !a.cg->active) return;
-  const int t = threadIdx.x;
-  const int el = t / Q2, w = t - el * Q2, tx = w % Q, ty = w / Q;
-  const long long e = (long long)blockIdx.x * EPB + el;
-  const bool active = el < EPB && e < a.ne;
-  double* sX = smem + (el < EPB ? el : 0) * PER;
-  double* sA = sX + NC * SX;
-  double* sS = sA + NC * SA;
-  // point data first (independent of everything else)
-  double Dq[Q];
-  if (active) {
-    const double* De = a.D + e * NQ + ty * Q + tx;
-#pragma unroll
-    for (int qz = 0; qz < Q; ++qz) Dq[qz] = __ldg(De + qz * Q2);
-  }
-  double acc = 0.0;
-  if (active) {
-    double beta = 0.0;
-    const double* po = nullptr;
-    if constexpr (CG) {
-      beta = a.cg->beta;
-      po = (a.cg->it & 1) ? a.pbuf0 : a.pbuf1;
-    }
-    const int* em = a.emap + e * NL;
-    long long nd[GR];
-#pragma unroll
-    for (int k = 0; k < GR; ++k) {
-      const int l = w + k * Q2;
-      nd[k] = l < NL ? (long long)__ldg(em + l) : -1;
-    }
-    double zv[GR][NC], pv[GR][NC];
-    uint8_t mk[GR][NC], ow[GR];
-#pragma unroll
-    for (int k = 0; k < GR; ++k) {
-      const int l = w + k * Q2;
-      if (nd[k] >= 0) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          zv[k][c] = __ldcg(a.x + nd[k] * NC + c);
-          if constexpr (CG) {
-            pv[k][c] = __ldcg(po + nd[k] * NC + c);
-            mk[k][c] = a.mask ? a.mask[nd[k] * NC + c] : 0;
-          }
-        }
-        if constexpr (CG) ow[k] = a.own[e * NL + l];
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < GR; ++k) {
-      const int l = w + k * Q2;
-      if (nd[k] >= 0) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          double val = zv[k][c];
-          if constexpr (CG) {
-            const double p = __dadd_rn(zv[k][c], __dmul_rn(beta, pv[k][c]));
-            if (mk[k][c] && ow[k]) acc = fma(p, p, acc);
-            val = mk[k][c] ? 0.0 : p;
-          }
-          sX[c * SX + l] = val;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (active && ty < D1) {  // X
-    double rowx[D1];
-#pragma unroll
-    for (int d = 0; d < D1; ++d) rowx[d] = cB[tx * D1 + d];
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-#pragma unroll
-      for (int dz = 0; dz < D1; ++dz) {
-        const double* src = sX + c * SX + (dz * D1 + ty) * D1;
-        double s = 0.0;
-#pragma unroll
-        for (int dx = 0; dx < D1; ++dx) s = fma(rowx[dx], src[dx], s);
-        sA[c * SA + (dz * D1 + ty) * Q + tx] = s;
-      }
-  }
-  __syncthreads();
-  if (active) {  // Y
-    double rowy[D1];
-#pragma unroll
-    for (int d = 0; d < D1; ++d) rowy[d] = cB[ty * D1 + d];
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-#pragma unroll
-      for (int dz = 0; dz < D1; ++dz) {
-        double s = 0.0;
-#pragma unroll
-        for (int dy = 0; dy < D1; ++dy) s = fma(rowy[dy], sA[c * SA + (dz * D1 + dy) * Q + tx], s);
-        sS[c * SB + (dz * Q + ty) * Q + tx] = s;
-      }
-  }
-  __syncthreads();
-  if (active) {  // Z, D, Z^T in registers; B from the constant bank
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      double col[D1];
-#pragma unroll
-      for (int dz = 0; dz < D1; ++dz) col[dz] = sS[c * SB + (dz * Q + ty) * Q + tx];
-      double u[Q];
-#pragma unroll
-      for (int qz = 0; qz < Q; ++qz) {
-        double s = 0.0;
-#pragma unroll
-        for (int dz = 0; dz < D1; ++dz) s = fma(cB[qz * D1 + dz], col[dz], s);
-        const double du = s * Dq[qz];
-        if constexpr (CG) acc = fma(du, s, acc);
-        u[qz] = du;
-      }
-#pragma unroll
-      for (int dz = 0; dz < D1; ++dz) {
-        double s = 0.0;
-#pragma unroll
-        for (int qz = 0; qz < Q; ++qz) s = fma(cB[qz * D1 + dz], u[qz], s);
-        sS[c * SB + (dz * Q + ty) * Q + tx] = s;
-      }
-    }
-  }
-  __syncthreads();
-  if (active && ty < D1) {  // Y^T
-    double coly[Q];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) coly[q] = cB[q * D1 + ty];
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-#pragma unroll
-      for (int dz = 0; dz < D1; ++dz) {
-        double s = 0.0;
-#pragma unroll
-        for (int qy = 0; qy < Q; ++qy) s = fma(coly[qy], sS[c * SB + (dz * Q + qy) * Q + tx], s);
-        sA[c * SA + (dz * D1 + ty) * Q + tx] = s;
-      }
-  }
-  __syncthreads();
-  if (active && ty < D1 && tx < D1) {  // X^T -> node-sorted E-vector
-    double colx[Q];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) colx[q] = cB[q * D1 + tx];
-    const int* sl = a.slot + e * NL;
-    int so[D1];
-#pragma unroll
-    for (int dz = 0; dz < D1; ++dz) so[dz] = __ldg(sl + (dz * D1 + ty) * D1 + tx);
-#pragma unroll
-    for (int dz = 0; dz < D1; ++dz) {
-      const long long o = (long long)so[dz] * NC;
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const double* src = sA + c * SA + (dz * D1 + ty) * Q;
-        double s = 0.0;
-#pragma unroll
-        for (int qx = 0; qx < Q; ++qx) s = fma(colx[qx], src[qx], s);
-        a.evec[o + c] = s;
-      }
-    }
-  }
-  if constexpr (CG) {
-    const double bs = block_sum<128>(acc, red);
-    if (threadIdx.x == 0) a.partials[blockIdx.x] = bs;
-    if (grid_last_block(&a.cg->cnt[0], &sflag)) {
-      const double pAp = reduce_partials<128>(a.partials, gridDim.x, red);
-      if (threadIdx.x == 0) {
-        a.cg->cnt[0] = 0;
-        if (pAp <= 0.0) {
-          a.cg->code = 3;
-          a.cg->active = 0;
-        } else {
-          a.cg->alpha = a.cg->rz / pAp;
-        }
-      }
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Warp-per-element 3D PA mass ("line" mapping).  Each lane owns whole tensor
@@ -731,42 +550,35 @@ __global__ void __launch_bounds__(128, MINB) k_mass3w(MassArgs a) {
       beta = a.cg->beta;
       po = (a.cg->it & 1) ? a.pbuf0 : a.pbuf1;
     }
-    const int* em = a.emap + e * NL;
-    long long nd[GR];
+    const int* em = (CG ? a.emapf : a.emap) + e * NL;
+    int wd[GR];
 #pragma unroll
     for (int k = 0; k < GR; ++k) {
       const int l = lane + 32 * k;
-      nd[k] = l < NL ? (long long)__ldg(em + l) : -1;
+      wd[k] = l < NL ? __ldg(em + l) : -1;
     }
-    double zv[GR][NC], pv[GR][NC];
-    uint8_t mk[GR][NC], ow[GR];
+    double vv[GR][NC];
 #pragma unroll
     for (int k = 0; k < GR; ++k) {
-      if (nd[k] >= 0) {
+      if (wd[k] >= 0) {
+        const long long n = CG ? emf_node(wd[k]) : (long long)wd[k];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          zv[k][c] = __ldcg(a.x + nd[k] * NC + c);
-          if constexpr (CG) {
-            pv[k][c] = __ldcg(po + nd[k] * NC + c);
-            mk[k][c] = a.mask ? a.mask[nd[k] * NC + c] : 0;
-          }
-        }
-        if constexpr (CG) ow[k] = a.own[e * NL + lane + 32 * k];
+        for (int c = 0; c < NC; ++c) vv[k][c] = CG ? cg_dir(po, n * NC + c, beta) : __ldcg(a.x + n * NC + c);
       }
     }
 #pragma unroll
     for (int k = 0; k < GR; ++k) {
       const int l = lane + 32 * k;
-      if (nd[k] >= 0) {
+      if (wd[k] >= 0) {
         const int dx = l % D1, dy = (l / D1) % D1, dz = l / (D1 * D1);
         const int si = (dz * D1 + dy) * PD + dx;
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-          double val = zv[k][c];
+          double val = vv[k][c];
           if constexpr (CG) {
-            const double p = __dadd_rn(zv[k][c], __dmul_rn(beta, pv[k][c]));
-            if (mk[k][c] && ow[k]) acc = fma(p, p, acc);
-            val = mk[k][c] ? 0.0 : p;
+            const bool m = emf_mask(wd[k], c);
+            if (m && emf_own(wd[k])) acc = fma(val, val, acc);
+            val = m ? 0.0 : val;
           }
           A[c * D1 * D1 * PD + si] = val;
         }
@@ -897,30 +709,24 @@ __global__ void __launch_bounds__(128, 4) k_mass_pc(MassArgs a) {
     double* T = smem + pe * TS + pr * QQ;
     // ---- phase 1 (planes): gather, x and y contractions in registers
     if (pact) {
-      const int* em = a.emap + e * NL + pz * DD;
-      long long nd[DD];
-#pragma unroll
-      for (int k = 0; k < DD; ++k) nd[k] = __ldg(em + k);
       double u[DD];
       if constexpr (CG) {
-        double zv[DD], pv[DD];
-        uint8_t mk[DD], ow[DD];
+        const int* em = a.emapf + e * NL + pz * DD;
+        int wd[DD];
+#pragma unroll
+        for (int k = 0; k < DD; ++k) wd[k] = __ldg(em + k);
+#pragma unroll
+        for (int k = 0; k < DD; ++k) u[k] = cg_dir(po, emf_node(wd[k]) * NC + pc, beta);
 #pragma unroll
         for (int k = 0; k < DD; ++k) {
-          zv[k] = __ldcg(a.x + nd[k] * NC + pc);
-          pv[k] = __ldcg(po + nd[k] * NC + pc);
-          mk[k] = a.mask ? a.mask[nd[k] * NC + pc] : 0;
-          ow[k] = a.own[e * NL + pz * DD + k];
-        }
-#pragma unroll
-        for (int k = 0; k < DD; ++k) {
-          const double p = __dadd_rn(zv[k], __dmul_rn(beta, pv[k]));
-          if (mk[k] && ow[k]) acc = fma(p, p, acc);
-          u[k] = mk[k] ? 0.0 : p;
+          const bool m = emf_mask(wd[k], pc);
+          if (m && emf_own(wd[k])) acc = fma(u[k], u[k], acc);
+          u[k] = m ? 0.0 : u[k];
         }
       } else {
+        const int* em = a.emap + e * NL + pz * DD;
 #pragma unroll
-        for (int k = 0; k < DD; ++k) u[k] = a.x[nd[k] * NC + pc];
+        for (int k = 0; k < DD; ++k) u[k] = a.x[(long long)__ldg(em + k) * NC + pc];
       }
       double v[D1][Q];  // after x: v[dy][qx]
 #pragma unroll
@@ -1023,95 +829,181 @@ __global__ void __launch_bounds__(128, 4) k_mass_pc(MassArgs a) {
   }
 }
 
-// Same plane + column decomposition with coalesced global I/O: the gather and the
-// E-vector scatter are done cooperatively by the whole CTA with lanes over
-// (node, component) -- x-adjacent nodes of an element are adjacent in memory on
-// structured meshes -- and staged through a padded shared-memory image
-// (plane stride DD+1, odd).
+// ---------------------------------------------------------------------------
+// Asynchronous-pipelined 3D PA mass for the CG (plane + column compute as in
+// k_mass_pc).  Per CTA, element groups flow through a 3-stage pipeline:
+//   * TMA bulk copies (cp.async.bulk, mbarrier completion) bring the contiguous
+//     per-group metadata -- packed element map, node-sorted slots, point data D --
+//     for the group after next into a double buffer;
+//   * cp.async 16-byte gathers fetch the next group's (z, p_{k-1}) pairs into a
+//     padded shared image while the current group computes;
+//   * the current group runs x/y (planes, registers), z (columns), y^T/x^T (planes).
+// No register holds in-flight data, so the gather latency overlaps compute.
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1D bulk copy global -> shared, completion counted on bar (16-byte aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 template <int P, int NC>
-struct MassPC2 {
-  static constexpr int D1 = P + 1, Q = P + 2, QQ = Q * Q, DD = D1 * D1, NL = D1 * DD;
+struct MassTMA {
+  static constexpr int D1 = P + 1, Q = P + 2, QQ = Q * Q, DD = D1 * D1, NL = D1 * DD, NQ = Q * Q * Q;
   static constexpr int PLN = NC * D1;
   static constexpr int EPC = 128 / PLN;
-  static constexpr int GS = PLN * (DD + 1);   // staged nodal image per element
-  static constexpr int TS = PLN * QQ;         // plane images per element
-  static constexpr size_t bytes = sizeof(double) * EPC * (GS + TS);
+  // metadata buffer: packed map (int), slots (int), D (double); each region padded for
+  // 16-byte-aligned bulk copies of a possibly unaligned source range
+  static constexpr int META_MAP = (EPC * NL * 4 + 32 + 15) / 16 * 16;
+  static constexpr int META_D = (EPC * NQ * 8 + 32 + 15) / 16 * 16;
+  static constexpr int META = 2 * META_MAP + META_D;   // bytes, multiple of 16
+  static constexpr int GP = DD + 1;                      // gather plane pitch (pairs)
+  static constexpr int GATH = EPC * PLN * GP * 16;       // bytes
+  static constexpr int TIMG = EPC * PLN * QQ * 8;        // bytes
+  static constexpr size_t bytes = 2 * (size_t)META + GATH + TIMG + 64;
 };
 
-template <int P, int NC, bool CG>
-__global__ void __launch_bounds__(128, 4) k_mass_pc2(MassArgs a) {
-  using M = MassPC2<P, NC>;
-  constexpr int D1 = P + 1, Q = P + 2, NL = D1 * D1 * D1, NQ = Q * Q * Q, QQ = Q * Q, DD = D1 * D1;
-  constexpr int PLN = M::PLN, EPC = M::EPC, TS = M::TS, GS = M::GS;
+struct MetaView {
+  const int* map;
+  const int* slot;
+  const double* D;
+};
+
+// issue the bulk copies of group [e0, e0+nel) into metadata buffer `buf`
+template <int P, int NC>
+__device__ __forceinline__ void meta_issue(char* buf, const MassArgs& a, long long e0, int nel,
+                                           unsigned long long* bar) {
+  using M = MassTMA<P, NC>;
+  auto span = [&](const char* src, long long nbytes, char* dst, unsigned& tx) {
+    const unsigned long long lo = (unsigned long long)src & ~15ull;
+    const unsigned long long hi = ((unsigned long long)src + nbytes + 15) & ~15ull;
+    bulk_g2s(dst, (const void*)lo, (unsigned)(hi - lo), bar);
+    tx += (unsigned)(hi - lo);
+  };
+  unsigned tx = 0;
+  // expect_tx must precede the copies' completion; compute sizes first
+  const char* s0 = (const char*)(a.emapf + e0 * M::NL);
+  const char* s1 = (const char*)(a.slot + e0 * M::NL);
+  const char* s2 = (const char*)(a.D + e0 * M::NQ);
+  const long long n0 = (long long)nel * M::NL * 4, n2 = (long long)nel * M::NQ * 8;
+  auto sz = [](const char* src, long long nbytes) {
+    const unsigned long long lo = (unsigned long long)src & ~15ull;
+    const unsigned long long hi = ((unsigned long long)src + nbytes + 15) & ~15ull;
+    return (unsigned)(hi - lo);
+  };
+  mbar_expect_tx(bar, sz(s0, n0) + sz(s1, n0) + sz(s2, n2));
+  span(s0, n0, buf, tx);
+  span(s1, n0, buf + M::META_MAP, tx);
+  span(s2, n2, buf + 2 * M::META_MAP, tx);
+}
+
+template <int P, int NC>
+__device__ __forceinline__ MetaView meta_view(char* buf, const MassArgs& a, long long e0) {
+  using M = MassTMA<P, NC>;
+  MetaView v;
+  v.map = (const int*)(buf + (((unsigned long long)(a.emapf + e0 * M::NL)) & 15ull));
+  v.slot = (const int*)(buf + M::META_MAP + (((unsigned long long)(a.slot + e0 * M::NL)) & 15ull));
+  v.D = (const double*)(buf + 2 * M::META_MAP + (((unsigned long long)(a.D + e0 * M::NQ)) & 15ull));
+  return v;
+}
+
+// cp.async gathers of the (z, p) pairs of group e0 (items (el, c, l), l fastest)
+template <int P, int NC>
+__device__ __forceinline__ void gather_issue(double2* gath, const MetaView& mv, const double* zp, int nel) {
+  using M = MassTMA<P, NC>;
+  constexpr int NL = M::NL, D1 = M::D1, DD = M::DD, GP = M::GP;
+  for (int it = threadIdx.x; it < nel * NC * NL; it += 128) {
+    const int el = it / (NC * NL), q = it - el * (NC * NL), c = q / NL, l = q - c * NL;
+    const long long n = emf_node(mv.map[el * NL + l]);
+    const int dz = l / DD, k = l - dz * DD;
+    cp_async16(gath + (el * M::PLN + c * D1 + dz) * GP + k, zp + (n * NC + c) * 2);
+  }
+  cp_async_commit();
+}
+
+template <int P, int NC>
+__global__ void __launch_bounds__(128, 2) k_mass_tma(MassArgs a) {
+  using M = MassTMA<P, NC>;
+  constexpr int D1 = P + 1, Q = P + 2, NL = M::NL, NQ = M::NQ, QQ = Q * Q, DD = D1 * D1;
+  constexpr int PLN = M::PLN, EPC = M::EPC, GP = M::GP;
   const double* cB = c_B[P - 1];
-  extern __shared__ double smem[];
-  double* sG = smem;              // [EPC][PLN][DD+1]
-  double* sT = smem + EPC * GS;   // [EPC][PLN][QQ]
+  extern __shared__ __align__(16) char smem_raw[];
+  char* metab[2] = {smem_raw, smem_raw + M::META};
+  double2* gath = (double2*)(smem_raw + 2 * M::META);
+  double* sT = (double*)(smem_raw + 2 * M::META + M::GATH);
+  __shared__ __align__(8) unsigned long long bars[2];
   __shared__ double red[32];
   __shared__ int sflag;
-  if (CG && !a.cg->active) return;
+  if (!a.cg->active) return;
   const int t = threadIdx.x;
+  const double beta = a.cg->beta;
+  const double* po = (a.cg->it & 1) ? a.pbuf0 : a.pbuf1;
   double acc = 0.0;
-  double beta = 0.0;
-  const double* po = nullptr;
-  if constexpr (CG) {
-    beta = a.cg->beta;
-    po = (a.cg->it & 1) ? a.pbuf0 : a.pbuf1;
+  const long long stride = (long long)gridDim.x * EPC;
+  const long long first = (long long)blockIdx.x * EPC;
+  auto nel_of = [&](long long e0) { return (int)((a.ne - e0) < EPC ? (a.ne - e0) : EPC); };
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const int pe = t / PLN, pr = t - pe * PLN;  // plane pr = c * D1 + dz
-  for (long long e0 = (long long)blockIdx.x * EPC; e0 < a.ne; e0 += (long long)gridDim.x * EPC) {
-    const int nel = (int)((a.ne - e0) < EPC ? (a.ne - e0) : EPC);
-    // ---- phase 0: cooperative gather -> sG.  Items (el, c, l) with l fastest (x-adjacent
-    // nodes are adjacent in memory; conflict-free smem writes); all index loads, then
-    // all value loads are issued before any use.
-    constexpr int GI = EPC * NC * NL, GR = (GI + 127) / 128;
-    {
-      int nd[GR];
-#pragma unroll
-      for (int r = 0; r < GR; ++r) {
-        const int it = t + 128 * r;
-        const int el = it / (NC * NL), q = it - el * (NC * NL), l = q % NL;
-        nd[r] = (it < GI && el < nel) ? __ldg(a.emap + (e0 + el) * NL + l) : -1;
-      }
-      double zv[GR], pv[GR];
-      uint8_t mk[GR], ow[GR];
-#pragma unroll
-      for (int r = 0; r < GR; ++r) {
-        const int it = t + 128 * r;
-        const int el = it / (NC * NL), q = it - el * (NC * NL), c = q / NL, l = q - c * NL;
-        if (nd[r] >= 0) {
-          zv[r] = __ldcg(a.x + (long long)nd[r] * NC + c);
-          if constexpr (CG) {
-            pv[r] = __ldcg(po + (long long)nd[r] * NC + c);
-            mk[r] = a.mask ? a.mask[(long long)nd[r] * NC + c] : 0;
-            ow[r] = a.own[(e0 + el) * NL + l];
-          }
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < GR; ++r) {
-        const int it = t + 128 * r;
-        const int el = it / (NC * NL), q = it - el * (NC * NL), c = q / NL, l = q - c * NL;
-        if (nd[r] >= 0) {
-          double val = zv[r];
-          if constexpr (CG) {
-            const double p = __dadd_rn(zv[r], __dmul_rn(beta, pv[r]));
-            if (mk[r] && ow[r]) acc = fma(p, p, acc);
-            val = mk[r] ? 0.0 : p;
-          }
-          const int dz = l / DD, k = l - dz * DD;
-          sG[el * GS + (c * D1 + dz) * (DD + 1) + k] = val;
-        }
-      }
+  __syncthreads();
+  if (first < a.ne) {
+    if (t == 0) {
+      meta_issue<P, NC>(metab[0], a, first, nel_of(first), &bars[0]);
+      if (first + stride < a.ne) meta_issue<P, NC>(metab[1], a, first + stride, nel_of(first + stride), &bars[1]);
     }
+    mbar_wait(&bars[0], 0);
+    gather_issue<P, NC>(gath, meta_view<P, NC>(metab[0], a, first), po, nel_of(first));
+  }
+  int i = 0;
+  for (long long e0 = first; e0 < a.ne; e0 += stride, ++i) {
+    const int b = i & 1;
+    const int nel = nel_of(e0);
+    const MetaView mv = meta_view<P, NC>(metab[b], a, e0);
+    cp_async_wait_all();
     __syncthreads();
-    // ---- phase 1 (planes): x and y contractions in registers -> sT
-    const bool pact = pe < nel;
-    if (pact) {
-      const double* g = sG + pe * GS + pr * (DD + 1);
+    // ---- phase 1 (planes): direction update, wall mask, x and y in registers -> sT
+    const int pe = t / PLN, pr = t - pe * PLN, pc = pr / D1, pz = pr - pc * D1;
+    if (pe < nel) {
+      const double2* g = gath + (pe * PLN + pr) * GP;
+      const int* mw = mv.map + pe * NL + pz * DD;
       double u[DD];
 #pragma unroll
-      for (int k = 0; k < DD; ++k) u[k] = g[k];
+      for (int k = 0; k < DD; ++k) {
+        const double2 q = g[k];
+        const double p = __dadd_rn(q.x, __dmul_rn(beta, q.y));
+        const int w = mw[k];
+        const bool m = emf_mask(w, pc);
+        if (m && emf_own(w)) acc = fma(p, p, acc);
+        u[k] = m ? 0.0 : p;
+      }
       double v[D1][Q];
 #pragma unroll
       for (int dy = 0; dy < D1; ++dy)
@@ -1122,7 +1014,7 @@ __global__ void __launch_bounds__(128, 4) k_mass_pc2(MassArgs a) {
           for (int dx = 0; dx < D1; ++dx) s = fma(cB[qx * D1 + dx], u[dy * D1 + dx], s);
           v[dy][qx] = s;
         }
-      double* T = sT + pe * TS + pr * QQ;
+      double* T = sT + (pe * PLN + pr) * QQ;
 #pragma unroll
       for (int qy = 0; qy < Q; ++qy)
 #pragma unroll
@@ -1134,14 +1026,19 @@ __global__ void __launch_bounds__(128, 4) k_mass_pc2(MassArgs a) {
         }
     }
     __syncthreads();
-    // ---- phase 2 (columns): z, D, z^T for all components of a (qx, qy) column
+    // gath is free: prefetch the next group's pairs (its metadata was requested a group ago)
+    const long long e1 = e0 + stride;
+    if (e1 < a.ne) {
+      mbar_wait(&bars[b ^ 1], ((i + 1) >> 1) & 1);
+      gather_issue<P, NC>(gath, meta_view<P, NC>(metab[b ^ 1], a, e1), po, nel_of(e1));
+    }
+    // ---- phase 2 (columns): z, D, z^T for all components (D from the metadata buffer)
     for (int it = t; it < nel * QQ; it += 128) {
       const int ce = it / QQ, l = it - ce * QQ;
-      const long long ee = e0 + ce;
       double Dq[Q];
 #pragma unroll
-      for (int qz = 0; qz < Q; ++qz) Dq[qz] = __ldg(a.D + ee * NQ + qz * QQ + l);
-      double* base = sT + ce * TS + l;
+      for (int qz = 0; qz < Q; ++qz) Dq[qz] = mv.D[ce * NQ + qz * QQ + l];
+      double* base = sT + ce * PLN * QQ + l;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         double col[D1];
@@ -1154,7 +1051,7 @@ __global__ void __launch_bounds__(128, 4) k_mass_pc2(MassArgs a) {
 #pragma unroll
           for (int dz = 0; dz < D1; ++dz) s = fma(cB[qz * D1 + dz], col[dz], s);
           const double du = s * Dq[qz];
-          if constexpr (CG) acc = fma(du, s, acc);
+          acc = fma(du, s, acc);
           w[qz] = du;
         }
 #pragma unroll
@@ -1167,9 +1064,9 @@ __global__ void __launch_bounds__(128, 4) k_mass_pc2(MassArgs a) {
       }
     }
     __syncthreads();
-    // ---- phase 3 (planes): y^T, x^T in registers -> sG (reused as the output image)
-    if (pact) {
-      const double* T = sT + pe * TS + pr * QQ;
+    // ---- phase 3 (planes): y^T, x^T -> node-sorted E-vector (slots from the metadata buffer)
+    if (pe < nel) {
+      const double* T = sT + (pe * PLN + pr) * QQ;
       double Tq[QQ];
 #pragma unroll
       for (int k = 0; k < QQ; ++k) Tq[k] = T[k];
@@ -1183,7 +1080,7 @@ __global__ void __launch_bounds__(128, 4) k_mass_pc2(MassArgs a) {
           for (int qy = 0; qy < Q; ++qy) s = fma(cB[qy * D1 + dy], Tq[qy * Q + qx], s);
           v[dy][qx] = s;
         }
-      double* g = sG + pe * GS + pr * (DD + 1);
+      const int* sl = mv.slot + pe * NL + pz * DD;
 #pragma unroll
       for (int dy = 0; dy < D1; ++dy)
 #pragma unroll
@@ -1191,44 +1088,28 @@ __global__ void __launch_bounds__(128, 4) k_mass_pc2(MassArgs a) {
           double s = 0.0;
 #pragma unroll
           for (int qx = 0; qx < Q; ++qx) s = fma(cB[qx * D1 + dx], v[dy][qx], s);
-          g[dy * D1 + dx] = s;
+          a.evec[(long long)sl[dy * D1 + dx] * NC + pc] = s;
         }
     }
     __syncthreads();
-    // ---- phase 4: cooperative node-sorted E-vector write (slot loads first)
-    {
-      int so[GR];
-#pragma unroll
-      for (int r = 0; r < GR; ++r) {
-        const int it = t + 128 * r;
-        const int el = it / (NC * NL), q = it - el * (NC * NL), l = q % NL;
-        so[r] = (it < GI && el < nel) ? __ldg(a.slot + (e0 + el) * NL + l) : -1;
-      }
-#pragma unroll
-      for (int r = 0; r < GR; ++r) {
-        const int it = t + 128 * r;
-        const int el = it / (NC * NL), q = it - el * (NC * NL), c = q / NL, l = q - c * NL;
-        if (so[r] >= 0) {
-          const int dz = l / DD, k = l - dz * DD;
-          a.evec[(long long)so[r] * NC + c] = sG[el * GS + (c * D1 + dz) * (DD + 1) + k];
-        }
-      }
+    // metadata buffer b is free: request the group after next into it
+    const long long e2 = e0 + 2 * stride;
+    if (t == 0 && e2 < a.ne) {
+      fence_proxy_async();
+      meta_issue<P, NC>(metab[b], a, e2, nel_of(e2), &bars[b]);
     }
-    __syncthreads();
   }
-  if constexpr (CG) {
-    const double bs = block_sum<128>(acc, red);
-    if (threadIdx.x == 0) a.partials[blockIdx.x] = bs;
-    if (grid_last_block(&a.cg->cnt[0], &sflag)) {
-      const double pAp = reduce_partials<128>(a.partials, gridDim.x, red);
-      if (threadIdx.x == 0) {
-        a.cg->cnt[0] = 0;
-        if (pAp <= 0.0) {
-          a.cg->code = 3;
-          a.cg->active = 0;
-        } else {
-          a.cg->alpha = a.cg->rz / pAp;
-        }
+  const double bs = block_sum<128>(acc, red);
+  if (threadIdx.x == 0) a.partials[blockIdx.x] = bs;
+  if (grid_last_block(&a.cg->cnt[0], &sflag)) {
+    const double pAp = reduce_partials<128>(a.partials, gridDim.x, red);
+    if (threadIdx.x == 0) {
+      a.cg->cnt[0] = 0;
+      if (pAp <= 0.0) {
+        a.cg->code = 3;
+        a.cg->active = 0;
+      } else {
+        a.cg->alpha = a.cg->rz / pAp;
       }
     }
   }
@@ -1274,8 +1155,8 @@ struct NodeArgs {
   const double* invd;   // (NN, NC) 1/diag (masked rows -> 1)
   double* x;
   double* r;
-  double* z;
-  double* pbuf0;
+  double* z;            // unused by the CG (z lives in the (z, p) pairs)
+  double* pbuf0;        // interleaved (z, p) pairs, ping-pong
   double* pbuf1;
   const double* rhs;    // cg_init from an explicit rhs (NN, NC) or null
   double* out;          // scatter output
@@ -1319,9 +1200,8 @@ __global__ void __launch_bounds__(256) k_cg_init(NodeArgs a) {
     if (a.mask && a.mask[j]) b = 0.0;
     const double z = a.invd[j] * b;
     a.r[j] = b;
-    a.z[j] = z;
+    reinterpret_cast<double2*>(a.pbuf0)[j] = make_double2(z, 0.0);  // (z_0, p_0 = 0)
     a.x[j] = 0.0;
-    a.pbuf0[j] = 0.0;
     rz = fma(b, z, rz);
     if (b != 0.0 || b != b) nz += 1.0;
   }
@@ -1390,7 +1270,8 @@ __global__ void __launch_bounds__(256, 4) k_cg_node(NodeArgs a) {
   const long long N = a.nn * NC;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long j0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; j0 < N; j0 += U * stride) {
-    double zj[U], pj[U], xj[U], rj[U], dj[U], s[U];
+    double2 zp[U];
+    double xj[U], rj[U], dj[U], s[U];
     bool m[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -1398,8 +1279,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_node(NodeArgs a) {
       if (j < N) {
         const long long n = j / NC;
         const int c = (int)(j - n * NC);
-        zj[u] = __ldcg(a.z + j);
-        pj[u] = __ldcg(po + j);
+        zp[u] = __ldcg(reinterpret_cast<const double2*>(po) + j);
         xj[u] = __ldcg(a.x + j);
         rj[u] = __ldcg(a.r + j);
         dj[u] = __ldg(a.invd + j);
@@ -1411,14 +1291,13 @@ __global__ void __launch_bounds__(256, 4) k_cg_node(NodeArgs a) {
     for (int u = 0; u < U; ++u) {
       const long long j = j0 + u * stride;
       if (j < N) {
-        const double p = __dadd_rn(zj[u], __dmul_rn(beta, pj[u]));
-        pn[j] = p;
+        const double p = __dadd_rn(zp[u].x, __dmul_rn(beta, zp[u].y));
         const double ap = m[u] ? p : s[u];
         a.x[j] = __dadd_rn(xj[u], __dmul_rn(alpha, p));
         const double r = __dsub_rn(rj[u], __dmul_rn(alpha, ap));
         a.r[j] = r;
         const double z = __dmul_rn(dj[u], r);
-        a.z[j] = z;
+        reinterpret_cast<double2*>(pn)[j] = make_double2(z, p);
         rz = fma(r, z, rz);
       }
     }
@@ -1501,6 +1380,19 @@ __global__ void k_dt(DtArgs a) {
   double att = dt;
   for (int i = 0; i < a.retry; ++i) att /= 2.0;
   a.dt[1] = att;
+}
+
+// pack node id | owner << 27 | wall mask(c) << (28 + c) for the CG kernels
+__global__ void k_build_emapf(const int* emap, const uint8_t* own, const uint8_t* mask, int nc, long long n_entries,
+                              int* out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_entries) return;
+  const int node = emap[t];
+  int w = node | (own[t] ? (1 << 27) : 0);
+  if (mask)
+    for (int c = 0; c < nc; ++c)
+      if (mask[(long long)node * nc + c]) w |= 1 << (28 + c);
+  out[t] = w;
 }
 
 __global__ void k_status_reset(StatusDev* st, int n) {
