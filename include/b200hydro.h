@@ -120,6 +120,10 @@ int hx_set_stream(hx_ctx* ctx, void* stream);
 const char* hx_last_error(hx_ctx* ctx);
 /* Number of kernels this context launched so far (evidence counter). */
 int64_t hx_kernel_launches(hx_ctx* ctx);
+/* Restriction layout chosen by hx_create: 1 = structured brick (the dofmap is the
+ * lexicographic numbering of cartesian_mesh, fespace.py:352-385: index-free CG kernels,
+ * element-major E-vectors), 0 = generic CSR transpose map.  Results are identical. */
+int hx_layout(hx_ctx* ctx);
 
 /* ---- restriction (fespace.py:221-234) -------------------------------- */
 

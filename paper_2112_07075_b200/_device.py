@@ -92,6 +92,10 @@ class DeviceContext:
                 raise ValueError(f"{what}: {msg}")
             raise LibError(f"{what} failed (code {rc}): {msg}")
 
+    def layout(self) -> str:
+        """'brick' (structured index-free CG kernels) or 'csr' (generic transpose map)."""
+        return "brick" if self.lib.hx_layout(self.h) == 1 else "csr"
+
     def launches(self) -> int:
         return int(self.lib.hx_kernel_launches(self.h))
 

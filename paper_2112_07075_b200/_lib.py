@@ -65,6 +65,7 @@ _SIGS = {
     "hx_set_stream": (C.c_int, [P, P]),
     "hx_last_error": (C.c_char_p, [P]),
     "hx_kernel_launches": (C.c_int64, [P]),
+    "hx_layout": (C.c_int, [P]),
     "hx_gather": (C.c_int, [P, C.c_int, P, C.c_int, P]),
     "hx_scatter_add": (C.c_int, [P, C.c_int, P, C.c_int, P]),
     "hx_geometry": (C.c_int, [P, P, P, P, P, P, C.POINTER(Inverted)]),

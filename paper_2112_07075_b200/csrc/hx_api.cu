@@ -13,10 +13,12 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/b200hydro.h"
 #include "hx_kernels.cuh"
+#include "hx_brick.cuh"
 
 using namespace hx;
 
@@ -24,6 +26,9 @@ struct hx_ctx {
   int dim, p, Q, D1, DT, nl, nq, nt;
   long long ne, nn;
   int device;
+  bool brick = false;  // dofmap is a lexicographic brick (cartesian_mesh): structured CG path
+  bool elem_major = false;  // brick CG E-vectors element-major (else node-sorted, CSR node pass)
+  Brick bk{};
   cudaStream_t stream = 0;
   std::string err;
   long long launches = 0;
@@ -211,7 +216,7 @@ struct LaunchRates {
       CK(smem_attr(kern, SM::bytes));
       attr = true;
     }
-    RatesArgs a{x, v, e, ctx->qd0, ctx->emap, ctx->slot, ctx->minv, tables(ctx), gamma, q1, q2, ctx->ne, evec, de, st, mode};
+    RatesArgs a{x, v, e, ctx->qd0, ctx->emap, ctx->elem_major ? nullptr : ctx->slot, ctx->minv, tables(ctx), gamma, q1, q2, ctx->ne, evec, de, st, mode};
     prof_begin(ctx, mode == 0 ? K_RATES : K_VALID);
     kern<<<(unsigned)ctx->ne, RATES_NT, SM::bytes, ctx->stream>>>(a);
     prof_end(ctx);
@@ -503,6 +508,40 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
       emap[e * nl + l] = (int)n;
       cnt[n + 1]++;
     }
+  // structured brick? (cartesian_mesh numbering, fespace.py:352-385)
+  if (ctx->dim == 3 && ctx->p >= 2) {
+    const int p = ctx->p;
+    const long long n1 = emap[p], n2 = emap[p * D1], n3 = emap[p * D1 * D1];
+    bool ok = emap[0] == 0 && n1 == p && n2 % p == 0 && n3 % p == 0 && n2 > 0 && n3 > 0;
+    long long Nx = ok ? n2 / p : 0, NxNy = ok ? n3 / p : 0;
+    ok = ok && Nx > 1 && NxNy % Nx == 0 && (Nx - 1) % p == 0;
+    long long Ny = ok ? NxNy / Nx : 0;
+    ok = ok && Ny > 1 && (Ny - 1) % p == 0;
+    const long long bx = ok ? (Nx - 1) / p : 1, by = ok ? (Ny - 1) / p : 1;
+    ok = ok && ne % (bx * by) == 0;
+    const long long bz = ok ? ne / (bx * by) : 1;
+    ok = ok && nn == NxNy * (bz * p + 1);
+    for (long long e = 0; ok && e < ne; ++e) {
+      const long long ez = e / (bx * by), ey = (e / bx) % by, ex = e % bx;
+      for (int l = 0; l < nl; ++l) {
+        const int dx = l % D1, dy = (l / D1) % D1, dz = l / (D1 * D1);
+        const long long want = (ex * p + dx) + Nx * (ey * p + dy) + NxNy * (ez * p + dz);
+        if (emap[e * nl + l] != want) {
+          ok = false;
+          break;
+        }
+      }
+    }
+    const char* env = getenv("HX_BRICK");
+    if (env && env[0] == '0') ok = false;
+    if (ok) {
+      ctx->brick = true;
+      const char* ev = getenv("HX_EVEC");  // HX_EVEC=sorted: node-sorted E with the brick mass kernel
+      ctx->elem_major = !(ev && strcmp(ev, "sorted") == 0);
+      ctx->bk = Brick{(int)bx, (int)by, (int)bz, (int)Nx, (int)Ny, NxNy, make_fastdiv((unsigned)bx),
+                      make_fastdiv((unsigned)(bx * by)), make_fastdiv((unsigned)Nx), make_fastdiv((unsigned)NxNy)};
+    }
+  }
   std::vector<int> off(nn + 1, 0);
   for (long long n = 0; n < nn; ++n) off[n + 1] = off[n] + cnt[n + 1];
   std::vector<int> fill(off.begin(), off.end() - 1);
@@ -669,6 +708,7 @@ extern "C" int hx_set_stream(hx_ctx* ctx, void* stream) {
 
 extern "C" const char* hx_last_error(hx_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 extern "C" int64_t hx_kernel_launches(hx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+extern "C" int hx_layout(hx_ctx* ctx) { return ctx && ctx->brick ? 1 : 0; }
 
 // ---------------------------------------------------------------------------
 // restriction
@@ -806,9 +846,86 @@ extern "C" int hx_mass_diagonal(hx_mass* m, double* diag) {
 struct CGLaunch {
   NodeArgs na;
   MassArgs ma;
-  unsigned gn, gnc;
+  MassBrickArgs mb;  // structured-brick mass (ctx->brick)
   int nc;
 };
+
+// node-sum functor for the context's E-vector layout: element-major brick sums or
+// the node-sorted CSR sums; f(sum, integral_constant<NC>)
+template <int N>
+using IC = std::integral_constant<int, N>;
+
+template <class F>
+static int with_node_sum(hx_ctx* ctx, int nc, const double* evec, F&& f) {
+  if (ctx->elem_major) {
+    switch (ctx->p * 10 + nc) {
+      case 21: return f(BrickSum<2, 1>{evec, ctx->bk}, IC<1>());
+      case 22: return f(BrickSum<2, 2>{evec, ctx->bk}, IC<2>());
+      case 23: return f(BrickSum<2, 3>{evec, ctx->bk}, IC<3>());
+      case 31: return f(BrickSum<3, 1>{evec, ctx->bk}, IC<1>());
+      case 32: return f(BrickSum<3, 2>{evec, ctx->bk}, IC<2>());
+      case 33: return f(BrickSum<3, 3>{evec, ctx->bk}, IC<3>());
+      case 41: return f(BrickSum<4, 1>{evec, ctx->bk}, IC<1>());
+      case 42: return f(BrickSum<4, 2>{evec, ctx->bk}, IC<2>());
+      case 43: return f(BrickSum<4, 3>{evec, ctx->bk}, IC<3>());
+    }
+    return fail(ctx, HX_EINVAL, "brick node sum: unsupported p=%d nc=%d", ctx->p, nc);
+  }
+  if (nc == 1) return f(CsrSum<1>{ctx->off, evec}, IC<1>());
+  if (nc == 2) return f(CsrSum<2>{ctx->off, evec}, IC<2>());
+  return f(CsrSum<3>{ctx->off, evec}, IC<3>());
+}
+
+template <int NC, class SUM>
+static int launch_cg_nodes(hx_ctx* ctx, const NodeArgs& na, SUM sum, bool init) {
+  auto kn = k_cg_node<NC, SUM>;
+  auto ki = k_cg_init<NC, SUM>;
+  static unsigned cap_n = 0, cap_i = 0;
+  if (!cap_n) {
+    cap_n = persistent_grid(kn, 256, 0, 1ll << 40);
+    cap_i = persistent_grid(ki, 256, 0, 1ll << 40);
+  }
+  const unsigned need = gblocks(ctx->nn * NC, 256);
+  if (init) {
+    prof_begin(ctx, K_CGINIT);
+    ki<<<std::min(need, cap_i), 256, 0, ctx->stream>>>(na, sum);
+  } else {
+    prof_begin(ctx, K_CGNODE);
+    kn<<<std::min(need, cap_n), 256, 0, ctx->stream>>>(na, sum);
+  }
+  prof_end(ctx);
+  CKL();
+  return HX_OK;
+}
+
+template <int P, int NC>
+static int launch_mass_brick(hx_ctx* ctx, const MassBrickArgs& a) {
+  using M = MassBrickCfg<P, NC>;
+  auto k = k_mass_brick<P, NC>;
+  CK(smem_attr(k, M::bytes));
+  static unsigned grid = 0;
+  if (!grid) grid = persistent_grid(k, 128, M::bytes, 1ll << 40);
+  prof_begin(ctx, K_MASS);
+  k<<<std::min(grid, gblocks(ctx->ne, M::EPC)), 128, M::bytes, ctx->stream>>>(a);
+  prof_end(ctx);
+  CKL();
+  return HX_OK;
+}
+
+static int mass_brick(hx_ctx* ctx, int nc, const MassBrickArgs& a) {
+  switch (ctx->p * 10 + nc) {
+    case 21: return launch_mass_brick<2, 1>(ctx, a);
+    case 22: return launch_mass_brick<2, 2>(ctx, a);
+    case 23: return launch_mass_brick<2, 3>(ctx, a);
+    case 31: return launch_mass_brick<3, 1>(ctx, a);
+    case 32: return launch_mass_brick<3, 2>(ctx, a);
+    case 33: return launch_mass_brick<3, 3>(ctx, a);
+    case 41: return launch_mass_brick<4, 1>(ctx, a);
+    case 42: return launch_mass_brick<4, 2>(ctx, a);
+    case 43: return launch_mass_brick<4, 3>(ctx, a);
+  }
+  return fail(ctx, HX_EINVAL, "brick mass: unsupported p=%d nc=%d", ctx->p, nc);
+}
 
 static int build_emapf(hx_ctx* ctx, const uint8_t* mask, int nc, int* out) {
   const long long n = ctx->ne * ctx->nl;
@@ -866,46 +983,61 @@ static int cg_prepare(hx_ctx* ctx, CGDev* cg, const double* D, const double* rhs
   ma.cg = cg;
   ma.partials = ctx->partials;
   L.nc = nc;
-  static unsigned cap_node[4] = {0, 0, 0, 0}, cap_init[4] = {0, 0, 0, 0};
-  if (!cap_node[nc]) {
-    if (nc == 1) {
-      cap_node[nc] = persistent_grid(k_cg_node<1>, 256, 0, 1ll << 40);
-      cap_init[nc] = persistent_grid(k_cg_init<1>, 256, 0, 1ll << 40);
-    } else if (nc == 2) {
-      cap_node[nc] = persistent_grid(k_cg_node<2>, 256, 0, 1ll << 40);
-      cap_init[nc] = persistent_grid(k_cg_init<2>, 256, 0, 1ll << 40);
-    } else {
-      cap_node[nc] = persistent_grid(k_cg_node<3>, 256, 0, 1ll << 40);
-      cap_init[nc] = persistent_grid(k_cg_init<3>, 256, 0, 1ll << 40);
-    }
-  }
-  L.gnc = std::min(gblocks(ctx->nn * nc, 256), cap_node[nc]);
-  L.gn = std::min(gblocks(ctx->nn * nc, 256), cap_init[nc]);
+  L.mb = MassBrickArgs{ctx->p0, ctx->p1, D, ctx->ne, ctx->evec, ctx->elem_major ? nullptr : ctx->slot, cg,
+                       ctx->partials, ctx->bk};
   return HX_OK;
 }
 
 static int cg_launch_init(hx_ctx* ctx, CGLaunch& L) {
-  prof_begin(ctx, K_CGINIT);
-  if (L.nc == 1) k_cg_init<1><<<L.gn, 256, 0, ctx->stream>>>(L.na);
-  else if (L.nc == 2) k_cg_init<2><<<L.gn, 256, 0, ctx->stream>>>(L.na);
-  else k_cg_init<3><<<L.gn, 256, 0, ctx->stream>>>(L.na);
-  prof_end(ctx);
-  CKL();
+  int rc = with_node_sum(ctx, L.nc, L.na.evec, [&](auto sum, auto ncc) {
+    return launch_cg_nodes<decltype(ncc)::value>(ctx, L.na, sum, true);
+  });
+  if (rc) return rc;
   L.na.evec = ctx->evec;
   L.na.rhs = nullptr;
   return HX_OK;
 }
 
-static int cg_launch_iter(hx_ctx* ctx, CGLaunch& L) {
-  int rc = dispatch<LaunchMass>(ctx, L.nc, true, L.ma);
-  if (rc) return rc;
+template <int P, int NC>
+static int launch_cg_node_brick(hx_ctx* ctx, const NodeArgs& na) {
+  auto k = k_cg_node_brick<P, NC>;
+  static unsigned cap = 0;
+  if (!cap) cap = persistent_grid(k, 256, 0, 1ll << 40);
   prof_begin(ctx, K_CGNODE);
-  if (L.nc == 1) k_cg_node<1><<<L.gnc, 256, 0, ctx->stream>>>(L.na);
-  else if (L.nc == 2) k_cg_node<2><<<L.gnc, 256, 0, ctx->stream>>>(L.na);
-  else k_cg_node<3><<<L.gnc, 256, 0, ctx->stream>>>(L.na);
+  k<<<std::min(gblocks(ctx->nn, 256), cap), 256, 0, ctx->stream>>>(na, ctx->bk);
   prof_end(ctx);
   CKL();
   return HX_OK;
+}
+
+static int g_node_kernel = -1;  // HX_NODE_KERNEL=node: thread-per-node brick node pass (element-major E)
+
+static int cg_node_brick(hx_ctx* ctx, int nc, const NodeArgs& na) {
+  switch (ctx->p * 10 + nc) {
+    case 21: return launch_cg_node_brick<2, 1>(ctx, na);
+    case 22: return launch_cg_node_brick<2, 2>(ctx, na);
+    case 23: return launch_cg_node_brick<2, 3>(ctx, na);
+    case 31: return launch_cg_node_brick<3, 1>(ctx, na);
+    case 32: return launch_cg_node_brick<3, 2>(ctx, na);
+    case 33: return launch_cg_node_brick<3, 3>(ctx, na);
+    case 41: return launch_cg_node_brick<4, 1>(ctx, na);
+    case 42: return launch_cg_node_brick<4, 2>(ctx, na);
+    case 43: return launch_cg_node_brick<4, 3>(ctx, na);
+  }
+  return fail(ctx, HX_EINVAL, "brick node pass: unsupported p=%d nc=%d", ctx->p, nc);
+}
+
+static int cg_launch_iter(hx_ctx* ctx, CGLaunch& L) {
+  int rc = ctx->brick ? mass_brick(ctx, L.nc, L.mb) : dispatch<LaunchMass>(ctx, L.nc, true, L.ma);
+  if (rc) return rc;
+  if (g_node_kernel < 0) {
+    const char* v = getenv("HX_NODE_KERNEL");
+    g_node_kernel = (v && strcmp(v, "node") == 0) ? 1 : 0;
+  }
+  if (ctx->elem_major && g_node_kernel == 1) return cg_node_brick(ctx, L.nc, L.na);
+  return with_node_sum(ctx, L.nc, ctx->evec, [&](auto sum, auto ncc) {
+    return launch_cg_nodes<decltype(ncc)::value>(ctx, L.na, sum, false);
+  });
 }
 
 static void cg_info_from(const CGDev& g, hx_cg_info* info) {

@@ -297,7 +297,9 @@ __global__ void __launch_bounds__(NT) k_rates(RatesArgs a) {
   __syncthreads();
   for (int i = tid; i < NL * DIM; i += NT) {
     const int l = i / DIM, c = i - l * DIM;
-    a.evec[(long long)a.slot[e * NL + l] * DIM + c] = fout[c * NL + l];
+    // node-sorted position (generic CSR path) or element-major (structured brick, coalesced)
+    const long long pos = a.slot ? (long long)a.slot[e * NL + l] * DIM + c : e * (NL * DIM) + i;
+    a.evec[pos] = fout[c * NL + l];
   }
   // de = M_e^{-1} (F^T v)_e   (einsum "eij,ej->ei", hydro.py:343)
   const double* mi = a.minv + e * NTH * NTH;
@@ -1186,8 +1188,8 @@ __global__ void __launch_bounds__(256) k_scatter(NodeArgs a) {
 // rz = r.z, norm0 = sqrt(rz); b == 0 everywhere -> 0 iterations.
 // b is rhs, or -(G^T evec) masked (rhs_v = -F.1, hydro.py:351, 320).  Persistent
 // grid-stride over (node, component).
-template <int NC>
-__global__ void __launch_bounds__(256) k_cg_init(NodeArgs a) {
+template <int NC, class SUM>
+__global__ void __launch_bounds__(256) k_cg_init(NodeArgs a, SUM sum) {
   __shared__ double red[32];
   __shared__ int sflag;
   double rz = 0.0, nz = 0.0;
@@ -1195,7 +1197,7 @@ __global__ void __launch_bounds__(256) k_cg_init(NodeArgs a) {
   for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += (long long)gridDim.x * blockDim.x) {
     const long long n = j / NC;
     const int c = (int)(j - n * NC);
-    const double s = a.rhs ? a.rhs[j] : node_sum1<NC>(a.off, a.evec, n, c);
+    const double s = a.rhs ? a.rhs[j] : sum(n, c);
     double b = a.negate ? -s : s;
     if (a.mask && a.mask[j]) b = 0.0;
     const double z = a.invd[j] * b;
@@ -1253,8 +1255,8 @@ __global__ void __launch_bounds__(256) k_cg_init(NodeArgs a) {
 // CG iteration tail (operators.py:352-365): p_k = z + beta p_{k-1} (written),
 // Ap = G^T evec (identity on masked rows), x += alpha p, r -= alpha Ap, z = D^{-1} r,
 // rz_new = r.z; stop test sqrt(max(rz_new,0)) <= tol*norm0; beta = rz_new/rz.
-template <int NC>
-__global__ void __launch_bounds__(256, 4) k_cg_node(NodeArgs a) {
+template <int NC, class SUM>
+__global__ void __launch_bounds__(256, 4) k_cg_node(NodeArgs a, SUM sum) {
   __shared__ double red[32];
   __shared__ int sflag;
   CGDev* g = a.cg;
@@ -1284,7 +1286,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_node(NodeArgs a) {
         rj[u] = __ldcg(a.r + j);
         dj[u] = __ldg(a.invd + j);
         m[u] = a.mask && a.mask[j];
-        s[u] = node_sum1<NC>(a.off, a.evec, n, c);
+        s[u] = sum(n, c);
       }
     }
 #pragma unroll

@@ -53,8 +53,13 @@ def test_geometry(d, p):
     assert rel(geom.wdetj, g["wdetj"]) < 1e-14
 
 
+@pytest.mark.parametrize("brick", [True, False], ids=["brick", "csr"])
 @pytest.mark.parametrize("d,p", CASES)
-def test_mass_pa(d, p):
+def test_mass_pa(d, p, brick, monkeypatch):
+    """PA mass apply / diagonal / device CG; `csr` forces the generic (index-array) CG
+    path on structured meshes, `brick` lets 3D p>=2 take the structured-brick kernels."""
+    if not brick:
+        monkeypatch.setenv("HX_BRICK", "0")
     from paper_2112_07075_b200.fespace import FiniteElementSpace, compute_geometric_factors
     from paper_2112_07075_b200.operators import MassPA, cg_solve
     from paper_2112_07075_b200.tensor_basis import gauss_legendre
@@ -150,10 +155,13 @@ def _problem(z):
     return problems.triple_point(d, float(z["gamma"]))
 
 
+@pytest.mark.parametrize("brick", [True, False], ids=["brick", "csr"])
 @pytest.mark.parametrize("name", RUNS)
 @pytest.mark.parametrize("fused", [False, True])
-def test_nstep_run_matches_reference(name, fused):
+def test_nstep_run_matches_reference(name, fused, brick, monkeypatch):
     """N Lagrange steps (timestep_estimate + rk2_step) vs the reference's final state."""
+    if not brick:
+        monkeypatch.setenv("HX_BRICK", "0")
     from paper_2112_07075_b200.fespace import cartesian_mesh
     from paper_2112_07075_b200.hydro import (LagrangeHydro, MaterialModel, StepControls, ViscosityModel,
                                              box_velocity_bc)
@@ -165,6 +173,7 @@ def test_nstep_run_matches_reference(name, fused):
     mesh = cartesian_mesh(d, tuple(z["extents"]), tuple(int(c) for c in z["counts"]), p)
     hy = LagrangeHydro(mesh, gauss_legendre(p + 2), MaterialModel(float(z["gamma"])),
                        ViscosityModel(float(z["q1"]), float(z["q2"])), bc_mask=box_velocity_bc(mesh))
+    assert hy._ctx.layout() == ("brick" if (brick and d == 3 and p >= 2) else "csr")
     rho0, v0, e0 = _problem(z)
     st = hy.initial_state(rho0, v0, e0)
     ctl = StepControls(cfl=float(z["cfl"]), dt_max=1.0, t_final=10.0)
