@@ -19,6 +19,7 @@
 #include "../../include/b200hydro.h"
 #include "hx_kernels.cuh"
 #include "hx_brick.cuh"
+#include "hx_rates.cuh"
 
 using namespace hx;
 
@@ -205,10 +206,41 @@ static constexpr int RATES_NT = 128;
 // ---------------------------------------------------------------------------
 // launchers
 
+static int g_rates_kernel = -1;  // HX_RATES=cta: the CTA-per-element rates kernel for 3D
+
+template <int P, int MODE>
+static int launch_rates_pc(hx_ctx* ctx, const RatesPCArgs& a) {
+  using R = RatesPC<P>;
+  auto k = k_rates_pc<P, MODE>;
+  static bool attr = false;
+  if (!attr) {
+    CK(smem_attr(k, R::bytes));
+    attr = true;
+  }
+  static unsigned grid = 0;
+  if (!grid) grid = persistent_grid(k, R::THREADS, R::bytes, 1ll << 40);
+  prof_begin(ctx, MODE == 0 ? K_RATES : K_VALID);
+  k<<<std::min(grid, gblocks(ctx->ne, R::EPC)), R::THREADS, R::bytes, ctx->stream>>>(a);
+  prof_end(ctx);
+  CKL();
+  return HX_OK;
+}
+
 template <int DIM, int P>
 struct LaunchRates {
   static int run(hx_ctx* ctx, const double* x, const double* v, const double* e, double* evec, double* de,
                  StatusDev* st, int mode, double gamma, double q1, double q2) {
+    if (g_rates_kernel < 0) {
+      const char* s = getenv("HX_RATES");
+      g_rates_kernel = (s && strcmp(s, "cta") == 0) ? 0 : 1;
+    }
+    if constexpr (DIM == 3 && P >= 2) {
+      if (g_rates_kernel == 1) {
+        RatesPCArgs a{x, v, e, ctx->qd0, ctx->emap, ctx->elem_major ? nullptr : ctx->slot, ctx->minv, ctx->wnd,
+                      ctx->psi1, gamma, q1, q2, ctx->ne, evec, de, st, ctx->bk, ctx->brick ? 1 : 0};
+        return mode == 0 ? launch_rates_pc<P, 0>(ctx, a) : launch_rates_pc<P, 1>(ctx, a);
+      }
+    }
     using SM = RatesSmem<DIM, P>;
     auto kern = k_rates<DIM, P, RATES_NT>;
     static bool attr = false;
@@ -663,6 +695,8 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
     }
     seen[ctx->p - 1] = tb;
     ok &= cudaMemcpyToSymbol(c_B, tb.data(), sizeof(double) * tb.size(), sizeof(double) * 30 * (ctx->p - 1)) ==
+          cudaSuccess;
+    ok &= cudaMemcpyToSymbol(c_Bt, d->Bt_host, sizeof(double) * Q * DT, sizeof(double) * 30 * (ctx->p - 1)) ==
           cudaSuccess;
     ok &= cudaMemcpyToSymbol(c_G, d->G_host, sizeof(double) * Q * D1, sizeof(double) * 30 * (ctx->p - 1)) ==
           cudaSuccess;

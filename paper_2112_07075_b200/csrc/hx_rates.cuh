@@ -1,0 +1,577 @@
+// hx_rates.cuh -- fused rates kernel (3D), the B200 mapping of LagrangeHydro.rates
+// minus the momentum solve (hydro.py:346-360): geometry (fespace.py:305-346),
+// stress_qdata (hydro.py:254-315), ForcePA F.1 and F^T v (operators.py:247-300) and
+// M_e^{-1} (hydro.py:339-344).  D_F never leaves shared memory.
+//
+// A CTA of 256 threads runs EPC elements per pass.  Every sum-factorisation stage is
+// its own phase with one thread per 1D line, so no thread carries more than one
+// line of one stage (short dependency chains, modest registers, all lanes busy):
+//   A   gather x, v node rows (6 fields) and e -> G image
+//   B1  x stage, thread per (field, z, y) row: B_x u, G_x u          -> X image
+//   B2  y stage, thread per (field, z, qx) line: B_y B_x, G_y B_x, B_y G_x -> T image
+//   C1  z stage + point physics, thread per quadrature point: J, grad v, v, e at q,
+//       EOS, tensor viscosity, CFL ratio, D_F; F.1 and F^T v integrands -> W image
+//   C2  transposed z stage, thread per (comp, qx, qy) column           -> Z image
+//   D1  transposed y stage, thread per (comp, z, qx) line              -> Y image
+//   D2  transposed x stage, thread per (comp, z, y) row                -> staging
+//   E   F.1 E-vector out (element-major or node-sorted) and de = M_e^{-1} F^T v
+// MODE 1 (validity of the new geometry, hydro.py:400-401) runs A-C1 on x only.
+// Shared images alias once dead: W over G+X, Z over T, Y over X, staging over G.
+#pragma once
+
+#include "hx_brick.cuh"
+
+namespace hx {
+
+__constant__ double c_Bt[4][30];  // thermodynamic basis (Q x DT) per order, like c_B
+
+template <int P>
+struct RatesPC {
+  static constexpr int D1 = P + 1, Q = P + 2, DT = P, DD = D1 * D1, QQ = Q * Q, NL = D1 * DD, NQ = Q * QQ;
+  static constexpr int NT = DT * DT * DT, DTT = DT * DT;
+  static constexpr int THREADS = 256;
+  static constexpr int EPC = THREADS / NQ > 0 ? THREADS / NQ : 1;
+  static constexpr int XPL = 6 * D1;                   // field planes
+  static constexpr int GP = DD + 1, EP = DTT + 1;      // gather pitches (field / thermo plane)
+  static constexpr int GS = XPL * GP + DT * EP;        // G image
+  static constexpr int XP = 2 * Q + 1;                 // row pitch of the x / y-transposed images
+  static constexpr int XFS = XPL * D1 * XP;            // X image, field rows
+  static constexpr int XS = XFS + DTT * Q;             // + thermo rows
+  static constexpr int TFS = XPL * 3 * QQ;             // T image, field planes
+  static constexpr int TS = TFS + DT * QQ;             // + thermo planes
+  static constexpr int WS = 10 * NQ;                   // W image (aliases G+X)
+  static constexpr int ZS = 9 * D1 * QQ + DT * QQ;     // Z image (aliases T)
+  static constexpr int YFS = 3 * D1 * D1 * XP;         // Y image (aliases X)
+  static constexpr int YS = YFS + DTT * Q;
+  static constexpr int OS = 3 * NL + NT;               // staging (aliases T)
+  // prefetch buffer (double-buffered, filled by cp.async one pass ahead):
+  // [G images EPC x GS | qd0 EPC x NQ | M_e^{-1} EPC x NT^2], regions 16-byte aligned
+  static constexpr int ev(int n) { return (n + 1) & ~1; }
+  static constexpr int FQ = ev(EPC * GS), FM = FQ + ev(EPC * NQ), FS = FM + ev(EPC * NT * NT);
+  static constexpr int XR = (XS > WS ? (XS > YS ? XS : YS) : (WS > YS ? WS : YS));  // X / W / Y region
+  static_assert(ZS <= TS && OS <= TS, "image aliasing");
+  static constexpr int PER = XR + TS;                  // working images per element
+  static constexpr size_t bytes = sizeof(double) * (2 * (size_t)FS + (size_t)EPC * PER + 2 * NQ);
+};
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16d(double* dst, const double* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+// contiguous span of n doubles (dst 16-byte aligned): 16-byte copies when src allows
+template <int NT>
+__device__ __forceinline__ void cp_span(double* dst, const double* src, int n, int t) {
+  if ((reinterpret_cast<unsigned long long>(src) & 15ull) == 0) {
+    for (int i = t; i < n / 2; i += NT) cp_async16d(dst + 2 * i, src + 2 * i);
+    if ((n & 1) && t == 0) cp_async8(dst + n - 1, src + n - 1);
+  } else {
+    for (int i = t; i < n; i += NT) cp_async8(dst + i, src + i);
+  }
+}
+
+struct RatesPCArgs {
+  const double* x;     // (NN, 3)
+  const double* v;     // (NN, 3)
+  const double* e;     // (NE*nt)
+  const double* qd0;   // (NE, nq)
+  const int* emap;     // (NE, nl) (generic meshes)
+  const int* slot;     // null: element-major E out; else node-sorted position
+  const double* minv;  // (NE, nt, nt)
+  const double* wnd;   // (nq)
+  const double* psi1;  // (nq)
+  double gamma, q1, q2;
+  long long ne;
+  double* evec;        // (NE, nl, 3) F.1 element vectors
+  double* de;          // (NE*nt)
+  StatusDev* st;
+  Brick b;
+  int brick;
+};
+
+// reference "inverse" (cof/det = J^{-T} in 3D, fespace.py:280-302,338) with one reciprocal
+__device__ __forceinline__ double det_inv_fast(const double (&J)[3][3], double (&inv)[3][3]) {
+  const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                     J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                     J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+  const double rd = 1.0 / det;
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int r0 = r == 0 ? 1 : 0, r1 = r == 2 ? 1 : 2;
+      const int c0 = c == 0 ? 1 : 0, c1 = c == 2 ? 1 : 2;
+      const double m = J[r0][c0] * J[r1][c1] - J[r0][c1] * J[r1][c0];
+      inv[r][c] = (((r + c) & 1) ? -m : m) * rd;
+    }
+  return det;
+}
+
+// stress_qdata at one point (hydro.py:271-315) + D_F (operators.py:258): the
+// arithmetic of point_physics with one reciprocal of det J and h = cbrt(det J)
+// (the reference's detj ** (1/3) to within an ulp).
+__device__ __forceinline__ void point_physics_fast(const double (&J)[3][3], const double (&dv)[3][3],
+                                                   const double (&vq)[3], double eq, double qd0, double gamma,
+                                                   double q1, double q2, PointOut<3>& o) {
+  o.det = det_inv_fast(J, o.jinv);
+  const double det = o.det;
+  const double rho = qd0 / det;
+  o.clamped = 0;
+  if (eq < 0.0) {
+    o.clamped = 1;
+    eq = 0.0;
+  }
+  const double p = (gamma - 1.0) * rho * eq;
+  const double cs = sqrt(gamma * (gamma - 1.0) * eq);
+  double gv[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      double s = 0.0;
+#pragma unroll
+      for (int l = 0; l < 3; ++l) s = fma(dv[a][l], o.jinv[l][b], s);
+      gv[a][b] = s;
+    }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) o.sigma[a][b] = (a == b) ? -p : 0.0;
+  const double div = gv[0][0] + gv[1][1] + gv[2][2];
+  const double h = cbrt(det);
+  if (q1 > 0.0 || q2 > 0.0) {
+    double mu = rho * h * (q1 * cs + q2 * h * fabs(div));
+    mu = div < 0.0 ? mu : 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) o.sigma[a][b] += mu * (0.5 * (gv[a][b] + gv[b][a]));
+  }
+  const double v2 = vq[0] * vq[0] + vq[1] * vq[1] + vq[2] * vq[2];
+  const double speed = cs + sqrt(v2);
+  o.ratio = speed > 0.0 ? h / fmax(speed, 1e-300) : __longlong_as_double(0x7ff0000000000000ll);
+}
+
+template <int P, int MODE>
+__global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
+  using R = RatesPC<P>;
+  constexpr int D1 = R::D1, Q = R::Q, DT = R::DT, DD = R::DD, QQ = R::QQ, NL = R::NL, NQ = R::NQ;
+  constexpr int NTH = R::NT, DTT = R::DTT, EPC = R::EPC, GP = R::GP, EP = R::EP;
+  constexpr int XPL = R::XPL, PER = R::PER, XP = R::XP, XFS = R::XFS, TFS = R::TFS, YFS = R::YFS;
+  constexpr int FS = R::FS, XR = R::XR;
+  constexpr int NT = R::THREADS;
+  constexpr int NF = MODE == 0 ? 6 : 3;  // fields gathered / contracted
+  const double* cB = c_B[P - 1];
+  const double* cG = c_G[P - 1];
+  const double* cBt = c_Bt[P - 1];
+  extern __shared__ __align__(16) double smem[];
+  double* work = smem + 2 * FS;  // per element: X/W/Y region, T/Z/O region
+  double* sw = work + EPC * PER;       // tensor weights
+  double* sp = sw + NQ;                // psi1
+  const int t = threadIdx.x;
+  for (int i = t; i < NQ; i += NT) {
+    sw[i] = a.wnd[i];
+    sp[i] = a.psi1[i];
+  }
+  double rmin = __longlong_as_double(0x7ff0000000000000ll);
+  long long clamps = 0;
+  unsigned long long key = ~0ull;
+  // A (prefetch): cp.async x, v node values, e, qd0 and M_e^{-1} of the pass at f0
+  // into prefetch buffer b (G image layout: field planes, padded)
+  auto prefetch = [&](int b, long long f0) {
+    if (f0 < a.ne) {
+      const int fel = (int)((a.ne - f0) < EPC ? (a.ne - f0) : EPC);
+      double* fb = smem + b * FS;
+      constexpr int ROW = 3 * D1;  // doubles per node row (D1 nodes x 3 comps, contiguous)
+      for (int it = t; it < fel * DD * ROW; it += NT) {
+        const int el = it / (DD * ROW), rem = it - el * (DD * ROW);
+        const int row = rem / ROW, sidx = rem - row * ROW;  // row = dz*D1 + dy
+        const int dz = row / D1, dy = row - dz * D1, dx = sidx / 3, c = sidx - dx * 3;
+        const long long e = f0 + el;
+        long long n;
+        if (a.brick) {
+          const unsigned ue = (unsigned)e;
+          const unsigned ez = a.b.fnxy.div(ue);
+          const unsigned r2 = ue - ez * (unsigned)(a.b.nx * a.b.ny);
+          const unsigned ey = a.b.fnx.div(r2), ex = r2 - ey * (unsigned)a.b.nx;
+          n = (long long)(ex * P + dx) + (long long)(ey * P + dy) * a.b.Nx + (long long)(ez * P + dz) * a.b.NxNy;
+        } else {
+          n = __ldg(a.emap + e * NL + row * D1 + dx);
+        }
+        double* g = fb + el * R::GS;
+        cp_async8(g + (c * D1 + dz) * GP + dy * D1 + dx, a.x + n * 3 + c);
+        if constexpr (MODE == 0) cp_async8(g + ((3 + c) * D1 + dz) * GP + dy * D1 + dx, a.v + n * 3 + c);
+      }
+      if constexpr (MODE == 0) {
+        for (int it = t; it < fel * NTH; it += NT) {
+          const int el = it / NTH, i = it - el * NTH;
+          const int dz = i / DTT, k = i - dz * DTT;
+          cp_async8(fb + el * R::GS + XPL * GP + dz * EP + k, a.e + (f0 + el) * NTH + i);
+        }
+        cp_span<NT>(fb + R::FQ, a.qd0 + f0 * NQ, fel * NQ, t);
+        cp_span<NT>(fb + R::FM, a.minv + f0 * (NTH * NTH), fel * NTH * NTH, t);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const long long stride = (long long)gridDim.x * EPC;
+  prefetch(0, (long long)blockIdx.x * EPC);
+  int buf = 0;
+
+  for (long long e0 = (long long)blockIdx.x * EPC; e0 < a.ne; e0 += stride, buf ^= 1) {
+    const int nel = (int)((a.ne - e0) < EPC ? (a.ne - e0) : EPC);
+    const double* gcur = smem + buf * FS;
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // this pass's prefetch landed; previous pass done with every image
+    prefetch(buf ^ 1, e0 + stride);  // overlaps this pass's compute
+    // ---- B1: x stage, thread per row
+    {
+      constexpr int FR = NF * D1 * D1;                 // field rows
+      constexpr int TASKS = FR + (MODE == 0 ? DTT : 0);
+#pragma unroll
+      for (int rep = 0; rep < (EPC * TASKS + NT - 1) / NT; ++rep) {
+        const int it = t + rep * NT;
+        if (it >= nel * TASKS) break;
+        const int el = it / TASKS, k = it - el * TASKS;
+        const double* g = gcur + el * R::GS;
+        double* X = work + el * PER;
+        if (k < FR) {
+          const int pl = k / D1, dy = k - pl * D1;  // pl = f*D1 + dz
+          double u[D1];
+#pragma unroll
+          for (int dx = 0; dx < D1; ++dx) u[dx] = g[pl * GP + dy * D1 + dx];
+          double* o = X + k * XP;
+#pragma unroll
+          for (int qx = 0; qx < Q; ++qx) {
+            double sb = 0.0, sg = 0.0;
+#pragma unroll
+            for (int dx = 0; dx < D1; ++dx) {
+              sb = fma(cB[qx * D1 + dx], u[dx], sb);
+              sg = fma(cG[qx * D1 + dx], u[dx], sg);
+            }
+            o[qx] = sb;
+            o[Q + qx] = sg;
+          }
+        } else {
+          const int r = k - FR;  // dz_t * DT + dy_t
+          double u[DT];
+#pragma unroll
+          for (int dx = 0; dx < DT; ++dx) u[dx] = g[XPL * GP + (r / DT) * EP + (r % DT) * DT + dx];
+#pragma unroll
+          for (int qx = 0; qx < Q; ++qx) {
+            double s = 0.0;
+#pragma unroll
+            for (int dx = 0; dx < DT; ++dx) s = fma(cBt[qx * DT + dx], u[dx], s);
+            X[XFS + r * Q + qx] = s;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- B2: y stage, thread per (plane, qx) line
+    {
+      constexpr int FL = NF * D1 * Q;
+      constexpr int TASKS = FL + (MODE == 0 ? DT * Q : 0);
+#pragma unroll
+      for (int rep = 0; rep < (EPC * TASKS + NT - 1) / NT; ++rep) {
+        const int it = t + rep * NT;
+        if (it >= nel * TASKS) break;
+        const int el = it / TASKS, k = it - el * TASKS;
+        const double* X = work + el * PER;
+        double* T = work + el * PER + XR;
+        if (k < FL) {
+          const int pl = k / Q, qx = k - pl * Q;
+          double vb[D1], vg[D1];
+#pragma unroll
+          for (int dy = 0; dy < D1; ++dy) {
+            vb[dy] = X[(pl * D1 + dy) * XP + qx];
+            vg[dy] = X[(pl * D1 + dy) * XP + Q + qx];
+          }
+          double* o = T + pl * 3 * QQ + qx;
+#pragma unroll
+          for (int qy = 0; qy < Q; ++qy) {
+            double bb = 0.0, gb = 0.0, bg = 0.0;
+#pragma unroll
+            for (int dy = 0; dy < D1; ++dy) {
+              bb = fma(cB[qy * D1 + dy], vb[dy], bb);
+              gb = fma(cG[qy * D1 + dy], vb[dy], gb);
+              bg = fma(cB[qy * D1 + dy], vg[dy], bg);
+            }
+            o[qy * Q] = bb;
+            o[QQ + qy * Q] = gb;
+            o[2 * QQ + qy * Q] = bg;
+          }
+        } else {
+          const int r = k - FL, dz = r / Q, qx = r - dz * Q;
+          double vb[DT];
+#pragma unroll
+          for (int dy = 0; dy < DT; ++dy) vb[dy] = X[XFS + (dz * DT + dy) * Q + qx];
+#pragma unroll
+          for (int qy = 0; qy < Q; ++qy) {
+            double s = 0.0;
+#pragma unroll
+            for (int dy = 0; dy < DT; ++dy) s = fma(cBt[qy * DT + dy], vb[dy], s);
+            T[TFS + dz * QQ + qy * Q + qx] = s;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- C1: z stage + point physics, thread per point
+#pragma unroll
+    for (int rep = 0; rep < (EPC * NQ + NT - 1) / NT; ++rep) {
+      const int it = t + rep * NT;
+      if (it >= nel * NQ) break;
+      // lanes run qz fastest: the Q points of a column share their T reads (broadcast)
+      const int el = it / NQ, kq = it - el * NQ;
+      const int col = kq / Q, qz = kq - col * Q;
+      const int q = qz * QQ + col;
+      const long long e = e0 + el;
+      const double* T = work + el * PER + XR;
+      double bz[D1], gz[D1];
+#pragma unroll
+      for (int dz = 0; dz < D1; ++dz) {
+        bz[dz] = cB[qz * D1 + dz];
+        gz[dz] = cG[qz * D1 + dz];
+      }
+      double J[3][3], dv[3][3], vq[3];
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0, iv = 0.0;
+#pragma unroll
+        for (int dz = 0; dz < D1; ++dz) {
+          const double* tt = T + (f * D1 + dz) * 3 * QQ + col;
+          const double bb = tt[0], gb = tt[QQ], bg = tt[2 * QQ];
+          d0 = fma(bz[dz], bg, d0);  // d/dxi_x: B_z B_y G_x
+          d1 = fma(bz[dz], gb, d1);  // d/dxi_y: B_z G_y B_x
+          d2 = fma(gz[dz], bb, d2);  // d/dxi_z: G_z B_y B_x
+          if (f >= 3) iv = fma(bz[dz], bb, iv);
+        }
+        if (f < 3) {
+          J[f][0] = d0;
+          J[f][1] = d1;
+          J[f][2] = d2;
+        } else {
+          dv[f - 3][0] = d0;
+          dv[f - 3][1] = d1;
+          dv[f - 3][2] = d2;
+          vq[f - 3] = iv;
+        }
+      }
+      if constexpr (MODE == 1) {
+        double inv[3][3];
+        const double det = det_inv_fast(J, inv);
+        if (det <= 0.0) {
+          const unsigned long long kk = (unsigned long long)q * a.ne + e;
+          key = kk < key ? kk : key;
+        }
+      } else {
+        double eq = 0.0;
+#pragma unroll
+        for (int dz = 0; dz < DT; ++dz) eq = fma(cBt[qz * DT + dz], T[TFS + dz * QQ + col], eq);
+        PointOut<3> po;
+        point_physics_fast(J, dv, vq, eq, gcur[R::FQ + el * NQ + q], a.gamma, a.q1, a.q2, po);
+        if (po.det <= 0.0) {
+          const unsigned long long kk = (unsigned long long)q * a.ne + e;
+          key = kk < key ? kk : key;
+        }
+        clamps += po.clamped;
+        rmin = fmin(rmin, po.ratio);
+        double DF[3][3];
+        force_point<3>(po.sigma, po.jinv, sw[q] * po.det, DF);
+        const double p1 = sp[q];
+        double* W = work + el * PER;  // aliases X (dead)
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int l = 0; l < 3; ++l) {
+            s += DF[c][l] * dv[c][l];
+            W[(c * 3 + l) * NQ + q] = DF[c][l] * p1;
+          }
+        W[9 * NQ + q] = s;
+      }
+    }
+    if constexpr (MODE == 1) continue;
+    __syncthreads();
+    // ---- C2: transposed z stage, thread per (comp, column) (+ F^T v per column)
+    {
+      constexpr int TASKS = 4 * QQ;
+#pragma unroll
+      for (int rep = 0; rep < (EPC * TASKS + NT - 1) / NT; ++rep) {
+        const int it = t + rep * NT;
+        if (it >= nel * TASKS) break;
+        const int el = it / TASKS, k = it - el * TASKS;
+        const int c = k / QQ, col = k - c * QQ;
+        const double* W = work + el * PER;
+        double* Z = work + el * PER + XR;  // aliases T (dead)
+        if (c < 3) {
+          double z0[D1], z1[D1], z2[D1];
+#pragma unroll
+          for (int dz = 0; dz < D1; ++dz) {
+            z0[dz] = 0.0;
+            z1[dz] = 0.0;
+            z2[dz] = 0.0;
+          }
+#pragma unroll
+          for (int qz = 0; qz < Q; ++qz) {
+            const double s0 = W[(c * 3 + 0) * NQ + qz * QQ + col];
+            const double s1 = W[(c * 3 + 1) * NQ + qz * QQ + col];
+            const double s2 = W[(c * 3 + 2) * NQ + qz * QQ + col];
+#pragma unroll
+            for (int dz = 0; dz < D1; ++dz) {
+              z0[dz] = fma(cB[qz * D1 + dz], s0, z0[dz]);
+              z1[dz] = fma(cB[qz * D1 + dz], s1, z1[dz]);
+              z2[dz] = fma(cG[qz * D1 + dz], s2, z2[dz]);
+            }
+          }
+#pragma unroll
+          for (int dz = 0; dz < D1; ++dz) {
+            Z[((c * 3 + 0) * D1 + dz) * QQ + col] = z0[dz];
+            Z[((c * 3 + 1) * D1 + dz) * QQ + col] = z1[dz];
+            Z[((c * 3 + 2) * D1 + dz) * QQ + col] = z2[dz];
+          }
+        } else {
+          double zt[DT];
+#pragma unroll
+          for (int dz = 0; dz < DT; ++dz) zt[dz] = 0.0;
+#pragma unroll
+          for (int qz = 0; qz < Q; ++qz) {
+            const double s = W[9 * NQ + qz * QQ + col];
+#pragma unroll
+            for (int dz = 0; dz < DT; ++dz) zt[dz] = fma(cBt[qz * DT + dz], s, zt[dz]);
+          }
+#pragma unroll
+          for (int dz = 0; dz < DT; ++dz) Z[9 * D1 * QQ + dz * QQ + col] = zt[dz];
+        }
+      }
+    }
+    __syncthreads();
+    // ---- D1: transposed y stage, thread per (comp, z, qx) (+ thermo (z, qx))
+    {
+      constexpr int FL = 3 * D1 * Q;
+      constexpr int TASKS = FL + DT * Q;
+#pragma unroll
+      for (int rep = 0; rep < (EPC * TASKS + NT - 1) / NT; ++rep) {
+        const int it = t + rep * NT;
+        if (it >= nel * TASKS) break;
+        const int el = it / TASKS, k = it - el * TASKS;
+        const double* Z = work + el * PER + XR;
+        double* Y = work + el * PER;  // aliases W (dead)
+        if (k < FL) {
+          const int pl = k / Q, qx = k - pl * Q;  // pl = c*D1 + dz
+          const int c = pl / D1, dz = pl - c * D1;
+          const double* z0 = Z + ((c * 3 + 0) * D1 + dz) * QQ + qx;
+          const double* z1 = Z + ((c * 3 + 1) * D1 + dz) * QQ + qx;
+          const double* z2 = Z + ((c * 3 + 2) * D1 + dz) * QQ + qx;
+          double yg[D1], yb[D1];
+#pragma unroll
+          for (int dy = 0; dy < D1; ++dy) {
+            yg[dy] = 0.0;
+            yb[dy] = 0.0;
+          }
+#pragma unroll
+          for (int qy = 0; qy < Q; ++qy) {
+            const double r0 = z0[qy * Q], r1 = z1[qy * Q], r2 = z2[qy * Q];
+#pragma unroll
+            for (int dy = 0; dy < D1; ++dy) {
+              yg[dy] = fma(cB[qy * D1 + dy], r0, yg[dy]);
+              yb[dy] = fma(cG[qy * D1 + dy], r1, yb[dy]);
+              yb[dy] = fma(cB[qy * D1 + dy], r2, yb[dy]);
+            }
+          }
+#pragma unroll
+          for (int dy = 0; dy < D1; ++dy) {
+            Y[(pl * D1 + dy) * XP + qx] = yg[dy];
+            Y[(pl * D1 + dy) * XP + Q + qx] = yb[dy];
+          }
+        } else {
+          const int r = k - FL, dz = r / Q, qx = r - dz * Q;
+          const double* z = Z + 9 * D1 * QQ + dz * QQ + qx;
+          double y[DT];
+#pragma unroll
+          for (int dy = 0; dy < DT; ++dy) y[dy] = 0.0;
+#pragma unroll
+          for (int qy = 0; qy < Q; ++qy) {
+            const double zz = z[qy * Q];
+#pragma unroll
+            for (int dy = 0; dy < DT; ++dy) y[dy] = fma(cBt[qy * DT + dy], zz, y[dy]);
+          }
+#pragma unroll
+          for (int dy = 0; dy < DT; ++dy) Y[YFS + (dz * DT + dy) * Q + qx] = y[dy];
+        }
+      }
+    }
+    __syncthreads();
+    // ---- D2: transposed x stage, thread per (comp, z, y) row (+ thermo rows) -> staging
+    {
+      constexpr int FR = 3 * D1 * D1;
+      constexpr int TASKS = FR + DTT;
+#pragma unroll
+      for (int rep = 0; rep < (EPC * TASKS + NT - 1) / NT; ++rep) {
+        const int it = t + rep * NT;
+        if (it >= nel * TASKS) break;
+        const int el = it / TASKS, k = it - el * TASKS;
+        const double* Y = work + el * PER;
+        double* O = work + el * PER + XR;  // aliases Z (dead): [c][l] F.1, then fv
+        if (k < FR) {
+          const int c = k / DD, r = k - c * DD;  // r = dz*D1 + dy
+          double yg[Q], yb[Q];
+#pragma unroll
+          for (int qx = 0; qx < Q; ++qx) {
+            yg[qx] = Y[k * XP + qx];
+            yb[qx] = Y[k * XP + Q + qx];
+          }
+#pragma unroll
+          for (int dx = 0; dx < D1; ++dx) {
+            double s = 0.0;
+#pragma unroll
+            for (int qx = 0; qx < Q; ++qx) {
+              s = fma(cG[qx * D1 + dx], yg[qx], s);
+              s = fma(cB[qx * D1 + dx], yb[qx], s);
+            }
+            O[c * NL + r * D1 + dx] = s;
+          }
+        } else {
+          const int r = k - FR;  // dz_t*DT + dy_t
+          double y[Q];
+#pragma unroll
+          for (int qx = 0; qx < Q; ++qx) y[qx] = Y[YFS + r * Q + qx];
+#pragma unroll
+          for (int dx = 0; dx < DT; ++dx) {
+            double s = 0.0;
+#pragma unroll
+            for (int qx = 0; qx < Q; ++qx) s = fma(cBt[qx * DT + dx], y[qx], s);
+            O[3 * NL + r * DT + dx] = s;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- E: F.1 E-vector out, de = M_e^{-1} (F^T v)  (einsum "eij,ej->ei", hydro.py:343)
+    for (int it = t; it < nel * NL * 3; it += NT) {
+      const int el = it / (NL * 3), rem = it - el * (NL * 3);
+      const int l = rem / 3, c = rem - l * 3;
+      const double val = work[el * PER + XR + c * NL + l];
+      const long long e = e0 + el;
+      const long long pos = a.slot ? (long long)__ldg(a.slot + e * NL + l) * 3 + c : e * (NL * 3) + rem;
+      a.evec[pos] = val;
+    }
+    for (int it = t; it < nel * NTH; it += NT) {
+      const int el = it / NTH, i = it - el * NTH;
+      const long long e = e0 + el;
+      const double* fv = work + el * PER + XR + 3 * NL;
+      const double* mi = gcur + R::FM + (el * NTH + i) * NTH;
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < NTH; ++j) s = fma(mi[j], fv[j], s);
+      a.de[e * NTH + i] = s;
+    }
+  }
+  publish_status<256>(a.st, rmin, clamps, key, nullptr);
+}
+
+}  // namespace hx
