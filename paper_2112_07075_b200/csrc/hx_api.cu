@@ -564,6 +564,7 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
         }
       }
     }
+    ok = ok && (long long)ne * nl * 3 < (1ll << 31);  // 32-bit element-major E offsets
     const char* env = getenv("HX_BRICK");
     if (env && env[0] == '0') ok = false;
     if (ok) {
@@ -571,7 +572,8 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
       const char* ev = getenv("HX_EVEC");  // HX_EVEC=sorted: node-sorted E with the brick mass kernel
       ctx->elem_major = !(ev && strcmp(ev, "sorted") == 0);
       ctx->bk = Brick{(int)bx, (int)by, (int)bz, (int)Nx, (int)Ny, NxNy, make_fastdiv((unsigned)bx),
-                      make_fastdiv((unsigned)(bx * by)), make_fastdiv((unsigned)Nx), make_fastdiv((unsigned)NxNy)};
+                      make_fastdiv((unsigned)(bx * by)), make_fastdiv((unsigned)Nx), make_fastdiv((unsigned)NxNy),
+                      nl - p, (int)bx * nl - p * D1, (int)(bx * by) * nl - p * D1 * D1};
     }
   }
   std::vector<int> off(nn + 1, 0);

@@ -43,7 +43,20 @@ struct Brick {
   int Nx, Ny;      // nodes per direction (p*n + 1)
   long long NxNy;
   FastDiv fnx, fnxy, fNx, fNxNy;  // element / node coordinate splits
+  int dX, dY, dZ;                 // element-major E offsets (in entries / NC) between the
+                                  // lower and upper element of a shared node along x, y, z
 };
+
+// node coordinate i along an axis with n elements of order P: first (lowest) element
+// coordinate e0, its local coordinate l0, and whether the next element shares the node
+template <int P>
+__device__ __forceinline__ void axis_first(int i, int n, int& e0, int& l0, int& two) {
+  const int q = i / P, r = i - q * P;
+  const bool face = (r == 0) && (q > 0);
+  e0 = face ? q - 1 : q;
+  l0 = face ? P : r;
+  two = face && (q < n);
+}
 
 // (element coordinate, local coordinate) pairs touching node coordinate i along one
 // axis with n elements of order P, ascending element order.  Returns the count.
@@ -84,10 +97,11 @@ struct BrickSum {
     const unsigned rem = (unsigned)n - k * (unsigned)b.NxNy;
     const unsigned j = b.fNx.div(rem);
     const int i = (int)(rem - j * (unsigned)b.Nx);
-    int ex[2], lx[2], ey[2], ly[2], ez[2], lz[2];
-    const int cx = axis_pairs<P>(i, b.nx, ex, lx);
-    const int cy = axis_pairs<P>((int)j, b.ny, ey, ly);
-    const int cz = axis_pairs<P>((int)k, b.nz, ez, lz);
+    int ex, lx, tx, ey, ly, ty, ez, lz, tz;
+    axis_first<P>(i, b.nx, ex, lx, tx);
+    axis_first<P>((int)j, b.ny, ey, ly, ty);
+    axis_first<P>((int)k, b.nz, ez, lz, tz);
+    const unsigned p0 = ((unsigned)((ez * b.ny + ey) * b.nx + ex) * NL + (lz * D1 + ly) * D1 + lx) * NC + c;
     double v[8];
 #pragma unroll
     for (int a = 0; a < 2; ++a)
@@ -95,14 +109,9 @@ struct BrickSum {
       for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
-          const bool ok = a < cz && bb < cy && g < cx;
-          double t = 0.0;
-          if (ok) {
-            const long long e = ((long long)ez[a] * b.ny + ey[bb]) * b.nx + ex[g];
-            const int l = (lz[a] * D1 + ly[bb]) * D1 + lx[g];
-            t = __ldcg(E + (e * NL + l) * NC + c);
-          }
-          v[(a * 2 + bb) * 2 + g] = t;
+          const bool ok = a <= tz && bb <= ty && g <= tx;
+          const unsigned pos = p0 + (unsigned)((a * b.dZ + bb * b.dY + g * b.dX) * NC);
+          v[(a * 2 + bb) * 2 + g] = ok ? __ldcg(E + pos) : 0.0;
         }
     double s = 0.0;
 #pragma unroll
@@ -166,6 +175,19 @@ __global__ void __launch_bounds__(128, 4) k_mass_brick(MassBrickArgs a) {
   double acc = 0.0;
   const int pe = t / PLN, pr = t - pe * PLN;
   __shared__ int sbase[EPC];  // first node of each element of the pass
+  // per-thread gather / copy-out slots within an element (pass invariant)
+  constexpr int ROWI = D1 * NC;                 // pairs per node row
+  constexpr int ELI = DD * ROWI;                // pairs (= E entries) per element
+  constexpr int SLOTS = (ELI + 127) / 128;
+  int soff[SLOTS], goff[SLOTS];
+#pragma unroll
+  for (int h = 0; h < SLOTS; ++h) {
+    const int it = h * 128 + t;
+    const int row = it / ROWI, s = it - row * ROWI;  // row = dz*D1 + dy
+    const int dz = row / D1, dy = row - dz * D1, dx = s / NC, c = s - dx * NC;
+    soff[h] = (c * D1 + dz) * GP + dy * D1 + dx;
+    goff[h] = (dx + dy * a.b.Nx + dz * (int)a.b.NxNy) * NC + c;
+  }
   for (long long e0 = (long long)blockIdx.x * EPC; e0 < a.ne; e0 += (long long)gridDim.x * EPC) {
     const int nel = (int)((a.ne - e0) < EPC ? (a.ne - e0) : EPC);
     if (t < nel) {
@@ -176,36 +198,19 @@ __global__ void __launch_bounds__(128, 4) k_mass_brick(MassBrickArgs a) {
       sbase[t] = (int)(ex * P + (ey * P) * (unsigned)a.b.Nx + (ez * P) * (unsigned)a.b.NxNy);
     }
     __syncthreads();
-    // ---- phase 0: node rows (D1 nodes x NC pairs, contiguous) -> p image
-    // (all of a thread's loads are issued before the first use: one latency per pass)
-    constexpr int ROWI = D1 * NC;  // pairs per row
-    constexpr int NIT = (EPC * DD * ROWI + 127) / 128;
-    constexpr int BAT = 8;
-#pragma unroll 1
-    for (int u0 = 0; u0 < NIT; u0 += BAT) {
-      double2 q[BAT];
+    // ---- phase 0: node rows (D1 nodes x NC pairs, contiguous) -> p image.  Thread t
+    // owns the same (row, pair) slots of every element of the pass (offsets hoisted
+    // out of the pass loop); all loads of a slot are issued before the first use.
 #pragma unroll
-      for (int u = 0; u < BAT; ++u) {
-        const int it = t + (u0 + u) * 128;
-        const int el = it / (DD * ROWI);
-        const int rem = it - el * (DD * ROWI);
-        const int row = rem / ROWI, s = rem - row * ROWI;  // row = dz*D1 + dy
-        const int dz = row / D1, dy = row - dz * D1;
-        const int dx = s / NC, c = s - dx * NC;
-        if (el < nel && u0 + u < NIT) {
-          const long long n = sbase[el] + dx + dy * a.b.Nx + dz * (int)a.b.NxNy;
-          q[u] = __ldcg(reinterpret_cast<const double2*>(po) + n * NC + c);
-        }
-      }
+    for (int h = 0; h < SLOTS; ++h) {
+      if (h * 128 + t < ELI) {
+        double2 q[EPC];
 #pragma unroll
-      for (int u = 0; u < BAT; ++u) {
-        const int it = t + (u0 + u) * 128;
-        const int el = it / (DD * ROWI);
-        const int rem = it - el * (DD * ROWI);
-        const int row = rem / ROWI, s = rem - row * ROWI;
-        const int dx = s / NC, c = s - dx * NC;
-        if (el < nel && u0 + u < NIT) sG[el * GS + c * D1 * GP + (row / D1) * GP + (row % D1) * D1 + dx] =
-            __dadd_rn(q[u].x, __dmul_rn(beta, q[u].y));
+        for (int el = 0; el < EPC; ++el)
+          if (el < nel) q[el] = __ldcg(reinterpret_cast<const double2*>(po) + (long long)sbase[el] * NC + goff[h]);
+#pragma unroll
+        for (int el = 0; el < EPC; ++el)
+          if (el < nel) sG[el * GS + soff[h]] = __dadd_rn(q[el].x, __dmul_rn(beta, q[el].y));
       }
     }
     __syncthreads();
@@ -311,13 +316,17 @@ __global__ void __launch_bounds__(128, 4) k_mass_brick(MassBrickArgs a) {
         for (int c = 0; c < NC; ++c) __stcg(a.evec + pos + c, sG[el * GS + (c * D1 + dz) * GP + k]);
       }
     } else {
+      // E entry (l, c) of an element sits at l*NC + c = (row*D1 + dx)*NC + c: the same
+      // slot enumeration as the gather, so soff maps it to the staging image
       double* out = a.evec + e0 * (NL * NC);
-      for (int it = t; it < nel * NL * NC; it += 128) {
-        const int el = it / (NL * NC);
-        const int rem = it - el * (NL * NC);
-        const int l = rem / NC, c = rem - l * NC;
-        const int dz = l / DD, k = l - dz * DD;
-        __stcg(out + it, sG[el * GS + (c * D1 + dz) * GP + k]);
+#pragma unroll
+      for (int h = 0; h < SLOTS; ++h) {
+        const int it = h * 128 + t;
+        if (it < ELI) {
+#pragma unroll
+          for (int el = 0; el < EPC; ++el)
+            if (el < nel) __stcg(out + el * ELI + it, sG[el * GS + soff[h]]);
+        }
       }
     }
     __syncthreads();
