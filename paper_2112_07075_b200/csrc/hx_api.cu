@@ -44,7 +44,8 @@ struct hx_ctx {
   double* evec = nullptr;     // (NE, nl, d)
   double* evec2 = nullptr;    // second E buffer (API scatter staging)
   double *r = nullptr, *z = nullptr, *p0 = nullptr, *p1 = nullptr;
-  double* partials = nullptr; // reduction partials
+  double* partials = nullptr; // reduction partials: two regions of preg doubles
+  long long preg = 0;
   double* hist = nullptr;     // CG residual history
   int hist_len = 0;
   CGDev* cg = nullptr;        // [2]: stage-1 and stage-2 momentum solves
@@ -315,21 +316,7 @@ static int launch_mass_pc(hx_ctx* ctx, bool cgmode, const MassArgs& a) {
   return HX_OK;
 }
 
-template <int P, int NC>
-static int launch_mass_tma(hx_ctx* ctx, const MassArgs& a) {
-  using M = MassTMA<P, NC>;
-  auto k = k_mass_tma<P, NC>;
-  CK(smem_attr(k, M::bytes));
-  static unsigned grid = 0;
-  if (!grid) grid = persistent_grid(k, 128, M::bytes, 1ll << 40);
-  prof_begin(ctx, K_MASS);
-  k<<<std::min(grid, gblocks(ctx->ne, M::EPC)), 128, M::bytes, ctx->stream>>>(a);
-  prof_end(ctx);
-  CKL();
-  return HX_OK;
-}
-
-static int g_mass_variant = -1;  // HX_MASS_KERNEL=line|pc|tma (default pc for p<=3; tma: async-pipelined CG variant)
+static int g_mass_variant = -1;  // HX_MASS_KERNEL=line|pc (generic 3D meshes; default pc for p<=3)
 
 template <int P, int NC>
 static int launch_mass3d(hx_ctx* ctx, bool cgmode, const MassArgs& a) {
@@ -337,9 +324,7 @@ static int launch_mass3d(hx_ctx* ctx, bool cgmode, const MassArgs& a) {
     const char* v = getenv("HX_MASS_KERNEL");
     g_mass_variant = 2;
     if (v && strcmp(v, "line") == 0) g_mass_variant = 1;
-    if (v && strcmp(v, "tma") == 0) g_mass_variant = 3;
   }
-  if (g_mass_variant == 3 && P <= 3 && cgmode) return launch_mass_tma<P, NC>(ctx, a);
   if (g_mass_variant >= 2 && P <= 3) return launch_mass_pc<P, NC>(ctx, cgmode, a);
   return launch_mass3w<P, NC>(ctx, cgmode, a);
 }
@@ -643,7 +628,8 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   ok &= dalloc(&ctx->p1, 2 * nv) == cudaSuccess;
   ok &= dalloc(&ctx->emapf, (size_t)ne * nl + 8) == cudaSuccess;
   ok &= dalloc(&ctx->emapf_api, (size_t)ne * nl + 8) == cudaSuccess;
-  ok &= dalloc(&ctx->partials, 2 * (size_t)std::max<long long>(gblocks(3 * nn, 256), gblocks(ne, 1)) + 64) == cudaSuccess;
+  ctx->preg = 2 * std::max<long long>(gblocks(3 * nn, 256), gblocks(ne, 1)) + 64;
+  ok &= dalloc(&ctx->partials, 2 * (size_t)ctx->preg) == cudaSuccess;
   ok &= dalloc(&ctx->cg, 2) == cudaSuccess;
   ok &= dalloc(&ctx->t_dev, 1) == cudaSuccess;
   ok &= cudaMallocHost((void**)&ctx->h_t, sizeof(double)) == cudaSuccess;
@@ -997,7 +983,9 @@ static int cg_prepare(hx_ctx* ctx, CGDev* cg, const double* D, const double* rhs
   na.rhs = rhs;
   na.nn = ctx->nn;
   na.cg = cg;
+  const size_t preg = (size_t)ctx->preg;  // partial regions: [node / init | mass]
   na.partials = ctx->partials;
+  na.pm = ctx->partials + preg;
   na.hist = hist;
   na.negate = negate;
   na.tol = rel_tol;
@@ -1017,10 +1005,10 @@ static int cg_prepare(hx_ctx* ctx, CGDev* cg, const double* D, const double* rhs
   ma.ne = ctx->ne;
   ma.evec = ctx->evec;
   ma.cg = cg;
-  ma.partials = ctx->partials;
+  ma.partials = ctx->partials + preg;
   L.nc = nc;
   L.mb = MassBrickArgs{ctx->p0, ctx->p1, D, ctx->ne, ctx->evec, ctx->elem_major ? nullptr : ctx->slot, cg,
-                       ctx->partials, ctx->bk};
+                       ctx->partials + preg, ctx->bk};
   return HX_OK;
 }
 
@@ -1034,46 +1022,20 @@ static int cg_launch_init(hx_ctx* ctx, CGLaunch& L) {
   return HX_OK;
 }
 
-template <int P, int NC>
-static int launch_cg_node_brick(hx_ctx* ctx, const NodeArgs& na) {
-  auto k = k_cg_node_brick<P, NC>;
-  static unsigned cap = 0;
-  if (!cap) cap = persistent_grid(k, 256, 0, 1ll << 40);
-  prof_begin(ctx, K_CGNODE);
-  k<<<std::min(gblocks(ctx->nn, 256), cap), 256, 0, ctx->stream>>>(na, ctx->bk);
-  prof_end(ctx);
-  CKL();
-  return HX_OK;
-}
-
-static int g_node_kernel = -1;  // HX_NODE_KERNEL=node: thread-per-node brick node pass (element-major E)
-
-static int cg_node_brick(hx_ctx* ctx, int nc, const NodeArgs& na) {
-  switch (ctx->p * 10 + nc) {
-    case 21: return launch_cg_node_brick<2, 1>(ctx, na);
-    case 22: return launch_cg_node_brick<2, 2>(ctx, na);
-    case 23: return launch_cg_node_brick<2, 3>(ctx, na);
-    case 31: return launch_cg_node_brick<3, 1>(ctx, na);
-    case 32: return launch_cg_node_brick<3, 2>(ctx, na);
-    case 33: return launch_cg_node_brick<3, 3>(ctx, na);
-    case 41: return launch_cg_node_brick<4, 1>(ctx, na);
-    case 42: return launch_cg_node_brick<4, 2>(ctx, na);
-    case 43: return launch_cg_node_brick<4, 3>(ctx, na);
-  }
-  return fail(ctx, HX_EINVAL, "brick node pass: unsupported p=%d nc=%d", ctx->p, nc);
-}
-
 static int cg_launch_iter(hx_ctx* ctx, CGLaunch& L) {
   int rc = ctx->brick ? mass_brick(ctx, L.nc, L.mb) : dispatch<LaunchMass>(ctx, L.nc, true, L.ma);
   if (rc) return rc;
-  if (g_node_kernel < 0) {
-    const char* v = getenv("HX_NODE_KERNEL");
-    g_node_kernel = (v && strcmp(v, "node") == 0) ? 1 : 0;
-  }
-  if (ctx->elem_major && g_node_kernel == 1) return cg_node_brick(ctx, L.nc, L.na);
   return with_node_sum(ctx, L.nc, ctx->evec, [&](auto sum, auto ncc) {
     return launch_cg_nodes<decltype(ncc)::value>(ctx, L.na, sum, false);
   });
+}
+
+static int cg_launch_finish(hx_ctx* ctx, CGLaunch& L) {
+  const long long n = ctx->nn * L.nc;
+  k_cg_finish<<<std::min<unsigned>(gblocks(n, 256), 1184), 256, 0, ctx->stream>>>(L.na.cg, ctx->p0, ctx->p1,
+                                                                                  L.na.x, n);
+  CKL();
+  return HX_OK;
 }
 
 static void cg_info_from(const CGDev& g, hx_cg_info* info) {
@@ -1107,6 +1069,8 @@ static int run_cg(hx_ctx* ctx, const double* D, const double* rhs, const double*
     if (done_iters > max_iter + 1) break;
     chunk = std::min(chunk * 2, 64);
   }
+  rc = cg_launch_finish(ctx, L);
+  if (rc) return rc;
   cg_info_from(*ctx->h_cg, info);
   return HX_OK;
 }
@@ -1141,7 +1105,7 @@ static int cg_capture(hx_ctx* ctx, CGLaunch& L) {
   ctx->stream = outer;
   if (rc) return rc;
   CK(cudaStreamEndCapture(ctx->gstream2, &body));
-  return HX_OK;
+  return cg_launch_finish(ctx, L);
 }
 
 __global__ void k_recip(const double* in, long long n, double* out) {
@@ -1550,7 +1514,7 @@ static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_
   CK(cudaStreamSynchronize(ctx->stream));
   const StatusDev s0 = ctx->h_st[0], s1 = ctx->h_st[1], s2 = ctx->h_st[2];
   const CGDev c0 = ctx->h_cg[0], c1 = ctx->h_cg[1];
-  ctx->launches += 9 + 2 * (long long)(c0.iters + c1.iters);
+  ctx->launches += 11 + 2 * (long long)(c0.iters + c1.iters);
   hx_step_info out{};
   const bool estimate = dt_fixed < 0.0;
   long long clamps = 0;

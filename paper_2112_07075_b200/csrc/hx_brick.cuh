@@ -58,33 +58,6 @@ __device__ __forceinline__ void axis_first(int i, int n, int& e0, int& l0, int& 
   two = face && (q < n);
 }
 
-// (element coordinate, local coordinate) pairs touching node coordinate i along one
-// axis with n elements of order P, ascending element order.  Returns the count.
-template <int P>
-__device__ __forceinline__ int axis_pairs(int i, int n, int (&ec)[2], int (&lc)[2]) {
-  const int q = i / P, r = i - q * P;
-  if (r != 0) {
-    ec[0] = q;
-    lc[0] = r;
-    return 1;
-  }
-  if (q == 0) {
-    ec[0] = 0;
-    lc[0] = 0;
-    return 1;
-  }
-  if (q == n) {
-    ec[0] = n - 1;
-    lc[0] = P;
-    return 1;
-  }
-  ec[0] = q - 1;
-  lc[0] = P;
-  ec[1] = q;
-  lc[1] = 0;
-  return 2;
-}
-
 // deterministic node sum of an element-major E-vector (NE, nl, NC): ascending element
 // order from 0.0, all (up to 8) loads issued before the adds
 template <int P, int NC>
@@ -158,7 +131,7 @@ struct MassBrickArgs {
 };
 
 template <int P, int NC>
-__global__ void __launch_bounds__(128, 4) k_mass_brick(MassBrickArgs a) {
+__global__ void __launch_bounds__(128, P >= 4 ? 4 : 5) k_mass_brick(MassBrickArgs a) {
   using M = MassBrickCfg<P, NC>;
   constexpr int D1 = M::D1, Q = M::Q, QQ = M::QQ, DD = M::DD, NL = M::NL, NQ = M::NQ;
   constexpr int PLN = M::PLN, EPC = M::EPC, GP = M::GP, GS = M::GS;
@@ -167,11 +140,11 @@ __global__ void __launch_bounds__(128, 4) k_mass_brick(MassBrickArgs a) {
   double* sG = smem;                 // gather image [el][c][dz][dy*D1+dx] (pitch GP); reused as staging
   double* sT = smem + EPC * GS;      // T image [el][c][dz][qy*Q+qx]
   __shared__ double red[32];
-  __shared__ int sflag;
-  if (!a.cg->active) return;
+  double beta;
+  int k;
+  if (!cg_mass_begin<128>(a.cg, red, beta, k)) return;
   const int t = threadIdx.x;
-  const double beta = a.cg->beta;
-  const double* po = (a.cg->it & 1) ? a.pbuf0 : a.pbuf1;
+  const double* po = (k & 1) ? a.pbuf0 : a.pbuf1;
   double acc = 0.0;
   const int pe = t / PLN, pr = t - pe * PLN;
   __shared__ int sbase[EPC];  // first node of each element of the pass
@@ -188,8 +161,13 @@ __global__ void __launch_bounds__(128, 4) k_mass_brick(MassBrickArgs a) {
     soff[h] = (c * D1 + dz) * GP + dy * D1 + dx;
     goff[h] = (dx + dy * a.b.Nx + dz * (int)a.b.NxNy) * NC + c;
   }
-  for (long long e0 = (long long)blockIdx.x * EPC; e0 < a.ne; e0 += (long long)gridDim.x * EPC) {
-    const int nel = (int)((a.ne - e0) < EPC ? (a.ne - e0) : EPC);
+  // balanced contiguous element range per CTA, walked in passes of up to EPC elements
+  // (all CTAs finish within one pass of each other)
+  const long long ebeg = a.ne * blockIdx.x / gridDim.x, eend = a.ne * (blockIdx.x + 1) / gridDim.x;
+  const int npass = (int)((eend - ebeg + EPC - 1) / EPC);
+  for (int ps = 0; ps < npass; ++ps) {
+    const long long e0 = ebeg + (eend - ebeg) * ps / npass;
+    const int nel = (int)(ebeg + (eend - ebeg) * (ps + 1) / npass - e0);
     if (t < nel) {
       const unsigned e = (unsigned)(e0 + t);
       const unsigned ez = a.b.fnxy.div(e);
@@ -204,13 +182,18 @@ __global__ void __launch_bounds__(128, 4) k_mass_brick(MassBrickArgs a) {
 #pragma unroll
     for (int h = 0; h < SLOTS; ++h) {
       if (h * 128 + t < ELI) {
-        double2 q[EPC];
+        constexpr int BAT = EPC < 6 ? EPC : 6;
 #pragma unroll
-        for (int el = 0; el < EPC; ++el)
-          if (el < nel) q[el] = __ldcg(reinterpret_cast<const double2*>(po) + (long long)sbase[el] * NC + goff[h]);
+        for (int e1 = 0; e1 < EPC; e1 += BAT) {
+          double2 q[BAT];
 #pragma unroll
-        for (int el = 0; el < EPC; ++el)
-          if (el < nel) sG[el * GS + soff[h]] = __dadd_rn(q[el].x, __dmul_rn(beta, q[el].y));
+          for (int u = 0; u < BAT; ++u)
+            if (e1 + u < nel)
+              q[u] = __ldcg(reinterpret_cast<const double2*>(po) + (long long)sbase[e1 + u] * NC + goff[h]);
+#pragma unroll
+          for (int u = 0; u < BAT; ++u)
+            if (e1 + u < nel) sG[(e1 + u) * GS + soff[h]] = __dadd_rn(q[u].x, __dmul_rn(beta, q[u].y));
+        }
       }
     }
     __syncthreads();
@@ -331,137 +314,7 @@ __global__ void __launch_bounds__(128, 4) k_mass_brick(MassBrickArgs a) {
     }
     __syncthreads();
   }
-  const double bs = block_sum<128>(acc, red);
-  if (threadIdx.x == 0) a.partials[blockIdx.x] = bs;
-  if (grid_last_block(&a.cg->cnt[0], &sflag)) {
-    const double pAp = reduce_partials<128>(a.partials, gridDim.x, red);
-    if (threadIdx.x == 0) {
-      a.cg->cnt[0] = 0;
-      if (pAp <= 0.0) {
-        a.cg->code = 3;
-        a.cg->active = 0;
-      } else {
-        a.cg->alpha = a.cg->rz / pAp;
-      }
-    }
-  }
-}
-
-}  // namespace hx
-
-namespace hx {
-
-// entries of node n in an element-major E-vector: up to 8 (element, local) positions in
-// ascending element order (absent ones: -1)
-template <int P, int NC>
-__device__ __forceinline__ void brick_entries(const Brick& b, unsigned n, long long (&pos)[8]) {
-  constexpr int D1 = P + 1, NL = D1 * D1 * D1;
-  const unsigned k = b.fNxNy.div(n);
-  const unsigned rem = n - k * (unsigned)b.NxNy;
-  const unsigned j = b.fNx.div(rem);
-  const int i = (int)(rem - j * (unsigned)b.Nx);
-  int ex[2], lx[2], ey[2], ly[2], ez[2], lz[2];
-  const int cx = axis_pairs<P>(i, b.nx, ex, lx);
-  const int cy = axis_pairs<P>((int)j, b.ny, ey, ly);
-  const int cz = axis_pairs<P>((int)k, b.nz, ez, lz);
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int bb = 0; bb < 2; ++bb)
-#pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        const bool ok = a < cz && bb < cy && g < cx;
-        const long long e = ((long long)ez[a] * b.ny + ey[bb]) * b.nx + ex[g];
-        const int l = (lz[a] * D1 + ly[bb]) * D1 + lx[g];
-        pos[(a * 2 + bb) * 2 + g] = ok ? (e * NL + l) * NC : -1;
-      }
-}
-
-// all NC components of node n from an element-major E-vector, ascending element order
-template <int P, int NC>
-__device__ __forceinline__ void brick_node_sum(const Brick& b, const double* E, unsigned n, double (&s)[NC]) {
-  long long pos[8];
-  brick_entries<P, NC>(b, n, pos);
-  double v[8][NC];
-#pragma unroll
-  for (int q = 0; q < 8; ++q)
-#pragma unroll
-    for (int c = 0; c < NC; ++c) v[q][c] = pos[q] >= 0 ? __ldcg(E + pos[q] + c) : 0.0;
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    double t = 0.0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) t += v[q][c];  // absent entries are +0.0: sums unchanged
-    s[c] = t;
-  }
-}
-
-// CG iteration tail on a brick, one thread per node (all components): the same
-// recurrence and rounding as k_cg_node (operators.py:352-365).
-template <int P, int NC>
-__global__ void __launch_bounds__(256, 3) k_cg_node_brick(NodeArgs a, Brick b) {
-  __shared__ double red[32];
-  __shared__ int sflag;
-  CGDev* g = a.cg;
-  if (!g->active) return;
-  const int k = g->it;
-  const double alpha = g->alpha, beta = g->beta;
-  const double* po = (k & 1) ? a.pbuf0 : a.pbuf1;
-  double* pn = (k & 1) ? a.pbuf1 : a.pbuf0;
-  double rz = 0.0;
-  const unsigned nn = (unsigned)a.nn;
-  for (unsigned n = blockIdx.x * blockDim.x + threadIdx.x; n < nn; n += gridDim.x * blockDim.x) {
-    double s[NC];
-    brick_node_sum<P, NC>(b, a.evec, n, s);
-    double2 zp[NC];
-    double xj[NC], rj[NC], dj[NC];
-    bool m[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const long long j = (long long)n * NC + c;
-      zp[c] = __ldcg(reinterpret_cast<const double2*>(po) + j);
-      xj[c] = __ldcg(a.x + j);
-      rj[c] = __ldcg(a.r + j);
-      dj[c] = __ldg(a.invd + j);
-      m[c] = a.mask && a.mask[j];
-    }
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const long long j = (long long)n * NC + c;
-      const double p = __dadd_rn(zp[c].x, __dmul_rn(beta, zp[c].y));
-      const double ap = m[c] ? p : s[c];
-      a.x[j] = __dadd_rn(xj[c], __dmul_rn(alpha, p));
-      const double r = __dsub_rn(rj[c], __dmul_rn(alpha, ap));
-      a.r[j] = r;
-      const double z = __dmul_rn(dj[c], r);
-      reinterpret_cast<double2*>(pn)[j] = make_double2(z, p);
-      rz = fma(r, z, rz);
-    }
-  }
-  const double brz = block_sum<256>(rz, red);
-  if (threadIdx.x == 0) a.partials[blockIdx.x] = brz;
-  if (grid_last_block(&g->cnt[1], &sflag)) {
-    const double rzn = reduce_partials<256>(a.partials, gridDim.x, red);
-    if (threadIdx.x == 0) {
-      g->cnt[1] = 0;
-      const double res = sqrt(fmax(rzn, 0.0));
-      if (a.hist) a.hist[k] = res;
-      g->nres = k + 1;
-      if (res <= g->tol * g->norm0) {
-        g->iters = k;
-        g->active = 0;
-      } else if (k >= g->max_iter) {
-        g->code = 4;
-        g->iters = k;
-        g->active = 0;
-      } else {
-        g->beta = rzn / g->rz;
-        g->rz = rzn;
-        g->it = k + 1;
-      }
-      cg_publish(g);
-    }
-  }
+  cg_partial(a.partials, &a.cg->nparts_m, block_sum<128>(acc, red));
 }
 
 }  // namespace hx

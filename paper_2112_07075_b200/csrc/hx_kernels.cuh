@@ -317,8 +317,22 @@ __global__ void __launch_bounds__(NT) k_rates(RatesArgs a) {
 // _solve_momentum (hydro.py:323-327) and the element-wise p.Ap partial:
 //   p.Ap = sum_e sum_q D (B w_e)^2 + sum_{masked} p^2.
 
+// Device CG state.  Each iteration k is a mass launch M(k) and a node launch N(k).
+// Grid reductions are finished by the CONSUMER launch: every CTA of N(k) sums M(k)'s
+// per-CTA p.Ap partials in the same fixed order (-> alpha_k), every CTA of M(k+1)
+// sums N(k)'s r.z partials (-> stop test, beta_{k+1}); block 0 publishes the scalars.
+// No fences, atomics or last-block tails on the iteration path.  Scalars that a
+// launch reads while its block 0 writes the next value are ping-ponged by parity.
 struct CGDev {
   double rz, norm0, alpha, beta, tol;
+  double rz2[2];      // rz_k at [k & 1]
+  double alpha2[2];   // alpha_k at [k & 1]
+  int pend;           // x lags one iteration: k (odd) whose x += a_k p_k is still to apply, else 0
+  int it_m, it_n;     // iteration index of the next mass / node launch
+  int nparts_m, nparts_n;
+  const double* parts_m;  // per-CTA p.Ap partials of the last mass launch
+  const double* parts_n;  // per-CTA r.z partials of the last node launch
+  double* hist;
   int it, active, code, iters, max_iter, nres;
   unsigned int cnt[4];
   unsigned long long cond;  // cudaGraphConditionalHandle of the WHILE node (graph mode)
@@ -340,6 +354,88 @@ __device__ __forceinline__ double cg_dir(const double* zp, long long j, double b
 // publish the CG "continue" flag to the enclosing WHILE graph node
 __device__ __forceinline__ void cg_publish(const CGDev* g) {
   if (g->use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)g->cond, g->active ? 1u : 0u);
+}
+
+// fixed-order sum of n grid partials, broadcast to every thread of the CTA
+template <int NT>
+__device__ __forceinline__ double reduce_bcast(const double* parts, int n, double* red) {
+  __shared__ double bc;
+  const double v = reduce_partials<NT>(parts, n, red);
+  if (threadIdx.x == 0) bc = v;
+  __syncthreads();
+  return bc;
+}
+
+// mass-launch prologue of iteration k = it_m: for k >= 2 finish N(k-1)'s r.z
+// reduction, stop test (operators.py:361-362) and beta_k = rz_{k-1}/rz_{k-2}.
+// Returns false when this launch has nothing to do.
+template <int NT>
+__device__ __forceinline__ bool cg_mass_begin(CGDev* g, double* red, double& beta, int& k) {
+  if (!g->active) return false;
+  k = g->it_m;
+  if (k == 1) {
+    beta = 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) g->it_n = 1;
+    return true;
+  }
+  const double rzk = reduce_bcast<NT>(g->parts_n, g->nparts_n, red);
+  const double res = sqrt(fmax(rzk, 0.0));
+  const bool conv = res <= g->tol * g->norm0;
+  const bool maxed = !conv && (k - 1 >= g->max_iter);
+  const double rzp = g->rz2[(k - 2) & 1];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (g->hist) g->hist[k - 1] = res;
+    g->nres = k;
+    if (conv || maxed) {
+      g->iters = k - 1;
+      if (maxed) g->code = 4;
+      g->active = 0;
+      cg_publish(g);
+    } else {
+      g->rz2[(k - 1) & 1] = rzk;
+      g->rz = rzk;
+      g->beta = rzk / rzp;
+      g->it_n = k;
+    }
+  }
+  if (conv || maxed) return false;
+  beta = rzk / rzp;
+  return true;
+}
+
+// node-launch prologue of iteration k = it_n: finish M(k)'s p.Ap reduction,
+// breakdown test (operators.py:354-355), alpha_k = rz_{k-1}/pAp.
+template <int NT>
+__device__ __forceinline__ bool cg_node_begin(CGDev* g, double* red, double& alpha, double& alpha_prev, int& k) {
+  if (!g->active) return false;
+  k = g->it_n;
+  const double pAp = reduce_bcast<NT>(g->parts_m, g->nparts_m, red);
+  if (pAp <= 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      g->code = 3;
+      g->active = 0;
+      cg_publish(g);
+    }
+    return false;
+  }
+  alpha = g->rz2[(k - 1) & 1] / pAp;
+  alpha_prev = g->alpha2[(k - 1) & 1];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    g->alpha2[k & 1] = alpha;
+    g->alpha = alpha;
+    g->it = k;
+    g->it_m = k + 1;
+    g->pend = (k & 1) ? k : 0;
+  }
+  return true;
+}
+
+// per-CTA partial of a CG launch (block 0 also records the grid size for the consumer)
+__device__ __forceinline__ void cg_partial(double* parts, int* nparts, double v) {
+  if (threadIdx.x == 0) {
+    parts[blockIdx.x] = v;
+    if (blockIdx.x == 0) *nparts = (int)gridDim.x;
+  }
 }
 
 struct MassArgs {
@@ -375,12 +471,14 @@ __global__ void __launch_bounds__(128) k_mass(MassArgs a) {
   constexpr int BUF = NC * NQ;
   extern __shared__ double smem[];
   __shared__ double red[32];
-  __shared__ int sflag;
   double* sB = smem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* A = smem + Q * D1 + warp * 2 * BUF;
   double* Bf = A + BUF;
-  if (CG && !a.cg->active) return;
+  double cg_beta = 0.0;
+  int cg_k = 0;
+  if constexpr (CG)
+    if (!cg_mass_begin<128>(a.cg, red, cg_beta, cg_k)) return;
   for (int i = threadIdx.x; i < Q * D1; i += blockDim.x) sB[i] = a.B[i];
   __syncthreads();
   const long long e = (long long)blockIdx.x * WARPS + warp;
@@ -389,8 +487,8 @@ __global__ void __launch_bounds__(128) k_mass(MassArgs a) {
   const double* pz = a.x;
   const double* po = nullptr;
   if constexpr (CG) {
-    beta = a.cg->beta;
-    po = (a.cg->it & 1) ? a.pbuf0 : a.pbuf1;  // (z, p)_{k-1} lives in pbuf[(k-1)&1]
+    beta = cg_beta;
+    po = (cg_k & 1) ? a.pbuf0 : a.pbuf1;  // (z, p)_{k-1} lives in pbuf[(k-1)&1]
   }
   if (e < a.ne) {
     const int* em = a.emap + e * NL;
@@ -431,20 +529,7 @@ __global__ void __launch_bounds__(128) k_mass(MassArgs a) {
     }
   }
   if constexpr (CG) {
-    const double bs = block_sum<128>(acc, red);
-    if (threadIdx.x == 0) a.partials[blockIdx.x] = bs;
-    if (grid_last_block(&a.cg->cnt[0], &sflag)) {
-      const double pAp = reduce_partials<128>(a.partials, gridDim.x, red);
-      if (threadIdx.x == 0) {
-        a.cg->cnt[0] = 0;
-        if (pAp <= 0.0) {
-          a.cg->code = 3;
-          a.cg->active = 0;
-        } else {
-          a.cg->alpha = a.cg->rz / pAp;
-        }
-      }
-    }
+    cg_partial(a.partials, &a.cg->nparts_m, block_sum<128>(acc, red));
   }
 }
 
@@ -537,8 +622,10 @@ __global__ void __launch_bounds__(128, MINB) k_mass3w(MassArgs a) {
   constexpr int ZR = (Q2 * NC + 31) / 32;     // z-stage rounds (columns per lane)
   extern __shared__ double smem[];
   __shared__ double red[32];
-  __shared__ int sflag;
-  if (CG && !a.cg->active) return;
+  double cg_beta = 0.0;
+  int cg_k = 0;
+  if constexpr (CG)
+    if (!cg_mass_begin<32 * WPB>(a.cg, red, cg_beta, cg_k)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* A = smem + warp * 2 * BUF;
   double* Bb = A + BUF;
@@ -549,8 +636,8 @@ __global__ void __launch_bounds__(128, MINB) k_mass3w(MassArgs a) {
     double beta = 0.0;
     const double* po = nullptr;
     if constexpr (CG) {
-      beta = a.cg->beta;
-      po = (a.cg->it & 1) ? a.pbuf0 : a.pbuf1;
+      beta = cg_beta;
+      po = (cg_k & 1) ? a.pbuf0 : a.pbuf1;
     }
     const int* em = (CG ? a.emapf : a.emap) + e * NL;
     int wd[GR];
@@ -651,20 +738,7 @@ __global__ void __launch_bounds__(128, MINB) k_mass3w(MassArgs a) {
     __syncwarp();
   }
   if constexpr (CG) {
-    const double bs = block_sum<32 * WPB>(acc, red);
-    if (threadIdx.x == 0) a.partials[blockIdx.x] = bs;
-    if (grid_last_block(&a.cg->cnt[0], &sflag)) {
-      const double pAp = reduce_partials<32 * WPB>(a.partials, gridDim.x, red);
-      if (threadIdx.x == 0) {
-        a.cg->cnt[0] = 0;
-        if (pAp <= 0.0) {
-          a.cg->code = 3;
-          a.cg->active = 0;
-        } else {
-          a.cg->alpha = a.cg->rz / pAp;
-        }
-      }
-    }
+    cg_partial(a.partials, &a.cg->nparts_m, block_sum<32 * WPB>(acc, red));
   }
 }
 
@@ -693,15 +767,17 @@ __global__ void __launch_bounds__(128, 4) k_mass_pc(MassArgs a) {
   const double* cB = c_B[P - 1];
   extern __shared__ double smem[];
   __shared__ double red[32];
-  __shared__ int sflag;
-  if (CG && !a.cg->active) return;
+  double cg_beta = 0.0;
+  int cg_k = 0;
+  if constexpr (CG)
+    if (!cg_mass_begin<128>(a.cg, red, cg_beta, cg_k)) return;
   const int t = threadIdx.x;
   double acc = 0.0;
   double beta = 0.0;
   const double* po = nullptr;
   if constexpr (CG) {
-    beta = a.cg->beta;
-    po = (a.cg->it & 1) ? a.pbuf0 : a.pbuf1;
+    beta = cg_beta;
+    po = (cg_k & 1) ? a.pbuf0 : a.pbuf1;
   }
   const int pe = t / PLN, pr = t - pe * PLN;
   const int pc = pr / D1, pz = pr - pc * D1;  // plane: component pc, z index pz
@@ -814,306 +890,7 @@ __global__ void __launch_bounds__(128, 4) k_mass_pc(MassArgs a) {
     __syncthreads();
   }
   if constexpr (CG) {
-    const double bs = block_sum<128>(acc, red);
-    if (threadIdx.x == 0) a.partials[blockIdx.x] = bs;
-    if (grid_last_block(&a.cg->cnt[0], &sflag)) {
-      const double pAp = reduce_partials<128>(a.partials, gridDim.x, red);
-      if (threadIdx.x == 0) {
-        a.cg->cnt[0] = 0;
-        if (pAp <= 0.0) {
-          a.cg->code = 3;
-          a.cg->active = 0;
-        } else {
-          a.cg->alpha = a.cg->rz / pAp;
-        }
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Asynchronous-pipelined 3D PA mass for the CG (plane + column compute as in
-// k_mass_pc).  Per CTA, element groups flow through a 3-stage pipeline:
-//   * TMA bulk copies (cp.async.bulk, mbarrier completion) bring the contiguous
-//     per-group metadata -- packed element map, node-sorted slots, point data D --
-//     for the group after next into a double buffer;
-//   * cp.async 16-byte gathers fetch the next group's (z, p_{k-1}) pairs into a
-//     padded shared image while the current group computes;
-//   * the current group runs x/y (planes, registers), z (columns), y^T/x^T (planes).
-// No register holds in-flight data, so the gather latency overlaps compute.
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// 1D bulk copy global -> shared, completion counted on bar (16-byte aligned, size % 16 == 0)
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-template <int P, int NC>
-struct MassTMA {
-  static constexpr int D1 = P + 1, Q = P + 2, QQ = Q * Q, DD = D1 * D1, NL = D1 * DD, NQ = Q * Q * Q;
-  static constexpr int PLN = NC * D1;
-  static constexpr int EPC = 128 / PLN;
-  // metadata buffer: packed map (int), slots (int), D (double); each region padded for
-  // 16-byte-aligned bulk copies of a possibly unaligned source range
-  static constexpr int META_MAP = (EPC * NL * 4 + 32 + 15) / 16 * 16;
-  static constexpr int META_D = (EPC * NQ * 8 + 32 + 15) / 16 * 16;
-  static constexpr int META = 2 * META_MAP + META_D;   // bytes, multiple of 16
-  static constexpr int GP = DD + 1;                      // gather plane pitch (pairs)
-  static constexpr int GATH = EPC * PLN * GP * 16;       // bytes
-  static constexpr int TIMG = EPC * PLN * QQ * 8;        // bytes
-  static constexpr size_t bytes = 2 * (size_t)META + GATH + TIMG + 64;
-};
-
-struct MetaView {
-  const int* map;
-  const int* slot;
-  const double* D;
-};
-
-// issue the bulk copies of group [e0, e0+nel) into metadata buffer `buf`
-template <int P, int NC>
-__device__ __forceinline__ void meta_issue(char* buf, const MassArgs& a, long long e0, int nel,
-                                           unsigned long long* bar) {
-  using M = MassTMA<P, NC>;
-  auto span = [&](const char* src, long long nbytes, char* dst, unsigned& tx) {
-    const unsigned long long lo = (unsigned long long)src & ~15ull;
-    const unsigned long long hi = ((unsigned long long)src + nbytes + 15) & ~15ull;
-    bulk_g2s(dst, (const void*)lo, (unsigned)(hi - lo), bar);
-    tx += (unsigned)(hi - lo);
-  };
-  unsigned tx = 0;
-  // expect_tx must precede the copies' completion; compute sizes first
-  const char* s0 = (const char*)(a.emapf + e0 * M::NL);
-  const char* s1 = (const char*)(a.slot + e0 * M::NL);
-  const char* s2 = (const char*)(a.D + e0 * M::NQ);
-  const long long n0 = (long long)nel * M::NL * 4, n2 = (long long)nel * M::NQ * 8;
-  auto sz = [](const char* src, long long nbytes) {
-    const unsigned long long lo = (unsigned long long)src & ~15ull;
-    const unsigned long long hi = ((unsigned long long)src + nbytes + 15) & ~15ull;
-    return (unsigned)(hi - lo);
-  };
-  mbar_expect_tx(bar, sz(s0, n0) + sz(s1, n0) + sz(s2, n2));
-  span(s0, n0, buf, tx);
-  span(s1, n0, buf + M::META_MAP, tx);
-  span(s2, n2, buf + 2 * M::META_MAP, tx);
-}
-
-template <int P, int NC>
-__device__ __forceinline__ MetaView meta_view(char* buf, const MassArgs& a, long long e0) {
-  using M = MassTMA<P, NC>;
-  MetaView v;
-  v.map = (const int*)(buf + (((unsigned long long)(a.emapf + e0 * M::NL)) & 15ull));
-  v.slot = (const int*)(buf + M::META_MAP + (((unsigned long long)(a.slot + e0 * M::NL)) & 15ull));
-  v.D = (const double*)(buf + 2 * M::META_MAP + (((unsigned long long)(a.D + e0 * M::NQ)) & 15ull));
-  return v;
-}
-
-// cp.async gathers of the (z, p) pairs of group e0 (items (el, c, l), l fastest)
-template <int P, int NC>
-__device__ __forceinline__ void gather_issue(double2* gath, const MetaView& mv, const double* zp, int nel) {
-  using M = MassTMA<P, NC>;
-  constexpr int NL = M::NL, D1 = M::D1, DD = M::DD, GP = M::GP;
-  for (int it = threadIdx.x; it < nel * NC * NL; it += 128) {
-    const int el = it / (NC * NL), q = it - el * (NC * NL), c = q / NL, l = q - c * NL;
-    const long long n = emf_node(mv.map[el * NL + l]);
-    const int dz = l / DD, k = l - dz * DD;
-    cp_async16(gath + (el * M::PLN + c * D1 + dz) * GP + k, zp + (n * NC + c) * 2);
-  }
-  cp_async_commit();
-}
-
-template <int P, int NC>
-__global__ void __launch_bounds__(128, 2) k_mass_tma(MassArgs a) {
-  using M = MassTMA<P, NC>;
-  constexpr int D1 = P + 1, Q = P + 2, NL = M::NL, NQ = M::NQ, QQ = Q * Q, DD = D1 * D1;
-  constexpr int PLN = M::PLN, EPC = M::EPC, GP = M::GP;
-  const double* cB = c_B[P - 1];
-  extern __shared__ __align__(16) char smem_raw[];
-  char* metab[2] = {smem_raw, smem_raw + M::META};
-  double2* gath = (double2*)(smem_raw + 2 * M::META);
-  double* sT = (double*)(smem_raw + 2 * M::META + M::GATH);
-  __shared__ __align__(8) unsigned long long bars[2];
-  __shared__ double red[32];
-  __shared__ int sflag;
-  if (!a.cg->active) return;
-  const int t = threadIdx.x;
-  const double beta = a.cg->beta;
-  const double* po = (a.cg->it & 1) ? a.pbuf0 : a.pbuf1;
-  double acc = 0.0;
-  const long long stride = (long long)gridDim.x * EPC;
-  const long long first = (long long)blockIdx.x * EPC;
-  auto nel_of = [&](long long e0) { return (int)((a.ne - e0) < EPC ? (a.ne - e0) : EPC); };
-  if (t == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (first < a.ne) {
-    if (t == 0) {
-      meta_issue<P, NC>(metab[0], a, first, nel_of(first), &bars[0]);
-      if (first + stride < a.ne) meta_issue<P, NC>(metab[1], a, first + stride, nel_of(first + stride), &bars[1]);
-    }
-    mbar_wait(&bars[0], 0);
-    gather_issue<P, NC>(gath, meta_view<P, NC>(metab[0], a, first), po, nel_of(first));
-  }
-  int i = 0;
-  for (long long e0 = first; e0 < a.ne; e0 += stride, ++i) {
-    const int b = i & 1;
-    const int nel = nel_of(e0);
-    const MetaView mv = meta_view<P, NC>(metab[b], a, e0);
-    cp_async_wait_all();
-    __syncthreads();
-    // ---- phase 1 (planes): direction update, wall mask, x and y in registers -> sT
-    const int pe = t / PLN, pr = t - pe * PLN, pc = pr / D1, pz = pr - pc * D1;
-    if (pe < nel) {
-      const double2* g = gath + (pe * PLN + pr) * GP;
-      const int* mw = mv.map + pe * NL + pz * DD;
-      double u[DD];
-#pragma unroll
-      for (int k = 0; k < DD; ++k) {
-        const double2 q = g[k];
-        const double p = __dadd_rn(q.x, __dmul_rn(beta, q.y));
-        const int w = mw[k];
-        const bool m = emf_mask(w, pc);
-        if (m && emf_own(w)) acc = fma(p, p, acc);
-        u[k] = m ? 0.0 : p;
-      }
-      double v[D1][Q];
-#pragma unroll
-      for (int dy = 0; dy < D1; ++dy)
-#pragma unroll
-        for (int qx = 0; qx < Q; ++qx) {
-          double s = 0.0;
-#pragma unroll
-          for (int dx = 0; dx < D1; ++dx) s = fma(cB[qx * D1 + dx], u[dy * D1 + dx], s);
-          v[dy][qx] = s;
-        }
-      double* T = sT + (pe * PLN + pr) * QQ;
-#pragma unroll
-      for (int qy = 0; qy < Q; ++qy)
-#pragma unroll
-        for (int qx = 0; qx < Q; ++qx) {
-          double s = 0.0;
-#pragma unroll
-          for (int dy = 0; dy < D1; ++dy) s = fma(cB[qy * D1 + dy], v[dy][qx], s);
-          T[qy * Q + qx] = s;
-        }
-    }
-    __syncthreads();
-    // gath is free: prefetch the next group's pairs (its metadata was requested a group ago)
-    const long long e1 = e0 + stride;
-    if (e1 < a.ne) {
-      mbar_wait(&bars[b ^ 1], ((i + 1) >> 1) & 1);
-      gather_issue<P, NC>(gath, meta_view<P, NC>(metab[b ^ 1], a, e1), po, nel_of(e1));
-    }
-    // ---- phase 2 (columns): z, D, z^T for all components (D from the metadata buffer)
-    for (int it = t; it < nel * QQ; it += 128) {
-      const int ce = it / QQ, l = it - ce * QQ;
-      double Dq[Q];
-#pragma unroll
-      for (int qz = 0; qz < Q; ++qz) Dq[qz] = mv.D[ce * NQ + qz * QQ + l];
-      double* base = sT + ce * PLN * QQ + l;
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        double col[D1];
-#pragma unroll
-        for (int dz = 0; dz < D1; ++dz) col[dz] = base[(c * D1 + dz) * QQ];
-        double w[Q];
-#pragma unroll
-        for (int qz = 0; qz < Q; ++qz) {
-          double s = 0.0;
-#pragma unroll
-          for (int dz = 0; dz < D1; ++dz) s = fma(cB[qz * D1 + dz], col[dz], s);
-          const double du = s * Dq[qz];
-          acc = fma(du, s, acc);
-          w[qz] = du;
-        }
-#pragma unroll
-        for (int dz = 0; dz < D1; ++dz) {
-          double s = 0.0;
-#pragma unroll
-          for (int qz = 0; qz < Q; ++qz) s = fma(cB[qz * D1 + dz], w[qz], s);
-          base[(c * D1 + dz) * QQ] = s;
-        }
-      }
-    }
-    __syncthreads();
-    // ---- phase 3 (planes): y^T, x^T -> node-sorted E-vector (slots from the metadata buffer)
-    if (pe < nel) {
-      const double* T = sT + (pe * PLN + pr) * QQ;
-      double Tq[QQ];
-#pragma unroll
-      for (int k = 0; k < QQ; ++k) Tq[k] = T[k];
-      double v[D1][Q];
-#pragma unroll
-      for (int dy = 0; dy < D1; ++dy)
-#pragma unroll
-        for (int qx = 0; qx < Q; ++qx) {
-          double s = 0.0;
-#pragma unroll
-          for (int qy = 0; qy < Q; ++qy) s = fma(cB[qy * D1 + dy], Tq[qy * Q + qx], s);
-          v[dy][qx] = s;
-        }
-      const int* sl = mv.slot + pe * NL + pz * DD;
-#pragma unroll
-      for (int dy = 0; dy < D1; ++dy)
-#pragma unroll
-        for (int dx = 0; dx < D1; ++dx) {
-          double s = 0.0;
-#pragma unroll
-          for (int qx = 0; qx < Q; ++qx) s = fma(cB[qx * D1 + dx], v[dy][qx], s);
-          a.evec[(long long)sl[dy * D1 + dx] * NC + pc] = s;
-        }
-    }
-    __syncthreads();
-    // metadata buffer b is free: request the group after next into it
-    const long long e2 = e0 + 2 * stride;
-    if (t == 0 && e2 < a.ne) {
-      fence_proxy_async();
-      meta_issue<P, NC>(metab[b], a, e2, nel_of(e2), &bars[b]);
-    }
-  }
-  const double bs = block_sum<128>(acc, red);
-  if (threadIdx.x == 0) a.partials[blockIdx.x] = bs;
-  if (grid_last_block(&a.cg->cnt[0], &sflag)) {
-    const double pAp = reduce_partials<128>(a.partials, gridDim.x, red);
-    if (threadIdx.x == 0) {
-      a.cg->cnt[0] = 0;
-      if (pAp <= 0.0) {
-        a.cg->code = 3;
-        a.cg->active = 0;
-      } else {
-        a.cg->alpha = a.cg->rz / pAp;
-      }
-    }
+    cg_partial(a.partials, &a.cg->nparts_m, block_sum<128>(acc, red));
   }
 }
 
@@ -1164,7 +941,8 @@ struct NodeArgs {
   double* out;          // scatter output
   long long nn;
   CGDev* cg;
-  double* partials;
+  double* partials;     // this launch's per-CTA partials (node launches: r.z)
+  double* pm;           // cg_init: where the mass launches put their p.Ap partials
   double* hist;
   int negate;           // cg_init from evec: rhs = -sum
   double tol;           // cg_init: stop tolerance and iteration cap
@@ -1226,6 +1004,15 @@ __global__ void __launch_bounds__(256) k_cg_init(NodeArgs a, SUM sum) {
       g->cnt[2] = 0;
       g->code = 0;
       g->beta = 0.0;
+      g->alpha = 0.0;
+      g->alpha2[0] = g->alpha2[1] = 0.0;
+      g->rz2[0] = t;
+      g->pend = 0;
+      g->it_m = 1;
+      g->it_n = 1;
+      g->parts_m = a.pm;
+      g->parts_n = a.partials;
+      g->hist = a.hist;
       g->it = 1;
       g->iters = 0;
       g->tol = a.tol;
@@ -1258,13 +1045,17 @@ __global__ void __launch_bounds__(256) k_cg_init(NodeArgs a, SUM sum) {
 template <int NC, class SUM>
 __global__ void __launch_bounds__(256, 4) k_cg_node(NodeArgs a, SUM sum) {
   __shared__ double red[32];
-  __shared__ int sflag;
   CGDev* g = a.cg;
-  if (!g->active) return;
-  const int k = g->it;
-  const double alpha = g->alpha, beta = g->beta;
+  double alpha, alpha_prev;
+  int k;
+  if (!cg_node_begin<256>(g, red, alpha, alpha_prev, k)) return;
+  const double beta = g->beta;
   const double* po = (k & 1) ? a.pbuf0 : a.pbuf1;
   double* pn = (k & 1) ? a.pbuf1 : a.pbuf0;
+  // x is stored every second iteration: at even k, x_k = (x_{k-2} + a_{k-1} p_{k-1}) +
+  // a_k p_k evaluated in registers -- the reference's two roundings, one store
+  // (p_{k-1} is the old pair's second half).  k_cg_finish applies a pending odd step.
+  const bool xk = (k & 1) == 0;
   double rz = 0.0;
   // grid-stride over (node, component), U items per thread per trip so that all
   // their loads are in flight together
@@ -1282,7 +1073,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_node(NodeArgs a, SUM sum) {
         const long long n = j / NC;
         const int c = (int)(j - n * NC);
         zp[u] = __ldcg(reinterpret_cast<const double2*>(po) + j);
-        xj[u] = __ldcg(a.x + j);
+        if (xk) xj[u] = __ldcg(a.x + j);
         rj[u] = __ldcg(a.r + j);
         dj[u] = __ldg(a.invd + j);
         m[u] = a.mask && a.mask[j];
@@ -1295,7 +1086,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_node(NodeArgs a, SUM sum) {
       if (j < N) {
         const double p = __dadd_rn(zp[u].x, __dmul_rn(beta, zp[u].y));
         const double ap = m[u] ? p : s[u];
-        a.x[j] = __dadd_rn(xj[u], __dmul_rn(alpha, p));
+        if (xk) a.x[j] = __dadd_rn(__dadd_rn(xj[u], __dmul_rn(alpha_prev, zp[u].y)), __dmul_rn(alpha, p));
         const double r = __dsub_rn(rj[u], __dmul_rn(alpha, ap));
         a.r[j] = r;
         const double z = __dmul_rn(dj[u], r);
@@ -1304,30 +1095,19 @@ __global__ void __launch_bounds__(256, 4) k_cg_node(NodeArgs a, SUM sum) {
       }
     }
   }
-  const double brz = block_sum<256>(rz, red);
-  if (threadIdx.x == 0) a.partials[blockIdx.x] = brz;
-  if (grid_last_block(&g->cnt[1], &sflag)) {
-    const double rzn = reduce_partials<256>(a.partials, gridDim.x, red);
-    if (threadIdx.x == 0) {
-      g->cnt[1] = 0;
-      const double res = sqrt(fmax(rzn, 0.0));
-      if (a.hist) a.hist[k] = res;
-      g->nres = k + 1;
-      if (res <= g->tol * g->norm0) {
-        g->iters = k;
-        g->active = 0;
-      } else if (k >= g->max_iter) {
-        g->code = 4;
-        g->iters = k;
-        g->active = 0;
-      } else {
-        g->beta = rzn / g->rz;
-        g->rz = rzn;
-        g->it = k + 1;
-      }
-      cg_publish(g);
-    }
-  }
+  cg_partial(a.partials, &g->nparts_n, block_sum<256>(rz, red));
+}
+
+// CG epilogue: apply the x update of a final odd iteration (x_k = x_{k-1} + a_k p_k;
+// p_k is the second half of the last pairs written, alpha still a_k)
+__global__ void __launch_bounds__(256) k_cg_finish(const CGDev* g, const double* pbuf0, const double* pbuf1,
+                                                   double* x, long long n) {
+  const int k = g->pend;
+  if (!k) return;
+  const double* pk = (k & 1) ? pbuf1 : pbuf0;  // pairs written by iteration k
+  const double alpha = g->alpha2[k & 1];
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x)
+    x[j] = __dadd_rn(x[j], __dmul_rn(alpha, __ldcg(pk + 2 * j + 1)));
 }
 
 // ---------------------------------------------------------------------------
