@@ -14,6 +14,7 @@
 #include <cstring>
 #include <string>
 #include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "../../include/b200hydro.h"
@@ -1101,7 +1102,13 @@ static int cg_capture(hx_ctx* ctx, CGLaunch& L) {
   cudaStream_t outer = ctx->stream;
   CK(cudaStreamBeginCaptureToGraph(ctx->gstream2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   ctx->stream = ctx->gstream2;
-  rc = cg_launch_iter(ctx, L);
+  // HX_CG_UNROLL iterations per WHILE body (launches past convergence exit at once)
+  static int unroll = -1;
+  if (unroll < 0) {
+    const char* v = getenv("HX_CG_UNROLL");
+    unroll = v ? std::max(1, atoi(v)) : 4;
+  }
+  for (int u = 0; u < unroll && rc == HX_OK; ++u) rc = cg_launch_iter(ctx, L);
   ctx->stream = outer;
   if (rc) return rc;
   CK(cudaStreamEndCapture(ctx->gstream2, &body));
