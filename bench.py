@@ -41,18 +41,35 @@ UNIT = "Mdof*steps/s"
 K_NAMES = ["rates", "mass_cg", "cg_node", "cg_init", "axpy", "validity", "other"]
 
 
-def algorithmic_bytes(d, p, ne, nn):
-    """Per-launch algorithmic bytes of each kernel class ('Kernels')."""
+def algorithmic_bytes(d, p, ne, nn, layout="brick"):
+    """Per-launch algorithmic bytes of each kernel class.
+
+    `brick`: the structured-brick kernels (index-free gathers, element-major E-vectors);
+    `csr`: the generic kernels (element map, node-sorted E-vector + transpose map)."""
     nl, nq, nt = (p + 1) ** d, (p + 2) ** d, max(p, 1) ** d
     V = d * nn
+    E = 8 * d * ne * nl  # one E-vector of d components
+    if layout == "brick":
+        return {
+            # (z, p_{k-1}) pairs gathered + D_M in; element-major E-vector out
+            "mass_cg": 16 * V + 8 * ne * nq + E,
+            # E-vector + (z, p) + r + 1/diag + mask in; (z, p) + r out; x read+written every 2nd iteration
+            "cg_node": E + 16 * V + 8 * V + 8 * V + V + 16 * V + 8 * V + 8 * V,
+            # x, v gathered + e + qdata0 + M_e^{-1} in; F.1 E-vector + de out
+            "rates": 16 * V + 8 * ne * nt + 8 * ne * nq + 8 * ne * nt * nt + E + 8 * ne * nt,
+            # E-vector + 1/diag + mask in; r, (z, p), x out
+            "cg_init": E + 8 * V + V + 8 * V + 16 * V + 8 * V,
+            "axpy": 3 * 2 * 8 * V + 3 * 8 * ne * nt,
+            "validity": 8 * V,
+        }
     return {
-        # D_M + gathered z, p_{k-1} + element map + owner flags + wall mask + E-vector out
-        "mass_cg": 8 * ne * nq + 16 * V + 4 * ne * nl + ne * nl + V + 8 * d * ne * nl,
-        # E-vector + transpose map + z, p_{k-1}, x, r, 1/diag, mask in; p, x, r, z out
-        "cg_node": 8 * d * ne * nl + 4 * ne * nl + 4 * (nn + 1) + 5 * 8 * V + V + 4 * 8 * V,
-        # x, v gathered + e + qdata0 + element map + M_e^{-1} in; F.1 E-vector + de out
-        "rates": 16 * V + 8 * ne * nt + 8 * ne * nq + 4 * ne * nl + 8 * ne * nt * nt + 8 * d * ne * nl + 8 * ne * nt,
-        "cg_init": 8 * d * ne * nl + 4 * ne * nl + 4 * (nn + 1) + V + 8 * V + 5 * 8 * V,
+        # D_M + gathered z, p_{k-1} + packed element map + node-sorted E-vector out (slot map)
+        "mass_cg": 8 * ne * nq + 16 * V + 4 * ne * nl + 4 * ne * nl + E,
+        # E-vector + transpose map + (z, p), r, 1/diag, mask in; (z, p), r out; x every 2nd iteration
+        "cg_node": E + 4 * (nn + 1) + 16 * V + 8 * V + 8 * V + V + 16 * V + 8 * V + 8 * V,
+        # x, v gathered + e + qdata0 + element map + M_e^{-1} in; F.1 E-vector (slot map) + de out
+        "rates": 16 * V + 8 * ne * nt + 8 * ne * nq + 4 * ne * nl + 8 * ne * nt * nt + 4 * ne * nl + E + 8 * ne * nt,
+        "cg_init": E + 4 * (nn + 1) + 8 * V + V + 8 * V + 16 * V + 8 * V,
         "axpy": 3 * 2 * 8 * V + 3 * 8 * ne * nt,
         "validity": 8 * V + 4 * ne * nl,
     }
@@ -408,7 +425,8 @@ def main():
 
     # ---- roofline of the dominant kernel
     pk, pk_src = peaks()
-    ab = algorithmic_bytes(d, p, mesh.num_elements, mesh.num_nodes)
+    layout = hy._ctx.layout()
+    ab = algorithmic_bytes(d, p, mesh.num_elements, mesh.num_nodes, layout)
     traffic = ncu_traffic()
     kern = {}
     for name, (tot, cnt) in ktimes.items():
@@ -442,6 +460,7 @@ def main():
                        "global_batch": V * world, "seq_len": None,
                        "parallelism": "replicas" if world > 1 else "single",
                        "l2": "flushed (256 MiB write) before every timed step",
+                       "layout": layout,
                        "cg_iterations": cg_iters},
             "e2e": e2e, "gpu_launches": launches, "roofline": roof, "kernels": kern,
             "kernel_pass": {"note": "kernel times from a second pass of the same steps launched without "
