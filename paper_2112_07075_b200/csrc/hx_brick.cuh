@@ -163,11 +163,12 @@ __global__ void __launch_bounds__(128, P >= 4 ? 4 : 5) k_mass_brick(MassBrickArg
   }
   // balanced contiguous element range per CTA, walked in passes of up to EPC elements
   // (all CTAs finish within one pass of each other)
-  const long long ebeg = a.ne * blockIdx.x / gridDim.x, eend = a.ne * (blockIdx.x + 1) / gridDim.x;
-  const int npass = (int)((eend - ebeg + EPC - 1) / EPC);
+  const int ebeg = (int)(a.ne * blockIdx.x / gridDim.x);
+  const int len = (int)(a.ne * (blockIdx.x + 1) / gridDim.x) - ebeg;
+  const int npass = (len + EPC - 1) / EPC;
   for (int ps = 0; ps < npass; ++ps) {
-    const long long e0 = ebeg + (eend - ebeg) * ps / npass;
-    const int nel = (int)(ebeg + (eend - ebeg) * (ps + 1) / npass - e0);
+    const int e0 = ebeg + len * ps / npass;
+    const int nel = ebeg + len * (ps + 1) / npass - e0;
     if (t < nel) {
       const unsigned e = (unsigned)(e0 + t);
       const unsigned ez = a.b.fnxy.div(e);
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(128, P >= 4 ? 4 : 5) k_mass_brick(MassBrickArg
 #pragma unroll
           for (int u = 0; u < BAT; ++u)
             if (e1 + u < nel)
-              q[u] = __ldcg(reinterpret_cast<const double2*>(po) + (long long)sbase[e1 + u] * NC + goff[h]);
+              q[u] = __ldcg(reinterpret_cast<const double2*>(po) + (sbase[e1 + u] * NC + goff[h]));
 #pragma unroll
           for (int u = 0; u < BAT; ++u)
             if (e1 + u < nel) sG[(e1 + u) * GS + soff[h]] = __dadd_rn(q[u].x, __dmul_rn(beta, q[u].y));
