@@ -37,10 +37,13 @@ struct RatesPC {
   static constexpr int XP = 2 * Q + 1;                 // row pitch of the x / y-transposed images
   static constexpr int XFS = XPL * D1 * XP;            // X image, field rows
   static constexpr int XS = XFS + DTT * Q;             // + thermo rows
-  static constexpr int TFS = XPL * 3 * QQ;             // T image, field planes
+  // plane pitch of the T and Z images: >= 3 QQ and = Q (mod 16) so that the lines of
+  // consecutive planes (Q doubles each) fall on consecutive bank pairs
+  static constexpr int PP = 3 * QQ + ((Q - 3 * QQ) % 16 + 16) % 16;
+  static constexpr int TFS = XPL * PP;                 // T image, field planes
   static constexpr int TS = TFS + DT * QQ;             // + thermo planes
   static constexpr int WS = 10 * NQ;                   // W image (aliases G+X)
-  static constexpr int ZS = 9 * D1 * QQ + DT * QQ;     // Z image (aliases T)
+  static constexpr int ZS = 3 * D1 * PP + DT * QQ;     // Z image (aliases T)
   static constexpr int YFS = 3 * D1 * D1 * XP;         // Y image (aliases X)
   static constexpr int YS = YFS + DTT * Q;
   static constexpr int OS = 3 * NL + NT;               // staging (aliases T)
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
   using R = RatesPC<P>;
   constexpr int D1 = R::D1, Q = R::Q, DT = R::DT, DD = R::DD, QQ = R::QQ, NL = R::NL, NQ = R::NQ;
   constexpr int NTH = R::NT, DTT = R::DTT, EPC = R::EPC, GP = R::GP, EP = R::EP;
-  constexpr int XPL = R::XPL, PER = R::PER, XP = R::XP, XFS = R::XFS, TFS = R::TFS, YFS = R::YFS;
+  constexpr int XPL = R::XPL, PER = R::PER, XP = R::XP, XFS = R::XFS, TFS = R::TFS, YFS = R::YFS, PP = R::PP;
   constexpr int FS = R::FS, XR = R::XR;
   constexpr int NT = R::THREADS;
   constexpr int NF = MODE == 0 ? 6 : 3;  // fields gathered / contracted
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
             vb[dy] = X[(pl * D1 + dy) * XP + qx];
             vg[dy] = X[(pl * D1 + dy) * XP + Q + qx];
           }
-          double* o = T + pl * 3 * QQ + qx;
+          double* o = T + pl * PP + qx;
 #pragma unroll
           for (int qy = 0; qy < Q; ++qy) {
             double bb = 0.0, gb = 0.0, bg = 0.0;
@@ -343,7 +346,7 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
         double d0 = 0.0, d1 = 0.0, d2 = 0.0, iv = 0.0;
 #pragma unroll
         for (int dz = 0; dz < D1; ++dz) {
-          const double* tt = T + (f * D1 + dz) * 3 * QQ + col;
+          const double* tt = T + (f * D1 + dz) * PP + col;
           const double bb = tt[0], gb = tt[QQ], bg = tt[2 * QQ];
           d0 = fma(bz[dz], bg, d0);  // d/dxi_x: B_z B_y G_x
           d1 = fma(bz[dz], gb, d1);  // d/dxi_y: B_z G_y B_x
@@ -430,9 +433,9 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
           }
 #pragma unroll
           for (int dz = 0; dz < D1; ++dz) {
-            Z[((c * 3 + 0) * D1 + dz) * QQ + col] = z0[dz];
-            Z[((c * 3 + 1) * D1 + dz) * QQ + col] = z1[dz];
-            Z[((c * 3 + 2) * D1 + dz) * QQ + col] = z2[dz];
+            Z[(c * D1 + dz) * PP + col] = z0[dz];
+            Z[(c * D1 + dz) * PP + QQ + col] = z1[dz];
+            Z[(c * D1 + dz) * PP + 2 * QQ + col] = z2[dz];
           }
         } else {
           double zt[DT];
@@ -445,7 +448,7 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
             for (int dz = 0; dz < DT; ++dz) zt[dz] = fma(cBt[qz * DT + dz], s, zt[dz]);
           }
 #pragma unroll
-          for (int dz = 0; dz < DT; ++dz) Z[9 * D1 * QQ + dz * QQ + col] = zt[dz];
+          for (int dz = 0; dz < DT; ++dz) Z[3 * D1 * PP + dz * QQ + col] = zt[dz];
         }
       }
     }
@@ -463,10 +466,9 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
         double* Y = work + el * PER;  // aliases W (dead)
         if (k < FL) {
           const int pl = k / Q, qx = k - pl * Q;  // pl = c*D1 + dz
-          const int c = pl / D1, dz = pl - c * D1;
-          const double* z0 = Z + ((c * 3 + 0) * D1 + dz) * QQ + qx;
-          const double* z1 = Z + ((c * 3 + 1) * D1 + dz) * QQ + qx;
-          const double* z2 = Z + ((c * 3 + 2) * D1 + dz) * QQ + qx;
+          const double* z0 = Z + pl * PP + qx;
+          const double* z1 = Z + pl * PP + QQ + qx;
+          const double* z2 = Z + pl * PP + 2 * QQ + qx;
           double yg[D1], yb[D1];
 #pragma unroll
           for (int dy = 0; dy < D1; ++dy) {
@@ -490,7 +492,7 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
           }
         } else {
           const int r = k - FL, dz = r / Q, qx = r - dz * Q;
-          const double* z = Z + 9 * D1 * QQ + dz * QQ + qx;
+          const double* z = Z + 3 * D1 * PP + dz * QQ + qx;
           double y[DT];
 #pragma unroll
           for (int dy = 0; dy < DT; ++dy) y[dy] = 0.0;
