@@ -200,6 +200,20 @@ def run_reference(args, rank):
 # B200 arm
 
 
+def problem_setup(args):
+    """(extents, counts, gamma, name) of the benchmark problem (BASELINE.json configs)."""
+    n = args.n
+    if args.problem == "sedov":
+        return (1.0, 1.0, 1.0), (n, n, n), 1.4, f"3D Sedov blast Q{args.p}-Q{args.p - 1}, {n}^3 hex elements per GPU"
+    if args.problem == "tgv":
+        return (1.0, 1.0, 1.0), (n, n, n), 5.0 / 3.0, (f"3D Taylor-Green vortex Q{args.p}-Q{args.p - 1} (inviscid), "
+                                                        f"{n}^3 elements")
+    # triple point [0,7]x[0,3]x[0,1.5]; n = elements along y, aspect 7:3:1.5
+    c = (round(n * 7 / 3), n, max(1, round(n / 2)))
+    return (7.0, 3.0, 1.5), c, 1.5, (f"3D triple point Q{args.p}-Q{args.p - 1} (single gamma), "
+                                      f"{c[0]}x{c[1]}x{c[2]} elements")
+
+
 def run_distributed(args, world, rank, local):
     """N>1: one brick of n^3 elements per rank (weak scaling) of a global Sedov mesh;
     element work on the device, shared-node halo sums and CG/CFL scalars over NCCL
@@ -289,6 +303,7 @@ def main():
     ap.add_argument("--n", type=int, default=23, help="elements per direction per GPU")
     ap.add_argument("--p", type=int, default=3, help="kinematic order (Q_p - Q_{p-1})")
     ap.add_argument("--cfl", type=float, default=0.05)
+    ap.add_argument("--problem", default="sedov", choices=["sedov", "tgv", "triple"])
     ap.add_argument("--cpu-n", type=int, default=12, help="CPU sample: elements per direction")
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
@@ -323,10 +338,20 @@ def main():
     from paper_2112_07075_b200.tensor_basis import gauss_legendre
 
     d, p, n = 3, args.p, args.n
-    mesh = cartesian_mesh(d, (1.0,) * d, (n,) * d, p)
-    hy = LagrangeHydro(mesh, gauss_legendre(p + 2), MaterialModel(1.4), ViscosityModel(0.5, 2.0),
-                       bc_mask=box_velocity_bc(mesh))
-    st0 = hy.initial_state(*problems.sedov(d, (1.0,) * d, (n,) * d))
+    extents, counts, gamma, pname = problem_setup(args)
+    mesh = cartesian_mesh(d, extents, counts, p)
+    # Taylor-Green runs inviscid (as the reference's own TG test, test_hydro.py:279-297): the
+    # flow is divergence-free, so the viscosity switch would act on rounding noise and the
+    # reference itself collapses dt (checked with the oracle)
+    visc = ViscosityModel(0.0, 0.0) if args.problem == "tgv" else ViscosityModel(0.5, 2.0)
+    hy = LagrangeHydro(mesh, gauss_legendre(p + 2), MaterialModel(gamma), visc, bc_mask=box_velocity_bc(mesh))
+    if args.problem == "sedov":
+        fns = problems.sedov(d, extents, counts)
+    elif args.problem == "tgv":
+        fns = problems.taylor_green(d, gamma)
+    else:
+        fns = problems.triple_point(d, gamma)
+    st0 = hy.initial_state(*fns)
     ctl = StepControls(cfl=args.cfl, dt_max=1.0, t_final=1e9)
     V = d * mesh.num_nodes
     lib, h = hy._ctx.lib, hy._ctx.h
@@ -455,8 +480,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"3D Sedov blast Q{p}-Q{p - 1}, {n}^3 hex elements per GPU, "
-                                   f"{V} velocity dofs per GPU, CFL {args.cfl}",
+            "config": {"workload": f"{pname}, {V} velocity dofs per GPU, CFL {args.cfl}",
                        "global_batch": V * world, "seq_len": None,
                        "parallelism": "replicas" if world > 1 else "single",
                        "l2": "flushed (256 MiB write) before every timed step",
