@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libb200hydro.so")
+# HX_LIB: alternative in-tree build of the same library (A/B measurements of compile-time variants)
+LIB_PATH = os.environ.get("HX_LIB") or os.path.join(HERE, "libb200hydro.so")
 
 HX_OK, HX_EINVAL, HX_EINVERTED, HX_ECG_BREAKDOWN, HX_ECG_MAXITER, HX_ECUDA, HX_ENCCL, HX_EUNDERFLOW = range(8)
 HX_SPACE_H1, HX_SPACE_L2 = 0, 1

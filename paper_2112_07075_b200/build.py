@@ -34,7 +34,8 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = True) -> str:
     if not force and up_to_date():
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", SRC]
+    extra = os.environ.get("HX_NVCC_EXTRA", "").split()
+    cmd = [NVCC, *FLAGS, *extra, "-o", OUT + ".tmp", SRC]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
