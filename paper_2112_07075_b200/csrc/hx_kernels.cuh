@@ -373,10 +373,40 @@ template <int NT>
 __device__ __forceinline__ bool cg_mass_begin(CGDev* g, double* red, double& beta, int& k) {
   if (!g->active) return false;
   k = g->it_m;
-  if (k == 1) {
+  if (k == 1) {  // finish k_cg_init's reduction: rz_0, any(b != 0)
+    __shared__ double b2[2];
+    double t = 0.0, nz = 0.0;
+    for (int i = threadIdx.x; i < g->nparts_n; i += NT) {
+      t += __ldcg(g->parts_n + 2 * i);
+      nz += __ldcg(g->parts_n + 2 * i + 1);
+    }
+    t = block_sum<NT>(t, red);
+    nz = block_sum<NT>(nz, red);
+    if (threadIdx.x == 0) {
+      b2[0] = t;
+      b2[1] = nz;
+    }
+    __syncthreads();
+    t = b2[0];
+    nz = b2[1];
+    const bool none = nz == 0.0, maxed = !none && g->max_iter <= 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (!none) {
+        g->norm0 = sqrt(t);
+        if (g->hist) g->hist[0] = g->norm0;
+      }
+      g->nres = none ? 0 : 1;
+      if (none || maxed) {
+        if (maxed) g->code = 4;
+        g->active = 0;
+        cg_publish(g);
+      } else {
+        g->rz = t;
+        g->rz2[0] = t;
+      }
+    }
     beta = 0.0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) g->it_n = 1;
-    return true;
+    return !(none || maxed);
   }
   const double rzk = reduce_bcast<NT>(g->parts_n, g->nparts_n, red);
   const double res = sqrt(fmax(rzk, 0.0));
@@ -962,79 +992,73 @@ __global__ void __launch_bounds__(256) k_scatter(NodeArgs a) {
   for (int c = 0; c < NC; ++c) a.out[n * NC + c] = s[c];
 }
 
-// CG start (cg_solve operators.py:340-350): r = b, z = D^{-1} r, x = 0, p_0 = 0,
-// rz = r.z, norm0 = sqrt(rz); b == 0 everywhere -> 0 iterations.
-// b is rhs, or -(G^T evec) masked (rhs_v = -F.1, hydro.py:351, 320).  Persistent
-// grid-stride over (node, component).
+// CG start (cg_solve operators.py:340-350): r = b, z = D^{-1} r, x = 0, p_0 = 0, and the
+// per-CTA partials of r.z and of the nonzero count of b; M(1) finishes the reduction
+// (norm0, the b == 0 and max_iter tests).  b is rhs, or -(G^T evec) masked
+// (rhs_v = -F.1, hydro.py:351, 320).  Persistent grid-stride over (node, component),
+// two items in flight per thread.
 template <int NC, class SUM>
-__global__ void __launch_bounds__(256) k_cg_init(NodeArgs a, SUM sum) {
+__global__ void __launch_bounds__(256, 4) k_cg_init(NodeArgs a, SUM sum) {
   __shared__ double red[32];
-  __shared__ int sflag;
   double rz = 0.0, nz = 0.0;
   const long long N = a.nn * NC;
-  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += (long long)gridDim.x * blockDim.x) {
-    const long long n = j / NC;
-    const int c = (int)(j - n * NC);
-    const double s = a.rhs ? a.rhs[j] : sum(n, c);
-    double b = a.negate ? -s : s;
-    if (a.mask && a.mask[j]) b = 0.0;
-    const double z = a.invd[j] * b;
-    a.r[j] = b;
-    reinterpret_cast<double2*>(a.pbuf0)[j] = make_double2(z, 0.0);  // (z_0, p_0 = 0)
-    a.x[j] = 0.0;
-    rz = fma(b, z, rz);
-    if (b != 0.0 || b != b) nz += 1.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  constexpr int U = 2;
+  for (long long j0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; j0 < N; j0 += U * stride) {
+    double s[U], d[U];
+    bool m[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long j = j0 + u * stride;
+      if (j < N) {
+        const long long n = j / NC;
+        const int c = (int)(j - n * NC);
+        s[u] = a.rhs ? a.rhs[j] : sum(n, c);
+        d[u] = a.invd[j];
+        m[u] = a.mask && a.mask[j];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long j = j0 + u * stride;
+      if (j < N) {
+        double b = a.negate ? -s[u] : s[u];
+        if (m[u]) b = 0.0;
+        const double z = d[u] * b;
+        a.r[j] = b;
+        reinterpret_cast<double2*>(a.pbuf0)[j] = make_double2(z, 0.0);  // (z_0, p_0 = 0)
+        a.x[j] = 0.0;
+        rz = fma(b, z, rz);
+        if (b != 0.0 || b != b) nz += 1.0;
+      }
+    }
   }
   const double brz = block_sum<256>(rz, red);
   const double bnz = block_sum<256>(nz, red);
   if (threadIdx.x == 0) {
     a.partials[2 * blockIdx.x] = brz;
     a.partials[2 * blockIdx.x + 1] = bnz;
-  }
-  if (grid_last_block(&a.cg->cnt[2], &sflag)) {
-    double t = 0.0, anyb = 0.0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += 256) {
-      t += __ldcg(a.partials + 2 * i);
-      anyb += __ldcg(a.partials + 2 * i + 1);
-    }
-    t = block_sum<256>(t, red);
-    anyb = block_sum<256>(anyb, red);
-    if (threadIdx.x == 0) {
+    if (blockIdx.x == 0) {
       CGDev* g = a.cg;
-      g->cnt[2] = 0;
       g->code = 0;
       g->beta = 0.0;
       g->alpha = 0.0;
       g->alpha2[0] = g->alpha2[1] = 0.0;
-      g->rz2[0] = t;
       g->pend = 0;
       g->it_m = 1;
       g->it_n = 1;
+      g->nparts_n = (int)gridDim.x;  // M(1) reads the (r.z, nonzero) pairs from here
       g->parts_m = a.pm;
       g->parts_n = a.partials;
       g->hist = a.hist;
       g->it = 1;
       g->iters = 0;
+      g->nres = 0;
       g->tol = a.tol;
       g->max_iter = a.max_iter;
       g->cond = a.cond;
       g->use_cond = a.use_cond;
-      if (anyb == 0.0 || a.max_iter <= 0) {
-        g->active = 0;
-        g->nres = anyb == 0.0 ? 0 : 1;
-        if (anyb != 0.0) {
-          g->norm0 = sqrt(t);
-          if (a.hist) a.hist[0] = g->norm0;
-          g->code = 4;
-        }
-      } else {
-        g->rz = t;
-        g->norm0 = sqrt(t);
-        if (a.hist) a.hist[0] = g->norm0;
-        g->nres = 1;
-        g->active = 1;
-      }
-      cg_publish(g);
+      g->active = 1;
     }
   }
 }
@@ -1129,14 +1153,32 @@ struct AxpyArgs {
   long long nte;       // NE*nt
 };
 
+// y = a + h*b on pairs of entries (16-byte accesses when every array is 16-byte aligned)
+__device__ __forceinline__ void axpy2(const double* a, const double* b, double* y, double h, long long i, long long n,
+                                      bool vec) {
+  if (vec && i + 1 < n) {
+    const double2 p = *reinterpret_cast<const double2*>(a + i);
+    const double2 q = *reinterpret_cast<const double2*>(b + i);
+    *reinterpret_cast<double2*>(y + i) = make_double2(__dadd_rn(p.x, __dmul_rn(h, q.x)),
+                                                      __dadd_rn(p.y, __dmul_rn(h, q.y)));
+  } else {
+    for (long long j = i; j < n && j < i + 2; ++j) y[j] = __dadd_rn(a[j], __dmul_rn(h, b[j]));
+  }
+}
+
 __global__ void __launch_bounds__(256) k_axpy_state(AxpyArgs a) {
   const double h = a.scale == 1.0 ? *a.dtp : (*a.dtp / 2.0);
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long i = 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  const bool vec = ((reinterpret_cast<unsigned long long>(a.x) | reinterpret_cast<unsigned long long>(a.v) |
+                     reinterpret_cast<unsigned long long>(a.e) | reinterpret_cast<unsigned long long>(a.dxs) |
+                     reinterpret_cast<unsigned long long>(a.dv) | reinterpret_cast<unsigned long long>(a.de) |
+                     reinterpret_cast<unsigned long long>(a.xo) | reinterpret_cast<unsigned long long>(a.vo) |
+                     reinterpret_cast<unsigned long long>(a.eo)) & 15ull) == 0;
   if (i < a.nv) {
-    a.xo[i] = __dadd_rn(a.x[i], __dmul_rn(h, a.dxs[i]));
-    a.vo[i] = __dadd_rn(a.v[i], __dmul_rn(h, a.dv[i]));
+    axpy2(a.x, a.dxs, a.xo, h, i, a.nv, vec);
+    axpy2(a.v, a.dv, a.vo, h, i, a.nv, vec);
   }
-  if (i < a.nte) a.eo[i] = __dadd_rn(a.e[i], __dmul_rn(h, a.de[i]));
+  if (i < a.nte) axpy2(a.e, a.de, a.eo, h, i, a.nte, vec);
 }
 
 // dt = min(cfl*ratio, dt_max, t_final - t) / 2^retry  (timestep_estimate hydro.py:364-373)
