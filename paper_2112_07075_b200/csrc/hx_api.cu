@@ -421,6 +421,16 @@ template <int DIM, int P>
 struct LaunchMinv {
   static int run(hx_ctx* ctx, double* minv_ref) {
     using D = Disc<DIM, P>;
+    if constexpr (DIM == 3 && P <= 3) {
+      constexpr int Q = P + 2, DT = P;
+      const size_t wb = sizeof(double) * 8 * (D::NQ + DT * DT * Q * Q + DT * DT * DT * DT * Q);
+      auto kw = k_minv_warp<P>;
+      CK(smem_attr(kw, wb));
+      kw<<<std::min<unsigned>(gblocks(ctx->ne, 8), 148 * 8), 256, wb, ctx->stream>>>(ctx->Dm, ctx->ne, ctx->minv,
+                                                                                     minv_ref);
+      CKL();
+      return HX_OK;
+    }
     const size_t bytes = sizeof(double) * (D::NT * 2 * D::NT + D::NQ * D::NT);
     auto k = k_minv<DIM, P>;
     CK(smem_attr(k, bytes));

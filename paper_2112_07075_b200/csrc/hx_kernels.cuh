@@ -578,6 +578,7 @@ __constant__ double c_B[4][30];
 // between stages.  CG fusion as in k_mass (direction update, wall mask, p.Ap).
 
 __constant__ double c_G[4][30];
+__constant__ double c_Bt[4][30];  // thermodynamic basis (Q x DT) per order, like c_B
 
 template <int P, int TAB>
 __device__ __forceinline__ double cmat(int i) {
@@ -1567,6 +1568,90 @@ __global__ void __launch_bounds__(128) k_mass_diag(const double* D, const double
 
 // per-element thermodynamic mass blocks M_e = Bth^T diag(D) Bth and their inverse
 // (hydro.py:229-232): Gauss-Jordan with partial pivoting, one CTA per element.
+// Thermodynamic mass inverses, one warp per element (3D, nt <= 32): M_e = B_t^T diag(D) B_t
+// (hydro.py:229-231) assembled by sum factorisation (x, y, z pairs of basis rows), then
+// inverted in place by Gauss-Jordan with lane j holding column j in registers (M_e is SPD:
+// no pivoting; the reference's LAPACK getri differs at rounding level only).
+template <int P>
+__global__ void __launch_bounds__(256) k_minv_warp(const double* Dm /*(NE,nq)*/, long long ne, double* minv,
+                                                   double* minv_ref) {
+  constexpr int Q = P + 2, DT = P, N = DT * DT * DT, NQ = Q * Q * Q, D2 = DT * DT;
+  static_assert(N <= 32, "one column per lane");
+  constexpr int WPB = 8;
+  constexpr int AX = D2 * Q * Q;        // A_x[(ix,jx)][qy][qz]
+  constexpr int AXY = D2 * D2 * Q;      // A_xy[(ix,jx)][(iy,jy)][qz]
+  constexpr int PER = NQ + AX + AXY;
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* sD = smem + warp * PER;
+  double* sAx = sD + NQ;
+  double* sAxy = sAx + AX;
+  const double* bt = c_Bt[P - 1];  // (Q, DT)
+  for (long long e = (long long)blockIdx.x * WPB + warp; e < ne; e += (long long)gridDim.x * WPB) {
+    for (int q = lane; q < NQ; q += 32) sD[q] = __ldg(Dm + e * NQ + q);
+    __syncwarp();
+    // x: A_x[ix,jx][qy,qz] = sum_qx Bt[qx][ix] Bt[qx][jx] D[qz][qy][qx]
+    for (int o = lane; o < AX; o += 32) {
+      const int ij = o / (Q * Q), r = o - ij * (Q * Q);  // r = qz*Q + qy
+      const int ix = ij / DT, jx = ij - ix * DT;
+      double s = 0.0;
+#pragma unroll
+      for (int qx = 0; qx < Q; ++qx) s = fma(bt[qx * DT + ix] * bt[qx * DT + jx], sD[r * Q + qx], s);
+      sAx[o] = s;
+    }
+    __syncwarp();
+    // y: A_xy[ij_x][iy,jy][qz] = sum_qy Bt[qy][iy] Bt[qy][jy] A_x[ij_x][qz][qy]
+    for (int o = lane; o < AXY; o += 32) {
+      const int ijx = o / (D2 * Q), r = o - ijx * (D2 * Q);
+      const int ijy = r / Q, qz = r - ijy * Q;
+      const int iy = ijy / DT, jy = ijy - iy * DT;
+      double s = 0.0;
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy)
+        s = fma(bt[qy * DT + iy] * bt[qy * DT + jy], sAx[ijx * Q * Q + qz * Q + qy], s);
+      sAxy[o] = s;
+    }
+    __syncwarp();
+    // z: column j = (jx, jy, jz) of M_e in registers of lane j (row i = (ix, iy, iz), x fastest)
+    double col[N];
+    const int j = lane < N ? lane : 0;
+    const int jx = j % DT, jy = (j / DT) % DT, jz = j / D2;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const int ix = i % DT, iy = (i / DT) % DT, iz = i / D2;
+      const double* a = sAxy + ((ix * DT + jx) * D2 + (iy * DT + jy)) * Q;
+      double s = 0.0;
+#pragma unroll
+      for (int qz = 0; qz < Q; ++qz) s = fma(bt[qz * DT + iz] * bt[qz * DT + jz], a[qz], s);
+      col[i] = s;
+    }
+    __syncwarp();
+    // in-place Gauss-Jordan: after step k, column k holds -A[i][k]/p (i != k) and 1/p
+#pragma unroll
+    for (int kk = 0; kk < N; ++kk) {
+      const double p = __shfl_sync(0xffffffffu, col[kk], kk);
+      const double rp = 1.0 / p;
+      const double akj = col[kk] * rp;
+      const bool own = lane == kk;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double aik = __shfl_sync(0xffffffffu, col[i], kk);
+        if (i == kk) continue;
+        col[i] = own ? -aik * rp : fma(-aik, akj, col[i]);
+      }
+      col[kk] = own ? rp : akj;
+    }
+    if (lane < N) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        minv[(e * N + i) * N + lane] = col[i];
+        if (minv_ref) minv_ref[(e * N + i) * N + lane] = col[i];
+      }
+    }
+    __syncwarp();
+  }
+}
+
 template <int DIM, int P>
 __global__ void __launch_bounds__(128) k_minv(const double* Dm /*(NE,nq)*/, const double* Bt, long long ne,
                                              double* minv, double* minv_ref) {

@@ -23,8 +23,6 @@
 
 namespace hx {
 
-__constant__ double c_Bt[4][30];  // thermodynamic basis (Q x DT) per order, like c_B
-
 template <int P>
 struct RatesPC {
   static constexpr int D1 = P + 1, Q = P + 2, DT = P, DD = D1 * D1, QQ = Q * Q, NL = D1 * DD, NQ = Q * QQ;
