@@ -45,6 +45,8 @@ struct hx_ctx {
   double* evec = nullptr;     // (NE, nl, d)
   double* evec2 = nullptr;    // second E buffer (API scatter staging)
   double *r = nullptr, *z = nullptr, *p0 = nullptr, *p1 = nullptr;
+  char* arena = nullptr;      // CG working set: pairs, r, 1/diag, mask, x (dv0, dv1), E-vector, D_M
+  size_t arena_bytes = 0;
   double* partials = nullptr; // reduction partials: two regions of preg doubles
   long long preg = 0;
   double* hist = nullptr;     // CG residual history
@@ -632,12 +634,32 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   ok &= dalloc(&ctx->idx, (size_t)ne * nl) == cudaSuccess;
   ok &= dalloc(&ctx->own, (size_t)ne * nl) == cudaSuccess;
   ok &= dalloc(&ctx->slot, (size_t)ne * nl + 8) == cudaSuccess;
-  ok &= dalloc(&ctx->evec, (size_t)ne * nl * dd) == cudaSuccess;
+  {
+    // CG working set in one arena (L2 persisting access window over it, see l2_window)
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t sizes[] = {al(16 * nv), al(16 * nv), al(8 * nv), al(8 * nv), al(nv), al(8 * nv), al(8 * nv),
+                            al(8 * (size_t)ne * nl * dd), al(8 * ((size_t)ne * nq + 8))};
+    size_t tot = 0;
+    for (size_t s : sizes) tot += s;
+    char* base = nullptr;
+    ok &= cudaMalloc(&base, tot) == cudaSuccess;
+    ctx->arena = base;
+    ctx->arena_bytes = tot;
+    if (base) {
+      char* q = base;
+      ctx->p0 = (double*)q; q += sizes[0];
+      ctx->p1 = (double*)q; q += sizes[1];
+      ctx->r = (double*)q; q += sizes[2];
+      ctx->invd = (double*)q; q += sizes[3];
+      ctx->mask = (uint8_t*)q; q += sizes[4];
+      ctx->dv0 = (double*)q; q += sizes[5];
+      ctx->dv1 = (double*)q; q += sizes[6];
+      ctx->evec = (double*)q; q += sizes[7];
+      ctx->Dm = (double*)q;
+    }
+  }
   ok &= dalloc(&ctx->evec2, (size_t)ne * std::max(nl * dd, nq)) == cudaSuccess;
-  ok &= dalloc(&ctx->r, nv) == cudaSuccess;
   ok &= dalloc(&ctx->z, nv) == cudaSuccess;
-  ok &= dalloc(&ctx->p0, 2 * nv) == cudaSuccess;  // interleaved (z, p) pairs
-  ok &= dalloc(&ctx->p1, 2 * nv) == cudaSuccess;
   ok &= dalloc(&ctx->emapf, (size_t)ne * nl + 8) == cudaSuccess;
   ok &= dalloc(&ctx->emapf_api, (size_t)ne * nl + 8) == cudaSuccess;
   ctx->preg = 2 * std::max<long long>(gblocks(3 * nn, 256), gblocks(ne, 1)) + 64;
@@ -650,17 +672,12 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   ok &= dalloc(&ctx->st, 4) == cudaSuccess;
   ok &= dalloc(&ctx->dt, 2) == cudaSuccess;
   ok &= dalloc(&ctx->scal, 16) == cudaSuccess;
-  ok &= dalloc(&ctx->Dm, (size_t)ne * nq + 8) == cudaSuccess;
   ok &= dalloc(&ctx->qd0, (size_t)ne * nq) == cudaSuccess;
   ok &= dalloc(&ctx->minv, (size_t)ne * ctx->nt * ctx->nt) == cudaSuccess;
   ok &= dalloc(&ctx->mdiag, nn) == cudaSuccess;
-  ok &= dalloc(&ctx->invd, nv) == cudaSuccess;
-  ok &= dalloc(&ctx->mask, nv) == cudaSuccess;
   ok &= dalloc(&ctx->xm, nv) == cudaSuccess;
   ok &= dalloc(&ctx->vm, nv) == cudaSuccess;
   ok &= dalloc(&ctx->em, (size_t)ne * ctx->nt) == cudaSuccess;
-  ok &= dalloc(&ctx->dv0, nv) == cudaSuccess;
-  ok &= dalloc(&ctx->dv1, nv) == cudaSuccess;
   ok &= dalloc(&ctx->de0, (size_t)ne * ctx->nt) == cudaSuccess;
   ok &= dalloc(&ctx->de1, (size_t)ne * ctx->nt) == cudaSuccess;
   ok &= cudaMallocHost((void**)&ctx->h_cg, 2 * sizeof(CGDev)) == cudaSuccess;
@@ -714,9 +731,9 @@ extern "C" int hx_destroy(hx_ctx* ctx) {
   if (!ctx) return HX_OK;
   cudaSetDevice(ctx->device);
   void* dev[] = {ctx->B,  ctx->G,    ctx->Bt,   ctx->wnd,  ctx->psi1, ctx->emap, ctx->off,   ctx->idx,
-                 ctx->own, ctx->slot, ctx->emapf, ctx->emapf_api, ctx->evec, ctx->evec2, ctx->r,   ctx->z,    ctx->p0,   ctx->p1,    ctx->partials,
-                 ctx->hist, ctx->cg,  ctx->st,   ctx->dt,   ctx->scal, ctx->Dm,   ctx->qd0,   ctx->minv,
-                 ctx->mdiag, ctx->invd, ctx->mask, ctx->xm, ctx->vm,   ctx->em,   ctx->dv0,   ctx->dv1,
+                 ctx->own, ctx->slot, ctx->emapf, ctx->emapf_api, ctx->arena, ctx->evec2, ctx->z, ctx->partials,
+                 ctx->hist, ctx->cg,  ctx->st,   ctx->dt,   ctx->scal, ctx->qd0,   ctx->minv,
+                 ctx->mdiag, ctx->xm, ctx->vm,   ctx->em,
                  ctx->de0, ctx->de1, ctx->hx_x, ctx->hx_v, ctx->hx_e, ctx->hx_xo, ctx->hx_vo, ctx->hx_eo};
   for (void* p : dev)
     if (p) cudaFree(p);
@@ -1416,6 +1433,31 @@ static int step_impl(hx_ctx* ctx, const hx_params* prm, double t, double dt_fixe
 
 // ---- the same step as ONE CUDA graph (attempt 0; retries fall back to step_impl)
 
+// Mark the CG working set (arena) as L2-persisting on a stream (HX_L2PERSIST=0 disables):
+// the ~21 iterations of a momentum solve re-read it while the rates kernels stream
+// through M_e^{-1} and the point data.  Captured into the step graph's kernel nodes.
+static void l2_window(hx_ctx* ctx, cudaStream_t s) {
+  static int on = -1;
+  if (on < 0) {
+    const char* v = getenv("HX_L2PERSIST");
+    on = (v && v[0] == '0') ? 0 : 1;
+  }
+  if (!on || !ctx->arena) return;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, ctx->device) != cudaSuccess) return;
+  if (prop.persistingL2CacheMaxSize <= 0 || prop.accessPolicyMaxWindowSize <= 0) return;
+  const size_t persist = std::min<size_t>(prop.persistingL2CacheMaxSize, ctx->arena_bytes);
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist);
+  cudaStreamAttrValue v = {};
+  v.accessPolicyWindow.base_ptr = ctx->arena;
+  v.accessPolicyWindow.num_bytes = std::min<size_t>(ctx->arena_bytes, (size_t)prop.accessPolicyMaxWindowSize);
+  v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)persist / (float)v.accessPolicyWindow.num_bytes);
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
+  cudaGetLastError();
+}
+
 static bool same_params(const hx_params& a, const hx_params& b) { return memcmp(&a, &b, sizeof a) == 0; }
 
 static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, const double* x, const double* v,
@@ -1429,6 +1471,8 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
   ctx->stream = ctx->gstream;
   cudaGraph_t graph = nullptr;
   int rc = HX_OK;
+  l2_window(ctx, ctx->gstream);
+  l2_window(ctx, ctx->gstream2);
   auto body = [&]() -> int {
     CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     int r = status_reset(ctx, ctx->st, 3);
