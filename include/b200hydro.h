@@ -49,6 +49,7 @@ enum { HX_SPACE_H1 = 0, HX_SPACE_L2 = 1 };
 typedef struct hx_ctx hx_ctx;
 typedef struct hx_mass hx_mass;
 typedef struct hx_force hx_force;
+typedef struct hx_op hx_op;
 
 /* Mesh + discretisation description (HighOrderMesh fespace.py:63-80,
  * FiniteElementSpace fespace.py:177-208, QuadratureRule1D tensor_basis.py:41-50,
@@ -170,6 +171,20 @@ int hx_force_destroy(hx_force* f);
 int hx_force_apply(hx_force* f, const double* e, double* y);
 /* ForcePA.apply_transpose: v (NN, d) -> y (NE*nt)  (operators.py:282-300) */
 int hx_force_apply_t(hx_force* f, const double* v, double* y);
+
+/* ---- remap-phase PA operators (operators.py:143-236) --------------------
+ * Scalar H1 operators on the same sum-factorised machinery (not on the Lagrange path).
+ * hx_diffusion_create: D[a][c] = sum_b jinv[a][b] jinv[c][b] wdetj (nu)   (DiffusionPA.__init__ :145-149)
+ * hx_convection_create: D[l] = sum_b jinv[l][b] u[b] wdetj               (ConvectionPA.__init__ :194-198)
+ * jinv (d,d,nq,NE), wdetj/nu (nq,NE), u_points (d,nq,NE); D_out (reference layout) may be NULL.
+ * hx_op_apply: y = sum_a G_a^T (sum_b D G_b x) (DiffusionPA.apply :151-168) or
+ *              y = B^T (sum_l D[l] G_l x)       (ConvectionPA.apply :200-214); x, y (NN). */
+int hx_diffusion_create(hx_ctx* ctx, const double* jinv, const double* wdetj, const double* nu, double* D_out,
+                        hx_op** out);
+int hx_convection_create(hx_ctx* ctx, const double* jinv, const double* u_points, const double* wdetj,
+                         double* D_out, hx_op** out);
+int hx_op_apply(hx_op* op, const double* x, double* y);
+int hx_op_destroy(hx_op* op);
 
 /* ---- Lagrange phase (hydro.py:220-405) ------------------------------- */
 

@@ -347,6 +347,46 @@ def force_apply_t(kin_dofmap, DF, Bk, Gk, Bt, v, d):
     return scatter_add(l2_dofmap(nt1**d, ne), e_flat(out, nt1**d), nt1**d * ne)
 
 
+def diffusion_D(jinv, wdetj, nu=None):
+    """D[a,c] = sum_b jinv[a,b] jinv[c,b] wdetj (nu) (DiffusionPA.__init__, operators.py:145-149)."""
+    scal = wdetj if nu is None else wdetj * nu
+    return np.einsum("abqe,cbqe,qe->acqe", jinv, jinv, scal)
+
+
+def diffusion_apply(dofmap, D, B, G, x, d):
+    """y = sum_a G_a^T (sum_b D[a,b] G_b x) (DiffusionPA.apply, operators.py:151-168)."""
+    n1, nq1, nl = B.shape[1], B.shape[0], dofmap.shape[0]
+    ne = dofmap.shape[1]
+    t = e_tensor(gather(dofmap, x), n1, d)
+    Dq = D.reshape((d, d) + (nq1,) * d + (ne,))
+    g = grad(B, G, t, d)
+    comps = []
+    for a in range(d):
+        s = Dq[a, 0] * g[0]
+        for b in range(1, d):
+            s = s + Dq[a, b] * g[b]
+        comps.append(s)
+    return scatter_add(dofmap, e_flat(grad_t(B, G, comps, d), nl), x.shape[0])
+
+
+def convection_D(jinv, u_points, wdetj):
+    """D[l] = sum_b jinv[l,b] u[b] wdetj (ConvectionPA.__init__, operators.py:194-198)."""
+    return np.einsum("lbqe,bqe,qe->lqe", jinv, u_points, wdetj)
+
+
+def convection_apply(dofmap, D, B, G, x, d):
+    """y = B^T (sum_l D[l] G_l x) (ConvectionPA.apply, operators.py:200-214)."""
+    n1, nq1, nl = B.shape[1], B.shape[0], dofmap.shape[0]
+    ne = dofmap.shape[1]
+    t = e_tensor(gather(dofmap, x), n1, d)
+    Dq = D.reshape((d,) + (nq1,) * d + (ne,))
+    g = grad(B, G, t, d)
+    s = Dq[0] * g[0]
+    for l in range(1, d):
+        s = s + Dq[l] * g[l]
+    return scatter_add(dofmap, e_flat(interp_t(B, s, d), nl), x.shape[0])
+
+
 class CGFailure(Exception):
     def __init__(self, msg, residuals):
         super().__init__(msg)

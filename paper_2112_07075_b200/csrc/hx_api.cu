@@ -21,6 +21,7 @@
 #include "hx_kernels.cuh"
 #include "hx_brick.cuh"
 #include "hx_rates.cuh"
+#include "hx_remap.cuh"
 
 using namespace hx;
 
@@ -99,6 +100,12 @@ struct hx_ctx {
 struct hx_mass {
   hx_ctx* ctx;
   double* D;  // (NE, nq)
+};
+
+struct hx_op {
+  hx_ctx* ctx;
+  int kind;   // 0 diffusion, 1 convection
+  double* D;  // (NE, d, d, nq) / (NE, d, nq)
 };
 
 struct hx_force {
@@ -1214,6 +1221,78 @@ extern "C" int hx_force_apply_t(hx_force* f, const double* v, double* y) {
   CK(cudaSetDevice(ctx->device));
   ForceArgs a{v, f->DF, ctx->emap, ctx->slot, tables(ctx), ctx->ne, nullptr, y};
   return dispatch<LaunchForce>(ctx, a, true);
+}
+
+// ---------------------------------------------------------------------------
+// remap-phase operators: DiffusionPA / ConvectionPA (operators.py:143-236)
+
+template <int DIM, int P>
+struct LaunchRemap {
+  static int run(hx_ctx* ctx, const hx_op* op, const double* x) {
+    using SM = RemapSmem<DIM, P>;
+    RemapArgs a{x, op->D, ctx->emap, ctx->slot, ctx->B, ctx->G, ctx->ne, ctx->evec2};
+    if (op->kind == 0) {
+      auto k = k_remap_op<DIM, P, 128, 0>;
+      CK(smem_attr(k, SM::bytes));
+      k<<<(unsigned)ctx->ne, 128, SM::bytes, ctx->stream>>>(a);
+    } else {
+      auto k = k_remap_op<DIM, P, 128, 1>;
+      CK(smem_attr(k, SM::bytes));
+      k<<<(unsigned)ctx->ne, 128, SM::bytes, ctx->stream>>>(a);
+    }
+    CKL();
+    return HX_OK;
+  }
+};
+
+static int remap_create(hx_ctx* ctx, int kind, const double* jinv, const double* wdetj, const double* nu,
+                        const double* u, double* D_out, hx_op** out) {
+  if (!ctx || !jinv || !wdetj || !out || (kind == 1 && !u)) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  const int d = ctx->dim;
+  hx_op* op = new hx_op{ctx, kind, nullptr};
+  const size_t n = (size_t)ctx->ne * (kind == 0 ? d * d : d) * ctx->nq;
+  if (dalloc(&op->D, n) != cudaSuccess) {
+    delete op;
+    return fail(ctx, HX_ECUDA, "alloc");
+  }
+  const long long np = (long long)ctx->nq * ctx->ne;
+  if (kind == 0) {
+    if (d == 2) k_diff_D<2><<<gblocks(np, 256), 256, 0, ctx->stream>>>(jinv, wdetj, nu, ctx->ne, ctx->nq, op->D, D_out);
+    else k_diff_D<3><<<gblocks(np, 256), 256, 0, ctx->stream>>>(jinv, wdetj, nu, ctx->ne, ctx->nq, op->D, D_out);
+  } else {
+    if (d == 2) k_conv_D<2><<<gblocks(np, 256), 256, 0, ctx->stream>>>(jinv, u, wdetj, ctx->ne, ctx->nq, op->D, D_out);
+    else k_conv_D<3><<<gblocks(np, 256), 256, 0, ctx->stream>>>(jinv, u, wdetj, ctx->ne, ctx->nq, op->D, D_out);
+  }
+  CKL();
+  *out = op;
+  return HX_OK;
+}
+
+extern "C" int hx_diffusion_create(hx_ctx* ctx, const double* jinv, const double* wdetj, const double* nu,
+                                   double* D_out, hx_op** out) {
+  return remap_create(ctx, 0, jinv, wdetj, nu, nullptr, D_out, out);
+}
+
+extern "C" int hx_convection_create(hx_ctx* ctx, const double* jinv, const double* u_points, const double* wdetj,
+                                    double* D_out, hx_op** out) {
+  return remap_create(ctx, 1, jinv, wdetj, nullptr, u_points, D_out, out);
+}
+
+extern "C" int hx_op_apply(hx_op* op, const double* x, double* y) {
+  if (!op || !x || !y) return HX_EINVAL;
+  hx_ctx* ctx = op->ctx;
+  CK(cudaSetDevice(ctx->device));
+  int rc = dispatch<LaunchRemap>(ctx, (const hx_op*)op, x);
+  if (rc) return rc;
+  return launch_scatter(ctx, ctx->evec2, 1, y);
+}
+
+extern "C" int hx_op_destroy(hx_op* op) {
+  if (!op) return HX_OK;
+  cudaFree(op->D);
+  delete op;
+  return HX_OK;
 }
 
 // ---------------------------------------------------------------------------

@@ -7,9 +7,10 @@ applies run in libb200hydro.so (sum-factorised sm_100a kernels with the
 deterministic restriction); `cg_solve` on a `MassPA.apply` runs entirely on the
 device with the stop test evaluated there (`hx_mass_cg`).
 
-`DiffusionPA` / `ConvectionPA` and the `.assemble()` full-assembly oracles are
-not part of the Lagrange hot path and are not provided; the
-test suite checks against the CPU oracle in `oracle/` instead.
+`DiffusionPA` / `ConvectionPA` (operators.py:143-236) belong to the remap phase,
+not the Lagrange hot path; they run on the same contraction machinery (SURVEY.md
+section 8f, "next").  The `.assemble()` full-assembly oracles are not provided: the
+test suite checks against the CPU oracle in `oracle/` and the reference's fixtures.
 """
 
 from __future__ import annotations
@@ -24,7 +25,7 @@ from . import _lib
 from ._device import context_for, empty, like, to_dev
 from .kernel_exec import SEQ, ExecPlace
 
-__all__ = ["MassPA", "ForcePA", "cg_solve", "CGError", "ELEMENT_BLOCK"]
+__all__ = ["MassPA", "ForcePA", "DiffusionPA", "ConvectionPA", "cg_solve", "CGError", "ELEMENT_BLOCK"]
 
 ELEMENT_BLOCK = 32  # reference team block (operators.py:39); informational on the device
 
@@ -106,6 +107,69 @@ class MassPA:
 
     def assemble(self):
         raise NotImplementedError("full assembly is a CPU test oracle; see oracle/pa_oracle.py")
+
+
+class _ScalarPA:
+    """Common part of the scalar H1 PA operators of the remap phase (operators.py:143-236)."""
+
+    def _finish(self, space, geom, place, h, Dout, ref_like):
+        self.space, self.geom, self.place = space, geom, place
+        self.basis = space.basis(geom.quad)
+        self.d = space.mesh.dim
+        self.q1d = geom.quad.n
+        self.ne = space.mesh.num_elements
+        self._h = h
+        self._fin = weakref.finalize(self, self._ctx.lib.hx_op_destroy, h)
+        self.D = like(Dout, ref_like)
+        self.stored_values = int(np.prod(tuple(Dout.shape)))
+
+    def _qshape(self):
+        return (self.q1d,) * self.d
+
+    def apply(self, x):
+        if tuple(x.shape) != (self.space.ndof,):
+            raise ValueError(f"vector of shape {tuple(x.shape)} does not match {self.space.ndof} dofs")
+        X = to_dev(x)
+        Y = empty((self.space.ndof,))
+        self._ctx.sync_stream()
+        self._ctx.check(self._ctx.lib.hx_op_apply(self._h, _lib.ptr(X), _lib.ptr(Y)), type(self).__name__)
+        return like(Y, x)
+
+    def assemble(self):
+        raise NotImplementedError("full assembly is a CPU test oracle; see oracle/pa_oracle.py")
+
+
+class DiffusionPA(_ScalarPA):
+    """Stiffness operator; D holds w detJ J^{-1} nu J^{-T} per point (operators.py:143-168)."""
+
+    def __init__(self, space, geom, nu=None, place: ExecPlace = SEQ):
+        self._ctx = context_for(space.mesh, geom.quad)
+        d, nq, ne = space.mesh.dim, geom.quad.n**space.mesh.dim, space.mesh.num_elements
+        Ji, W = to_dev(geom.jinv), to_dev(geom.wdetj)
+        Nu = None if nu is None else to_dev(nu)
+        Dout = empty((d, d, nq, ne))
+        h = C.c_void_p()
+        self._ctx.sync_stream()
+        self._ctx.check(self._ctx.lib.hx_diffusion_create(self._ctx.h, _lib.ptr(Ji), _lib.ptr(W), _lib.ptr(Nu),
+                                                          _lib.ptr(Dout), C.byref(h)), "DiffusionPA")
+        self._finish(space, geom, place, h, Dout, geom.wdetj)
+
+
+class ConvectionPA(_ScalarPA):
+    """(K w)_i = integral phi_i (u . grad w); D holds w detJ J^{-1} u per point (operators.py:188-214)."""
+
+    def __init__(self, space, geom, u_points, place: ExecPlace = SEQ):
+        self._ctx = context_for(space.mesh, geom.quad)
+        d, nq, ne = space.mesh.dim, geom.quad.n**space.mesh.dim, space.mesh.num_elements
+        if tuple(u_points.shape) != (d, nq, ne):
+            raise ValueError(f"u_points must have shape {(d, nq, ne)}")
+        Ji, W, U = to_dev(geom.jinv), to_dev(geom.wdetj), to_dev(u_points)
+        Dout = empty((d, nq, ne))
+        h = C.c_void_p()
+        self._ctx.sync_stream()
+        self._ctx.check(self._ctx.lib.hx_convection_create(self._ctx.h, _lib.ptr(Ji), _lib.ptr(U), _lib.ptr(W),
+                                                           _lib.ptr(Dout), C.byref(h)), "ConvectionPA")
+        self._finish(space, geom, place, h, Dout, geom.wdetj)
 
 
 class ForcePA:

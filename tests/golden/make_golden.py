@@ -12,6 +12,7 @@ Fixtures
   ops_{d}d_p{p}.npz  operator-level results on randomly perturbed meshes
                      (geometry, mass apply/diag, force apply/apply_t, gather,
                      scatter_add, stress_qdata, momentum CG, energy solve, rates)
+  remap_{d}d_p{p}.npz DiffusionPA / ConvectionPA D tables and applies (remap phase)
   run_*.npz          N-step Lagrange runs of the BASELINE configs at parity size,
                      with the noise floor (1e-15 relative perturbation of e0)
 """
@@ -75,6 +76,29 @@ def main():
             out[f"coords_{i}"] = m.coords
             out[f"case_{i}"] = np.array([d, p] + list(counts) + [0] * (3 - len(counts)))
         np.savez_compressed(os.path.join(HERE, "mesh.npz"), **out)
+
+    # ---- remap-phase PA operators (DiffusionPA, ConvectionPA; operators.py:143-236)
+    if args.only in (None, "remap"):
+        for d in (2, 3):
+            for p in (1, 2, 3, 4):
+                counts = (3, 2) if d == 2 else (2, 2, 2)
+                seed = 500 + 10 * d + p
+                mesh = perturbed_mesh(fespace.cartesian_mesh, d, counts, p, seed)
+                quad = tensor_basis.gauss_legendre(p + 2)
+                geom = fespace.compute_geometric_factors(mesh, quad)
+                h1 = fespace.FiniteElementSpace(mesh, "H1")
+                rng = np.random.default_rng(900 + seed)
+                nq, ne = quad.n**d, mesh.num_elements
+                nu = 1.0 + 0.5 * rng.uniform(size=(nq, ne))
+                dif = operators.DiffusionPA(h1, geom, nu=nu)
+                dif1 = operators.DiffusionPA(h1, geom)
+                u = rng.normal(size=(d, nq, ne))
+                con = operators.ConvectionPA(h1, geom, u)
+                x = rng.normal(size=h1.ndof)
+                np.savez_compressed(os.path.join(HERE, f"remap_{d}d_p{p}.npz"), coords=mesh.coords,
+                                    dofmap=mesh.node_dofmap, jinv=geom.jinv, wdetj=geom.wdetj, nu=nu,
+                                    diff_D=dif.D, diff_x=x, diff_y=dif.apply(x), diff1_D=dif1.D,
+                                    diff1_y=dif1.apply(x), conv_u=u, conv_D=con.D, conv_y=con.apply(x))
 
     # ---- operator-level fixtures
     if args.only in (None, "ops"):

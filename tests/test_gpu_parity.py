@@ -198,3 +198,28 @@ def test_nstep_run_matches_reference(name, fused, brick, monkeypatch):
     assert abs(energies[-1] - float(z["energies"][-1])) <= tol * abs(float(z["energies"][-1]))
     assert st.t == pytest.approx(float(z["t"]), rel=1e-12)
     assert hy.clamp_warnings == int(z["clamps"])
+
+
+@pytest.mark.parametrize("d,p", CASES)
+def test_remap_operators(d, p):
+    """DiffusionPA / ConvectionPA (operators.py:143-236) vs the reference's fixtures."""
+    from paper_2112_07075_b200.fespace import FiniteElementSpace, compute_geometric_factors
+    from paper_2112_07075_b200.operators import ConvectionPA, DiffusionPA
+    from paper_2112_07075_b200.tensor_basis import gauss_legendre
+
+    g = golden(f"remap_{d}d_p{p}")
+    mesh = _mesh_from(g, d, p)
+    geom = compute_geometric_factors(mesh, gauss_legendre(p + 2))
+    h1 = FiniteElementSpace(mesh, "H1")
+    dif = DiffusionPA(h1, geom, nu=g["nu"])
+    assert rel(dif.D, g["diff_D"]) < 1e-14
+    assert dif.stored_values == g["diff_D"].size
+    assert rel(dif.apply(g["diff_x"]), g["diff_y"]) < 1e-13
+    dif1 = DiffusionPA(h1, geom)
+    assert rel(dif1.D, g["diff1_D"]) < 1e-14
+    assert rel(dif1.apply(g["diff_x"]), g["diff1_y"]) < 1e-13
+    con = ConvectionPA(h1, geom, g["conv_u"])
+    assert rel(con.D, g["conv_D"]) < 1e-14
+    assert rel(con.apply(g["diff_x"]), g["conv_y"]) < 1e-13
+    with pytest.raises(ValueError):
+        dif.apply(np.zeros(h1.ndof + 1))

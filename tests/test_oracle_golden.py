@@ -138,3 +138,23 @@ def test_oracle_runs_match_reference(name):
     assert rel(dts, z["dts"]) < tol
     assert abs(energies[-1] - z["energies"][-1]) < tol * abs(z["energies"][-1])
     assert hy.clamps == int(z["clamps"])
+
+
+@pytest.mark.parametrize("d,p", CASES)
+def test_remap_operator_fixtures(d, p):
+    """DiffusionPA / ConvectionPA (operators.py:143-236): oracle restatement vs the reference."""
+    g = golden(f"remap_{d}d_p{p}")
+    dofmap, x = g["dofmap"], g["coords"]
+    qpts, qw = O.gauss_legendre(p + 2)
+    _, _, jinv, wdetj = O.geometry(dofmap, x, p, qpts, qw, d)
+    assert rel(jinv, g["jinv"]) < 1e-14 and rel(wdetj, g["wdetj"]) < 1e-14
+    B, G = O.basis_tables(O.gauss_lobatto(p), qpts)
+    D = O.diffusion_D(jinv, wdetj, g["nu"])
+    assert rel(D, g["diff_D"]) < 1e-14
+    assert rel(O.diffusion_apply(dofmap, D, B, G, g["diff_x"], d), g["diff_y"]) < 1e-13
+    D1 = O.diffusion_D(jinv, wdetj)
+    assert rel(D1, g["diff1_D"]) < 1e-14
+    assert rel(O.diffusion_apply(dofmap, D1, B, G, g["diff_x"], d), g["diff1_y"]) < 1e-13
+    Dc = O.convection_D(jinv, g["conv_u"], wdetj)
+    assert rel(Dc, g["conv_D"]) < 1e-14
+    assert rel(O.convection_apply(dofmap, Dc, B, G, g["diff_x"], d), g["conv_y"]) < 1e-13
