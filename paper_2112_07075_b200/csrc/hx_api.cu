@@ -962,9 +962,9 @@ static int launch_mass_brick(hx_ctx* ctx, const MassBrickArgs& a) {
   auto k = k_mass_brick<P, NC>;
   CK(smem_attr(k, M::bytes));
   static unsigned grid = 0;
-  if (!grid) grid = persistent_grid(k, 128, M::bytes, 1ll << 40);
+  if (!grid) grid = persistent_grid(k, M::NT, M::bytes, 1ll << 40);
   prof_begin(ctx, K_MASS);
-  k<<<std::min(grid, gblocks(ctx->ne, M::EPC)), 128, M::bytes, ctx->stream>>>(a);
+  k<<<std::min(grid, gblocks(ctx->ne, M::EPC)), M::NT, M::bytes, ctx->stream>>>(a);
   prof_end(ctx);
   CKL();
   return HX_OK;

@@ -107,11 +107,15 @@ struct CsrSum {
 // (Masked components of p are exactly 0 in this CG -- r, z start at 0 there and
 // Ap := p keeps them 0 -- so p.Ap needs no wall term and p no mask.)
 
+#ifndef MASS_BRICK_NT
+#define MASS_BRICK_NT 128
+#endif
 template <int P, int NC>
 struct MassBrickCfg {
+  static constexpr int NT = MASS_BRICK_NT;   // threads per CTA
   static constexpr int D1 = P + 1, Q = P + 2, QQ = Q * Q, DD = D1 * D1, NL = D1 * DD, NQ = Q * QQ;
   static constexpr int PLN = NC * D1;          // planes per element
-  static constexpr int EPC = 128 / PLN;        // elements per pass
+  static constexpr int EPC = NT / PLN;         // elements per pass
   static constexpr int GP = DD + 1;            // padded plane pitch of the gather / staging image
   static constexpr int GS = PLN * GP;          // gather doubles per element
   static constexpr int TS = PLN * QQ;          // T image doubles per element
@@ -131,7 +135,7 @@ struct MassBrickArgs {
 };
 
 template <int P, int NC>
-__global__ void __launch_bounds__(128, P >= 4 ? 4 : 5) k_mass_brick(MassBrickArgs a) {
+__global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : 5) * 128 / MASS_BRICK_NT) k_mass_brick(MassBrickArgs a) {
   using M = MassBrickCfg<P, NC>;
   constexpr int D1 = M::D1, Q = M::Q, QQ = M::QQ, DD = M::DD, NL = M::NL, NQ = M::NQ;
   constexpr int PLN = M::PLN, EPC = M::EPC, GP = M::GP, GS = M::GS;
@@ -142,7 +146,7 @@ __global__ void __launch_bounds__(128, P >= 4 ? 4 : 5) k_mass_brick(MassBrickArg
   __shared__ double red[32];
   double beta;
   int k;
-  if (!cg_mass_begin<128>(a.cg, red, beta, k)) return;
+  if (!cg_mass_begin<M::NT>(a.cg, red, beta, k)) return;
   const int t = threadIdx.x;
   const double* po = (k & 1) ? a.pbuf0 : a.pbuf1;
   double acc = 0.0;
@@ -151,11 +155,11 @@ __global__ void __launch_bounds__(128, P >= 4 ? 4 : 5) k_mass_brick(MassBrickArg
   // per-thread gather / copy-out slots within an element (pass invariant)
   constexpr int ROWI = D1 * NC;                 // pairs per node row
   constexpr int ELI = DD * ROWI;                // pairs (= E entries) per element
-  constexpr int SLOTS = (ELI + 127) / 128;
+  constexpr int SLOTS = (ELI + M::NT - 1) / M::NT;
   int soff[SLOTS], goff[SLOTS];
 #pragma unroll
   for (int h = 0; h < SLOTS; ++h) {
-    const int it = h * 128 + t;
+    const int it = h * M::NT + t;
     const int row = it / ROWI, s = it - row * ROWI;  // row = dz*D1 + dy
     const int dz = row / D1, dy = row - dz * D1, dx = s / NC, c = s - dx * NC;
     soff[h] = (c * D1 + dz) * GP + dy * D1 + dx;
@@ -182,7 +186,7 @@ __global__ void __launch_bounds__(128, P >= 4 ? 4 : 5) k_mass_brick(MassBrickArg
     // out of the pass loop); all loads of a slot are issued before the first use.
 #pragma unroll
     for (int h = 0; h < SLOTS; ++h) {
-      if (h * 128 + t < ELI) {
+      if (h * M::NT + t < ELI) {
         constexpr int BAT = EPC < 6 ? EPC : 6;
 #pragma unroll
         for (int e1 = 0; e1 < EPC; e1 += BAT) {
@@ -228,7 +232,7 @@ __global__ void __launch_bounds__(128, P >= 4 ? 4 : 5) k_mass_brick(MassBrickArg
     }
     __syncthreads();
     // ---- phase 2 (columns): z, D, z^T for all components of a (qx, qy) column
-    for (int it = t; it < nel * QQ; it += 128) {
+    for (int it = t; it < nel * QQ; it += M::NT) {
       const int ce = it / QQ, l = it - ce * QQ;
       const long long ee = e0 + ce;
       double Dq[Q];
@@ -292,7 +296,7 @@ __global__ void __launch_bounds__(128, P >= 4 ? 4 : 5) k_mass_brick(MassBrickArg
     // through the slot map (read contiguously, scattered 8-byte stores)
     if (a.slot) {
       const int* sl = a.slot + e0 * NL;
-      for (int it = t; it < nel * NL; it += 128) {
+      for (int it = t; it < nel * NL; it += M::NT) {
         const int el = it / NL, l = it - el * NL;
         const int dz = l / DD, k = l - dz * DD;
         const long long pos = (long long)__ldg(sl + it) * NC;
@@ -305,7 +309,7 @@ __global__ void __launch_bounds__(128, P >= 4 ? 4 : 5) k_mass_brick(MassBrickArg
       double* out = a.evec + e0 * (NL * NC);
 #pragma unroll
       for (int h = 0; h < SLOTS; ++h) {
-        const int it = h * 128 + t;
+        const int it = h * M::NT + t;
         if (it < ELI) {
 #pragma unroll
           for (int el = 0; el < EPC; ++el)
@@ -315,7 +319,7 @@ __global__ void __launch_bounds__(128, P >= 4 ? 4 : 5) k_mass_brick(MassBrickArg
     }
     __syncthreads();
   }
-  cg_partial(a.partials, &a.cg->nparts_m, block_sum<128>(acc, red));
+  cg_partial(a.partials, &a.cg->nparts_m, block_sum<M::NT>(acc, red));
 }
 
 }  // namespace hx
