@@ -208,10 +208,12 @@ def problem_setup(args):
     if args.problem == "tgv":
         return (1.0, 1.0, 1.0), (n, n, n), 5.0 / 3.0, (f"3D Taylor-Green vortex Q{args.p}-Q{args.p - 1} (inviscid), "
                                                         f"{n}^3 elements")
-    # triple point [0,7]x[0,3]x[0,1.5]; n = elements along y, aspect 7:3:1.5
-    c = (round(n * 7 / 3), n, max(1, round(n / 2)))
-    return (7.0, 3.0, 1.5), c, 1.5, (f"3D triple point Q{args.p}-Q{args.p - 1} (single gamma), "
-                                      f"{c[0]}x{c[1]}x{c[2]} elements")
+    # multi-material triple point [0,7]x[0,3]x[0,1.5], gamma (1.5, 1.4, 1.5) by region;
+    # n = elements per unit length (even, so that x = 1 and y = 1.5 are element faces)
+    k = max(2, n - n % 2)
+    c = (7 * k, 3 * k, 3 * k // 2)
+    return (7.0, 3.0, 1.5), c, None, (f"3D triple point Q{args.p}-Q{args.p - 1}, multi-material "
+                                       f"(per-element gamma 1.5/1.4/1.5), {c[0]}x{c[1]}x{c[2]} elements")
 
 
 def run_distributed(args, world, rank, local):
@@ -344,13 +346,13 @@ def main():
     # flow is divergence-free, so the viscosity switch would act on rounding noise and the
     # reference itself collapses dt (checked with the oracle)
     visc = ViscosityModel(0.0, 0.0) if args.problem == "tgv" else ViscosityModel(0.5, 2.0)
-    hy = LagrangeHydro(mesh, gauss_legendre(p + 2), MaterialModel(gamma), visc, bc_mask=box_velocity_bc(mesh))
     if args.problem == "sedov":
         fns = problems.sedov(d, extents, counts)
     elif args.problem == "tgv":
         fns = problems.taylor_green(d, gamma)
     else:
-        fns = problems.triple_point(d, gamma)
+        *fns, gamma = problems.triple_point_multi(d, counts, extents)
+    hy = LagrangeHydro(mesh, gauss_legendre(p + 2), MaterialModel(gamma), visc, bc_mask=box_velocity_bc(mesh))
     st0 = hy.initial_state(*fns)
     ctl = StepControls(cfl=args.cfl, dt_max=1.0, t_final=1e9)
     V = d * mesh.num_nodes

@@ -125,6 +125,10 @@ int64_t hx_kernel_launches(hx_ctx* ctx);
  * lexicographic numbering of cartesian_mesh, fespace.py:352-385: index-free CG kernels,
  * element-major E-vectors), 0 = generic CSR transpose map.  Results are identical. */
 int hx_layout(hx_ctx* ctx);
+/* Multi-material extension (not in the reference, whose MaterialModel has one gamma,
+ * hydro.py:40-48): per-element adiabatic index gamma_e (NE, device) used by the stress /
+ * rates kernels instead of hx_params.gamma; NULL restores the single gamma. */
+int hx_set_material(hx_ctx* ctx, const double* gamma_e);
 
 /* ---- restriction (fespace.py:221-234) -------------------------------- */
 

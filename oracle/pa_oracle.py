@@ -456,8 +456,10 @@ class Hydro:
         self.dofmap = dofmap
         self.coords0 = coords
         self.nn, self.ne = coords.shape[0], dofmap.shape[1]
-        self.gamma, self.q1, self.q2 = gamma, q1, q2
-        if gamma <= 1.0:
+        # gamma: one value (the reference) or one per element (multi-material extension)
+        self.gamma = np.asarray(gamma, dtype=float)[None, :] if np.ndim(gamma) > 0 else gamma
+        self.q1, self.q2 = q1, q2
+        if np.any(np.asarray(gamma) <= 1.0):
             raise ValueError("adiabatic index must exceed 1")
         self.tol = momentum_rel_tol
         self.qpts, self.qw = gauss_legendre(p + 2 if q1d is None else q1d)

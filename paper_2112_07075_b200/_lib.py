@@ -67,6 +67,7 @@ _SIGS = {
     "hx_last_error": (C.c_char_p, [P]),
     "hx_kernel_launches": (C.c_int64, [P]),
     "hx_layout": (C.c_int, [P]),
+    "hx_set_material": (C.c_int, [P, P]),
     "hx_diffusion_create": (C.c_int, [P, P, P, P, P, C.POINTER(C.c_void_p)]),
     "hx_convection_create": (C.c_int, [P, P, P, P, P, C.POINTER(C.c_void_p)]),
     "hx_op_apply": (C.c_int, [P, P, P]),

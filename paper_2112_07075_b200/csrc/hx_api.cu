@@ -46,6 +46,7 @@ struct hx_ctx {
   double* evec = nullptr;     // (NE, nl, d)
   double* evec2 = nullptr;    // second E buffer (API scatter staging)
   double *r = nullptr, *z = nullptr, *p0 = nullptr, *p1 = nullptr;
+  double* gamma_e = nullptr;  // per-element adiabatic index override (hx_set_material) or null
   char* arena = nullptr;      // CG working set: pairs, r, 1/diag, mask, x (dv0, dv1), E-vector, D_M
   size_t arena_bytes = 0;
   double* partials = nullptr; // reduction partials: two regions of preg doubles
@@ -249,7 +250,7 @@ struct LaunchRates {
     if constexpr (DIM == 3 && P >= 2) {
       if (g_rates_kernel == 1) {
         RatesPCArgs a{x, v, e, ctx->qd0, ctx->emap, ctx->elem_major ? nullptr : ctx->slot, ctx->minv, ctx->wnd,
-                      ctx->psi1, gamma, q1, q2, ctx->ne, evec, de, st, ctx->bk, ctx->brick ? 1 : 0};
+                      ctx->psi1, gamma, q1, q2, ctx->gamma_e, ctx->ne, evec, de, st, ctx->bk, ctx->brick ? 1 : 0};
         return mode == 0 ? launch_rates_pc<P, 0>(ctx, a) : launch_rates_pc<P, 1>(ctx, a);
       }
     }
@@ -260,7 +261,8 @@ struct LaunchRates {
       CK(smem_attr(kern, SM::bytes));
       attr = true;
     }
-    RatesArgs a{x, v, e, ctx->qd0, ctx->emap, ctx->elem_major ? nullptr : ctx->slot, ctx->minv, tables(ctx), gamma, q1, q2, ctx->ne, evec, de, st, mode};
+    RatesArgs a{x, v, e, ctx->qd0, ctx->emap, ctx->elem_major ? nullptr : ctx->slot, ctx->minv, tables(ctx), gamma, q1, q2,
+                ctx->gamma_e, ctx->ne, evec, de, st, mode};
     prof_begin(ctx, mode == 0 ? K_RATES : K_VALID);
     kern<<<(unsigned)ctx->ne, RATES_NT, SM::bytes, ctx->stream>>>(a);
     prof_end(ctx);
@@ -740,7 +742,7 @@ extern "C" int hx_destroy(hx_ctx* ctx) {
   void* dev[] = {ctx->B,  ctx->G,    ctx->Bt,   ctx->wnd,  ctx->psi1, ctx->emap, ctx->off,   ctx->idx,
                  ctx->own, ctx->slot, ctx->emapf, ctx->emapf_api, ctx->arena, ctx->evec2, ctx->z, ctx->partials,
                  ctx->hist, ctx->cg,  ctx->st,   ctx->dt,   ctx->scal, ctx->qd0,   ctx->minv,
-                 ctx->mdiag, ctx->xm, ctx->vm,   ctx->em,
+                 ctx->mdiag, ctx->xm, ctx->vm,   ctx->em, ctx->gamma_e,
                  ctx->de0, ctx->de1, ctx->hx_x, ctx->hx_v, ctx->hx_e, ctx->hx_xo, ctx->hx_vo, ctx->hx_eo};
   for (void* p : dev)
     if (p) cudaFree(p);
@@ -767,6 +769,22 @@ extern "C" int hx_set_stream(hx_ctx* ctx, void* stream) {
 extern "C" const char* hx_last_error(hx_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 extern "C" int64_t hx_kernel_launches(hx_ctx* ctx) { return ctx ? ctx->launches : 0; }
 extern "C" int hx_layout(hx_ctx* ctx) { return ctx && ctx->brick ? 1 : 0; }
+
+extern "C" int hx_set_material(hx_ctx* ctx, const double* gamma_e) {
+  if (!ctx) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  if (!gamma_e) {
+    if (ctx->gamma_e) cudaFree(ctx->gamma_e);
+    ctx->gamma_e = nullptr;
+  } else {
+    if (!ctx->gamma_e) CK(dalloc(&ctx->gamma_e, (size_t)ctx->ne));
+    CK(cudaMemcpyAsync(ctx->gamma_e, gamma_e, sizeof(double) * ctx->ne, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  for (auto& g : ctx->graphs)  // captured steps bake the material pointer in
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  ctx->graphs.clear();
+  return HX_OK;
+}
 
 // ---------------------------------------------------------------------------
 // restriction
@@ -1344,7 +1362,7 @@ extern "C" int hx_stress(hx_ctx* ctx, const hx_params* prm, const double* x, con
   StatusDev* st = ctx->st + 3;
   int rc = status_reset(ctx, st);
   if (rc) return rc;
-  StressArgs a{x, v, e, qdata0, ctx->emap, tables(ctx), prm->gamma, prm->q1, prm->q2, ctx->ne, sigma, st};
+  StressArgs a{x, v, e, qdata0, ctx->emap, tables(ctx), prm->gamma, prm->q1, prm->q2, ctx->gamma_e, ctx->ne, sigma, st};
   rc = dispatch<LaunchStress>(ctx, a);
   if (rc) return rc;
   rc = read_status(ctx, st, ctx->h_st + 3);

@@ -173,6 +173,7 @@ struct RatesArgs {
   const double* minv;  // (NE, nt, nt)
   Tables tab;
   double gamma, q1, q2;
+  const double* gam;   // per-element adiabatic index (multi-material extension) or null
   long long ne;
   double* evec;        // (NE, nl, d)  element F.1
   double* de;          // (NE*nt)      M_e^{-1} F^T v
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(NT) k_rates(RatesArgs a) {
       vq[c] = rOut[((DIM + c) * (DIM + 1) + DIM) * NQ + q];
     }
     PointOut<DIM> po;
-    point_physics<DIM>(J, dv, vq, eq[q], a.qd0[e * NQ + q], a.gamma, a.q1, a.q2, po);
+    point_physics<DIM>(J, dv, vq, eq[q], a.qd0[e * NQ + q], a.gam ? __ldg(a.gam + e) : a.gamma, a.q1, a.q2, po);
     if (po.det <= 0.0) {
       const unsigned long long k = (unsigned long long)q * a.ne + e;
       key = k < key ? k : key;
@@ -1370,6 +1371,7 @@ struct StressArgs {
   const int* emap;
   Tables tab;
   double gamma, q1, q2;
+  const double* gam;   // per-element adiabatic index (multi-material extension) or null
   long long ne;
   double* sigma;         // (d,d,nq,NE) or null
   StatusDev* st;
@@ -1421,7 +1423,7 @@ __global__ void __launch_bounds__(NT) k_stress(StressArgs a) {
     }
     const long long pe = (long long)q * ne + e;
     PointOut<DIM> po;
-    point_physics<DIM>(J, dv, vq, eq[q], a.qdata0[pe], a.gamma, a.q1, a.q2, po);
+    point_physics<DIM>(J, dv, vq, eq[q], a.qdata0[pe], a.gam ? __ldg(a.gam + e) : a.gamma, a.q1, a.q2, po);
     if (po.det <= 0.0) {
       const unsigned long long k = (unsigned long long)q * ne + e;
       key = k < key ? k : key;

@@ -85,6 +85,7 @@ struct RatesPCArgs {
   const double* wnd;   // (nq)
   const double* psi1;  // (nq)
   double gamma, q1, q2;
+  const double* gam;   // per-element adiabatic index (multi-material extension) or null
   long long ne;
   double* evec;        // (NE, nl, 3) F.1 element vectors
   double* de;          // (NE*nt)
@@ -374,7 +375,8 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
 #pragma unroll
         for (int dz = 0; dz < DT; ++dz) eq = fma(cBt[qz * DT + dz], T[TFS + dz * QQ + col], eq);
         PointOut<3> po;
-        point_physics_fast(J, dv, vq, eq, gcur[R::FQ + el * NQ + q], a.gamma, a.q1, a.q2, po);
+        point_physics_fast(J, dv, vq, eq, gcur[R::FQ + el * NQ + q], a.gam ? __ldg(a.gam + e) : a.gamma, a.q1,
+                           a.q2, po);
         if (po.det <= 0.0) {
           const unsigned long long kk = (unsigned long long)q * a.ne + e;
           key = kk < key ? kk : key;

@@ -43,15 +43,23 @@ __all__ = [
 ]
 
 
-@dataclass(frozen=True)
+@dataclass(frozen=True, eq=False)
 class MaterialModel:
-    """Ideal gas p = (gamma - 1) rho e (hydro.py:40-48)."""
+    """Ideal gas p = (gamma - 1) rho e (hydro.py:40-48).
+
+    Extension (not in the reference, which has one gamma): `gamma` may be an array of one
+    adiabatic index per element (multi-material, e.g. the triple point); the device kernels
+    then read gamma per element (hx_set_material)."""
 
     gamma: float = 5.0 / 3.0
 
     def __post_init__(self):
-        if self.gamma <= 1.0:
+        if np.any(np.asarray(self.gamma, dtype=float) <= 1.0):
             raise ValueError("adiabatic index must exceed 1")
+
+    @property
+    def per_element(self) -> bool:
+        return np.ndim(self.gamma) > 0
 
 
 @dataclass(frozen=True)
@@ -177,12 +185,20 @@ class LagrangeHydro:
         self._ctx = DeviceContext(mesh, quad)
         self._mask_dev = to_dev(np.asarray(self.bc_mask), torch.uint8)
         self._phase_ready = False
+        if material.per_element:
+            g = np.asarray(material.gamma, dtype=float).reshape(-1)
+            if g.shape != (mesh.num_elements,):
+                raise ValueError(f"per-element gamma must have {mesh.num_elements} entries")
+            self._gamma_dev = to_dev(g)
+            self._ctx.sync_stream()
+            self._ctx.check(self._ctx.lib.hx_set_material(self._ctx.h, _lib.ptr(self._gamma_dev)), "MaterialModel")
 
     # -- helpers ----------------------------------------------------------------
 
     def _params(self, controls: StepControls | None = None, rel_tol=None, max_retries=5):
         c = controls or StepControls()
-        return _lib.Params(float(self.material.gamma), float(self.viscosity.q1), float(self.viscosity.q2),
+        g0 = float(np.asarray(self.material.gamma, dtype=float).reshape(-1)[0])
+        return _lib.Params(g0, float(self.viscosity.q1), float(self.viscosity.q2),
                            float(self.momentum_rel_tol if rel_tol is None else rel_tol), 2000, int(max_retries),
                            float(c.cfl), float(c.dt_min), float(c.dt_max), float(c.t_final))
 

@@ -10,7 +10,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["sedov", "taylor_green", "triple_point"]
+__all__ = ["sedov", "taylor_green", "triple_point", "triple_point_multi"]
 
 
 def sedov(dim, extents, counts, energy=0.25):
@@ -78,3 +78,48 @@ def triple_point(dim, gamma=1.5):
         return pr / ((gamma - 1.0) * rho)
 
     return rho0, v0, e0
+
+
+TRIPLE_GAMMA = (1.5, 1.4, 1.5)  # Laghos triple point: left, lower-right, upper-right
+
+
+def _triple_region(x, y):
+    """0: x < 1; 1: x >= 1, y < 1.5; 2: x >= 1, y >= 1.5."""
+    return np.where(x < 1.0, 0, np.where(y < 1.5, 1, 2))
+
+
+def triple_point_multi(dim, counts, extents=(7.0, 3.0, 1.5)):
+    """Multi-material triple point (Laghos convention): the three regions of `triple_point`
+    with their own adiabatic index (1.5, 1.4, 1.5).  Returns (rho0_fn, v0_fn, e0_fn,
+    gamma_e) with one gamma per element (element regions from the centroids; the region
+    boundaries x = 1, y = 1.5 must be element faces).  A multi-material extension: the
+    reference's MaterialModel has one gamma (hydro.py:40-48), so parity is against the
+    oracle with the same per-element gamma."""
+    ext = np.asarray(extents[:dim], float)
+    cnt = np.asarray(counts[:dim], int)
+    h = ext / cnt
+    for a, b in ((0, 1.0), (1, 1.5)):
+        if abs(b / h[a] - round(b / h[a])) > 1e-9:
+            raise ValueError("triple-point region boundaries must be element faces")
+    ne = int(np.prod(cnt))
+    ec = np.array(np.unravel_index(np.arange(ne), cnt, order="F"), dtype=float)
+    cen = (ec + 0.5) * h[:, None]
+    reg = _triple_region(cen[0], cen[1])
+    gamma_e = np.asarray(TRIPLE_GAMMA)[reg]
+
+    def fields(pts):
+        r = _triple_region(pts[0], pts[1])
+        rho = np.where(r == 2, 0.125, 1.0)
+        return rho, np.where(r == 0, 1.0, 0.1), np.asarray(TRIPLE_GAMMA)[r]
+
+    def rho0(xq):
+        return fields(xq)[0]
+
+    def v0(x):
+        return np.zeros_like(x)
+
+    def e0(pts):
+        rho, pr, g = fields(pts)
+        return pr / ((g - 1.0) * rho)
+
+    return rho0, v0, e0, gamma_e

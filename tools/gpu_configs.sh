@@ -6,7 +6,7 @@ run() { NAME=$1; shift; timeout 400 python bench.py --steps 10 --warmup 3 --no-c
 run sedov_q3_n23 --p 3 --n 23
 run sedov_q2_n34 --p 2 --n 34
 run tgv_q4_n17 --p 4 --n 17 --problem tgv
-run triple_q3_n22 --p 3 --n 22 --problem triple
+run triple_q3_k8 --p 3 --n 8 --problem triple
 run sedov_q3_n30 --p 3 --n 30
 python - <<'PY'
 import json, glob, os
