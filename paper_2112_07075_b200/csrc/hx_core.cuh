@@ -428,8 +428,21 @@ __device__ __forceinline__ bool grid_last_block(unsigned int* counter, int* sfla
 // fixed-order sum of n partials by one block of NT threads; result in thread 0
 template <int NT>
 __device__ __forceinline__ double reduce_partials(const double* partials, int n, double* sbuf) {
+  // up to 8 strided partials per thread, all loads in flight before the (ordered) adds;
+  // larger grids fall back to the loop
   double acc = 0.0;
-  for (int i = threadIdx.x; i < n; i += NT) acc += __ldcg(partials + i);
+  if (n <= 8 * NT) {
+    double w[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int i = threadIdx.x + c * NT;
+      w[c] = i < n ? __ldcg(partials + i) : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc += w[c];
+  } else {
+    for (int i = threadIdx.x; i < n; i += NT) acc += __ldcg(partials + i);
+  }
   return block_sum<NT>(acc, sbuf);
 }
 
