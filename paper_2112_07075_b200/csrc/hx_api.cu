@@ -239,6 +239,24 @@ static int launch_rates_pc(hx_ctx* ctx, const RatesPCArgs& a) {
   return HX_OK;
 }
 
+template <int P>
+static int launch_valid(hx_ctx* ctx, const RatesPCArgs& a) {
+  using V = ValidCfg<P>;
+  auto k = k_valid<P>;
+  static bool attr = false;
+  if (!attr) {
+    CK(smem_attr(k, V::bytes));
+    attr = true;
+  }
+  static unsigned grid = 0;
+  if (!grid) grid = persistent_grid(k, V::NT, V::bytes, 1ll << 40);
+  prof_begin(ctx, K_VALID);
+  k<<<std::min(grid, gblocks(ctx->ne, V::EPC)), V::NT, V::bytes, ctx->stream>>>(a);
+  prof_end(ctx);
+  CKL();
+  return HX_OK;
+}
+
 template <int DIM, int P>
 struct LaunchRates {
   static int run(hx_ctx* ctx, const double* x, const double* v, const double* e, double* evec, double* de,
@@ -251,7 +269,7 @@ struct LaunchRates {
       if (g_rates_kernel == 1) {
         RatesPCArgs a{x, v, e, ctx->qd0, ctx->emap, ctx->elem_major ? nullptr : ctx->slot, ctx->minv, ctx->wnd,
                       ctx->psi1, gamma, q1, q2, ctx->gamma_e, ctx->ne, evec, de, st, ctx->bk, ctx->brick ? 1 : 0};
-        return mode == 0 ? launch_rates_pc<P, 0>(ctx, a) : launch_rates_pc<P, 1>(ctx, a);
+        return mode == 0 ? launch_rates_pc<P, 0>(ctx, a) : launch_valid<P>(ctx, a);
       }
     }
     using SM = RatesSmem<DIM, P>;

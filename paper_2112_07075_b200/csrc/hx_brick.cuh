@@ -110,16 +110,34 @@ struct CsrSum {
 #ifndef MASS_BRICK_NT
 #define MASS_BRICK_NT 128
 #endif
+#ifndef MASS_ALIAS
+#define MASS_ALIAS 1
+#endif
+#ifndef MASS_BAT
+#define MASS_BAT 0
+#endif
+#ifndef MASS_BRICK_MINB
+#define MASS_BRICK_MINB 5
+#endif
 template <int P, int NC>
 struct MassBrickCfg {
   static constexpr int NT = MASS_BRICK_NT;   // threads per CTA
   static constexpr int D1 = P + 1, Q = P + 2, QQ = Q * Q, DD = D1 * D1, NL = D1 * DD, NQ = Q * QQ;
   static constexpr int PLN = NC * D1;          // planes per element
   static constexpr int EPC = NT / PLN;         // elements per pass
+#if MASS_ALIAS
+  // gather / staging planes live inside the T planes: each plane thread reads its own
+  // plane into registers before it overwrites it (phases 1 and 3), so one image suffices
+  static constexpr int GP = QQ;
+  static constexpr int GS = PLN * GP;
+  static constexpr int TS = PLN * QQ;
+  static constexpr size_t bytes = sizeof(double) * (size_t)EPC * TS;
+#else
   static constexpr int GP = DD + 1;            // padded plane pitch of the gather / staging image
   static constexpr int GS = PLN * GP;          // gather doubles per element
   static constexpr int TS = PLN * QQ;          // T image doubles per element
   static constexpr size_t bytes = sizeof(double) * (size_t)EPC * (GS + TS);
+#endif
 };
 
 struct MassBrickArgs {
@@ -135,14 +153,18 @@ struct MassBrickArgs {
 };
 
 template <int P, int NC>
-__global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : 5) * 128 / MASS_BRICK_NT) k_mass_brick(MassBrickArgs a) {
+__global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : MASS_BRICK_MINB) * 128 / MASS_BRICK_NT) k_mass_brick(MassBrickArgs a) {
   using M = MassBrickCfg<P, NC>;
   constexpr int D1 = M::D1, Q = M::Q, QQ = M::QQ, DD = M::DD, NL = M::NL, NQ = M::NQ;
   constexpr int PLN = M::PLN, EPC = M::EPC, GP = M::GP, GS = M::GS;
   const double* cB = c_B[P - 1];
   extern __shared__ double smem[];
   double* sG = smem;                 // gather image [el][c][dz][dy*D1+dx] (pitch GP); reused as staging
+#if MASS_ALIAS
+  double* sT = smem;
+#else
   double* sT = smem + EPC * GS;      // T image [el][c][dz][qy*Q+qx]
+#endif
   __shared__ double red[32];
   double beta;
   int k;
@@ -184,6 +206,28 @@ __global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : 5) * 128 / MASS_B
     // ---- phase 0: node rows (D1 nodes x NC pairs, contiguous) -> p image.  Thread t
     // owns the same (row, pair) slots of every element of the pass (offsets hoisted
     // out of the pass loop); all loads of a slot are issued before the first use.
+#if MASS_BAT
+    {
+      // every (slot, element) load of the thread in flight together, BAT at a time
+      constexpr int TOT = SLOTS * EPC, BAT = MASS_BAT < TOT ? MASS_BAT : TOT;
+#pragma unroll
+      for (int b0 = 0; b0 < TOT; b0 += BAT) {
+        double2 q[BAT];
+#pragma unroll
+        for (int u = 0; u < BAT; ++u) {
+          const int h = (b0 + u) / EPC, el = (b0 + u) - h * EPC;
+          if (b0 + u < TOT && h * M::NT + t < ELI && el < nel)
+            q[u] = __ldcg(reinterpret_cast<const double2*>(po) + (sbase[el] * NC + goff[h]));
+        }
+#pragma unroll
+        for (int u = 0; u < BAT; ++u) {
+          const int h = (b0 + u) / EPC, el = (b0 + u) - h * EPC;
+          if (b0 + u < TOT && h * M::NT + t < ELI && el < nel)
+            sG[el * GS + soff[h]] = __dadd_rn(q[u].x, __dmul_rn(beta, q[u].y));
+        }
+      }
+    }
+#else
 #pragma unroll
     for (int h = 0; h < SLOTS; ++h) {
       if (h * M::NT + t < ELI) {
@@ -201,6 +245,7 @@ __global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : 5) * 128 / MASS_B
         }
       }
     }
+#endif
     __syncthreads();
     // ---- phase 1 (planes): x and y contractions in registers -> T
     const bool pact = pe < nel;

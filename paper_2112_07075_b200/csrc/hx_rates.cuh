@@ -576,4 +576,139 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
   publish_status<256>(a.st, rmin, clamps, key, nullptr);
 }
 
+
+// ---------------------------------------------------------------------------
+// Geometry validity of a new state (rk2_step's check, hydro.py:400-401 ->
+// compute_geometric_factors fespace.py:305-346): det J at every quadrature point,
+// first inverted (q-major) point as the status key.  x only, so it gets its own lean
+// kernel: 4 elements per pass, 4 CTAs per SM, no prefetch buffers.  J is formed with
+// the same contraction order as k_rates_pc (x, y, z stages, ascending sums from 0.0)
+// and det with det_inv_fast's expression, so both kernels agree on every det J.
+template <int P>
+struct ValidCfg {
+  static constexpr int D1 = P + 1, Q = P + 2, DD = D1 * D1, QQ = Q * Q, NQ = Q * QQ;
+  static constexpr int NT = 128, EPC = 4;
+  static constexpr int GP = DD + 1, GS = 3 * D1 * GP;         // gather image (c, dz) planes
+  static constexpr int XP = 2 * Q + 1, XS = 3 * DD * XP;      // x-stage rows (c, dz, dy)
+  static constexpr int PP = 3 * QQ + ((Q - 3 * QQ) % 16 + 16) % 16;
+  static constexpr int TS = 3 * D1 * PP;                      // y-stage planes (c, dz), aliases G
+  static constexpr int PER = XS + (TS > GS ? TS : GS);
+  static constexpr size_t bytes = sizeof(double) * (size_t)EPC * PER;
+};
+
+template <int P>
+__global__ void __launch_bounds__(128, 4) k_valid(RatesPCArgs a) {
+  using V = ValidCfg<P>;
+  constexpr int D1 = V::D1, Q = V::Q, DD = V::DD, QQ = V::QQ, NQ = V::NQ, NL = D1 * DD;
+  constexpr int NT = V::NT, EPC = V::EPC, GP = V::GP, XP = V::XP, PP = V::PP, PER = V::PER, XS = V::XS;
+  const double* cB = c_B[P - 1];
+  const double* cG = c_G[P - 1];
+  extern __shared__ __align__(16) double smem[];
+  const int t = threadIdx.x;
+  unsigned long long key = ~0ull;
+  for (long long e0 = (long long)blockIdx.x * EPC; e0 < a.ne; e0 += (long long)gridDim.x * EPC) {
+    const int nel = (int)((a.ne - e0) < EPC ? (a.ne - e0) : EPC);
+    // gather x node rows -> G image (aliases the T image of the previous pass)
+    constexpr int ROW = 3 * D1;
+    for (int it = t; it < nel * DD * ROW; it += NT) {
+      const int el = it / (DD * ROW), rem = it - el * (DD * ROW);
+      const int row = rem / ROW, sidx = rem - row * ROW;
+      const int dz = row / D1, dy = row - dz * D1, dx = sidx / 3, c = sidx - dx * 3;
+      const long long e = e0 + el;
+      long long n;
+      if (a.brick) {
+        const unsigned ue = (unsigned)e;
+        const unsigned ez = a.b.fnxy.div(ue);
+        const unsigned r2 = ue - ez * (unsigned)(a.b.nx * a.b.ny);
+        const unsigned ey = a.b.fnx.div(r2), ex = r2 - ey * (unsigned)a.b.nx;
+        n = (long long)(ex * P + dx) + (long long)(ey * P + dy) * a.b.Nx + (long long)(ez * P + dz) * a.b.NxNy;
+      } else {
+        n = __ldg(a.emap + e * NL + row * D1 + dx);
+      }
+      smem[el * PER + XS + (c * D1 + dz) * GP + dy * D1 + dx] = __ldg(a.x + n * 3 + c);
+    }
+    __syncthreads();
+    // x stage, thread per (c, dz, dy) row
+    for (int it = t; it < nel * 3 * DD; it += NT) {
+      const int el = it / (3 * DD), k = it - el * (3 * DD);
+      const int pl = k / D1, dy = k - pl * D1;
+      const double* g = smem + el * PER + XS + pl * GP + dy * D1;
+      double u[D1];
+#pragma unroll
+      for (int dx = 0; dx < D1; ++dx) u[dx] = g[dx];
+      double* o = smem + el * PER + k * XP;
+#pragma unroll
+      for (int qx = 0; qx < Q; ++qx) {
+        double sb = 0.0, sg = 0.0;
+#pragma unroll
+        for (int dx = 0; dx < D1; ++dx) {
+          sb = fma(cB[qx * D1 + dx], u[dx], sb);
+          sg = fma(cG[qx * D1 + dx], u[dx], sg);
+        }
+        o[qx] = sb;
+        o[Q + qx] = sg;
+      }
+    }
+    __syncthreads();
+    // y stage, thread per (c, dz, qx) line -> T (over the dead G image)
+    for (int it = t; it < nel * 3 * D1 * Q; it += NT) {
+      const int el = it / (3 * D1 * Q), k = it - el * (3 * D1 * Q);
+      const int pl = k / Q, qx = k - pl * Q;
+      const double* X = smem + el * PER;
+      double vb[D1], vg[D1];
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy) {
+        vb[dy] = X[(pl * D1 + dy) * XP + qx];
+        vg[dy] = X[(pl * D1 + dy) * XP + Q + qx];
+      }
+      double* o = smem + el * PER + XS + pl * PP + qx;
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy) {
+        double bb = 0.0, gb = 0.0, bg = 0.0;
+#pragma unroll
+        for (int dy = 0; dy < D1; ++dy) {
+          bb = fma(cB[qy * D1 + dy], vb[dy], bb);
+          gb = fma(cG[qy * D1 + dy], vb[dy], gb);
+          bg = fma(cB[qy * D1 + dy], vg[dy], bg);
+        }
+        o[qy * Q] = bb;
+        o[QQ + qy * Q] = gb;
+        o[2 * QQ + qy * Q] = bg;
+      }
+    }
+    __syncthreads();
+    // z stage + det J, thread per point
+    for (int it = t; it < nel * NQ; it += NT) {
+      const int el = it / NQ, kq = it - el * NQ;
+      const int col = kq / Q, qz = kq - col * Q;
+      const int q = qz * QQ + col;
+      const double* T = smem + el * PER + XS;
+      double J[3][3];
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+#pragma unroll
+        for (int dz = 0; dz < D1; ++dz) {
+          const double* tt = T + (f * D1 + dz) * PP + col;
+          d0 = fma(cB[qz * D1 + dz], tt[2 * QQ], d0);
+          d1 = fma(cB[qz * D1 + dz], tt[QQ], d1);
+          d2 = fma(cG[qz * D1 + dz], tt[0], d2);
+        }
+        J[f][0] = d0;
+        J[f][1] = d1;
+        J[f][2] = d2;
+      }
+      const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                         J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                         J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+      if (det <= 0.0) {
+        const unsigned long long kk = (unsigned long long)q * a.ne + (e0 + el);
+        key = kk < key ? kk : key;
+      }
+    }
+    __syncthreads();
+  }
+  publish_status<NT>(a.st, __longlong_as_double(0x7ff0000000000000ll), 0, key, nullptr);
+}
+
 }  // namespace hx
