@@ -93,6 +93,25 @@ struct BrickSum {
   }
 };
 
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16d(double* dst, const double* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+// contiguous span of n doubles (dst 16-byte aligned): 16-byte copies when src allows
+template <int NT>
+__device__ __forceinline__ void cp_span(double* dst, const double* src, int n, int t) {
+  if ((reinterpret_cast<unsigned long long>(src) & 15ull) == 0) {
+    for (int i = t; i < n / 2; i += NT) cp_async16d(dst + 2 * i, src + 2 * i);
+    if ((n & 1) && t == 0) cp_async8(dst + n - 1, src + n - 1);
+  } else {
+    for (int i = t; i < n; i += NT) cp_async8(dst + i, src + i);
+  }
+}
+
 // generic (CSR, node-sorted E-vector) node sum as a functor
 template <int NC>
 struct CsrSum {
@@ -113,6 +132,12 @@ struct CsrSum {
 #ifndef MASS_ALIAS
 #define MASS_ALIAS 1
 #endif
+#ifndef MASS_LD
+#define MASS_LD __ldcg
+#endif
+#ifndef MASS_DPF
+#define MASS_DPF 0
+#endif
 #ifndef MASS_BAT
 #define MASS_BAT 0
 #endif
@@ -131,7 +156,7 @@ struct MassBrickCfg {
   static constexpr int GP = QQ;
   static constexpr int GS = PLN * GP;
   static constexpr int TS = PLN * QQ;
-  static constexpr size_t bytes = sizeof(double) * (size_t)EPC * TS;
+  static constexpr size_t bytes = sizeof(double) * (size_t)EPC * (TS + (MASS_DPF ? NQ : 0));
 #else
   static constexpr int GP = DD + 1;            // padded plane pitch of the gather / staging image
   static constexpr int GS = PLN * GP;          // gather doubles per element
@@ -158,12 +183,15 @@ __global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : MASS_BRICK_MINB) 
   constexpr int D1 = M::D1, Q = M::Q, QQ = M::QQ, DD = M::DD, NL = M::NL, NQ = M::NQ;
   constexpr int PLN = M::PLN, EPC = M::EPC, GP = M::GP, GS = M::GS;
   const double* cB = c_B[P - 1];
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   double* sG = smem;                 // gather image [el][c][dz][dy*D1+dx] (pitch GP); reused as staging
 #if MASS_ALIAS
   double* sT = smem;
 #else
   double* sT = smem + EPC * GS;      // T image [el][c][dz][qy*Q+qx]
+#endif
+#if MASS_DPF
+  double* sD = smem + EPC * M::TS;   // D of the pass (cp.async at the start of the pass)
 #endif
   __shared__ double red[32];
   double beta;
@@ -195,6 +223,11 @@ __global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : MASS_BRICK_MINB) 
   for (int ps = 0; ps < npass; ++ps) {
     const int e0 = ebeg + len * ps / npass;
     const int nel = ebeg + len * (ps + 1) / npass - e0;
+#if MASS_DPF
+    // D of the pass lands in shared memory while the gather and phase 1 run
+    cp_span<M::NT>(sD, a.D + (long long)e0 * NQ, nel * NQ, t);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+#endif
     if (t < nel) {
       const unsigned e = (unsigned)(e0 + t);
       const unsigned ez = a.b.fnxy.div(e);
@@ -238,7 +271,7 @@ __global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : MASS_BRICK_MINB) 
 #pragma unroll
           for (int u = 0; u < BAT; ++u)
             if (e1 + u < nel)
-              q[u] = __ldcg(reinterpret_cast<const double2*>(po) + (sbase[e1 + u] * NC + goff[h]));
+              q[u] = MASS_LD(reinterpret_cast<const double2*>(po) + (sbase[e1 + u] * NC + goff[h]));
 #pragma unroll
           for (int u = 0; u < BAT; ++u)
             if (e1 + u < nel) sG[(e1 + u) * GS + soff[h]] = __dadd_rn(q[u].x, __dmul_rn(beta, q[u].y));
@@ -275,6 +308,9 @@ __global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : MASS_BRICK_MINB) 
           T[qy * Q + qx] = s;
         }
     }
+#if MASS_DPF
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+#endif
     __syncthreads();
     // ---- phase 2 (columns): z, D, z^T for all components of a (qx, qy) column
     for (int it = t; it < nel * QQ; it += M::NT) {
@@ -282,7 +318,12 @@ __global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : MASS_BRICK_MINB) 
       const long long ee = e0 + ce;
       double Dq[Q];
 #pragma unroll
-      for (int qz = 0; qz < Q; ++qz) Dq[qz] = __ldg(a.D + ee * NQ + qz * QQ + l);
+      for (int qz = 0; qz < Q; ++qz)
+#if MASS_DPF
+        Dq[qz] = sD[ce * NQ + qz * QQ + l];
+#else
+        Dq[qz] = __ldg(a.D + ee * NQ + qz * QQ + l);
+#endif
       double* base = sT + ce * M::TS + l;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {

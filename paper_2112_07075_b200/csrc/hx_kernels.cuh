@@ -958,6 +958,12 @@ __device__ __forceinline__ void node_sum(const int* off, const int* idx, const d
   (void)idx;
 }
 
+#ifndef NODE_U
+#define NODE_U 2
+#endif
+#ifndef NODE_MINB
+#define NODE_MINB 4
+#endif
 struct NodeArgs {
   const int* off;
   const int* idx;
@@ -1069,7 +1075,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_init(NodeArgs a, SUM sum) {
 // Ap = G^T evec (identity on masked rows), x += alpha p, r -= alpha Ap, z = D^{-1} r,
 // rz_new = r.z; stop test sqrt(max(rz_new,0)) <= tol*norm0; beta = rz_new/rz.
 template <int NC, class SUM>
-__global__ void __launch_bounds__(256, 4) k_cg_node(NodeArgs a, SUM sum) {
+__global__ void __launch_bounds__(256, NODE_MINB) k_cg_node(NodeArgs a, SUM sum) {
   __shared__ double red[32];
   CGDev* g = a.cg;
   double alpha, alpha_prev;
@@ -1085,7 +1091,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_node(NodeArgs a, SUM sum) {
   double rz = 0.0;
   // grid-stride over (node, component), U items per thread per trip so that all
   // their loads are in flight together
-  constexpr int U = 2;
+  constexpr int U = NODE_U;
   const long long N = a.nn * NC;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long j0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; j0 < N; j0 += U * stride) {

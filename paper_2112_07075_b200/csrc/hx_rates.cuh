@@ -55,25 +55,6 @@ struct RatesPC {
   static constexpr size_t bytes = sizeof(double) * (2 * (size_t)FS + (size_t)EPC * PER + 2 * NQ);
 };
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async16d(double* dst, const double* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
-               : "memory");
-}
-// contiguous span of n doubles (dst 16-byte aligned): 16-byte copies when src allows
-template <int NT>
-__device__ __forceinline__ void cp_span(double* dst, const double* src, int n, int t) {
-  if ((reinterpret_cast<unsigned long long>(src) & 15ull) == 0) {
-    for (int i = t; i < n / 2; i += NT) cp_async16d(dst + 2 * i, src + 2 * i);
-    if ((n & 1) && t == 0) cp_async8(dst + n - 1, src + n - 1);
-  } else {
-    for (int i = t; i < n; i += NT) cp_async8(dst + i, src + i);
-  }
-}
-
 struct RatesPCArgs {
   const double* x;     // (NN, 3)
   const double* v;     // (NN, 3)
@@ -608,24 +589,38 @@ __global__ void __launch_bounds__(128, 4) k_valid(RatesPCArgs a) {
   unsigned long long key = ~0ull;
   for (long long e0 = (long long)blockIdx.x * EPC; e0 < a.ne; e0 += (long long)gridDim.x * EPC) {
     const int nel = (int)((a.ne - e0) < EPC ? (a.ne - e0) : EPC);
-    // gather x node rows -> G image (aliases the T image of the previous pass)
-    constexpr int ROW = 3 * D1;
-    for (int it = t; it < nel * DD * ROW; it += NT) {
-      const int el = it / (DD * ROW), rem = it - el * (DD * ROW);
-      const int row = rem / ROW, sidx = rem - row * ROW;
-      const int dz = row / D1, dy = row - dz * D1, dx = sidx / 3, c = sidx - dx * 3;
-      const long long e = e0 + el;
-      long long n;
-      if (a.brick) {
-        const unsigned ue = (unsigned)e;
-        const unsigned ez = a.b.fnxy.div(ue);
-        const unsigned r2 = ue - ez * (unsigned)(a.b.nx * a.b.ny);
-        const unsigned ey = a.b.fnx.div(r2), ex = r2 - ey * (unsigned)a.b.nx;
-        n = (long long)(ex * P + dx) + (long long)(ey * P + dy) * a.b.Nx + (long long)(ez * P + dz) * a.b.NxNy;
-      } else {
-        n = __ldg(a.emap + e * NL + row * D1 + dx);
+    // gather x node rows -> G image (aliases the T image of the previous pass); every
+    // load of the thread is issued before the first shared store
+    constexpr int ROW = 3 * D1, GI = EPC * DD * ROW, GU = (GI + NT - 1) / NT;
+    {
+      double xv[GU];
+      int so[GU];
+#pragma unroll
+      for (int u = 0; u < GU; ++u) {
+        const int it = t + u * NT;
+        so[u] = -1;
+        if (it < nel * DD * ROW) {
+          const int el = it / (DD * ROW), rem = it - el * (DD * ROW);
+          const int row = rem / ROW, sidx = rem - row * ROW;
+          const int dz = row / D1, dy = row - dz * D1, dx = sidx / 3, c = sidx - dx * 3;
+          const long long e = e0 + el;
+          long long n;
+          if (a.brick) {
+            const unsigned ue = (unsigned)e;
+            const unsigned ez = a.b.fnxy.div(ue);
+            const unsigned r2 = ue - ez * (unsigned)(a.b.nx * a.b.ny);
+            const unsigned ey = a.b.fnx.div(r2), ex = r2 - ey * (unsigned)a.b.nx;
+            n = (long long)(ex * P + dx) + (long long)(ey * P + dy) * a.b.Nx + (long long)(ez * P + dz) * a.b.NxNy;
+          } else {
+            n = __ldg(a.emap + e * NL + row * D1 + dx);
+          }
+          xv[u] = __ldg(a.x + n * 3 + c);
+          so[u] = el * PER + XS + (c * D1 + dz) * GP + dy * D1 + dx;
+        }
       }
-      smem[el * PER + XS + (c * D1 + dz) * GP + dy * D1 + dx] = __ldg(a.x + n * 3 + c);
+#pragma unroll
+      for (int u = 0; u < GU; ++u)
+        if (so[u] >= 0) smem[so[u]] = xv[u];
     }
     __syncthreads();
     // x stage, thread per (c, dz, dy) row
