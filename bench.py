@@ -75,6 +75,38 @@ def algorithmic_bytes(d, p, ne, nn, layout="brick"):
     }
 
 
+def algorithmic_flops(d, p, ne):
+    """Per-launch algorithmic fp64 flops (2 per multiply-add) of the contraction kernels.
+
+    Sum-factorised contractions as the kernels perform them; the
+    point physics of the rates kernel (EOS, viscosity, D_F, det J^-1) is not counted, so
+    the rates figure is a lower bound."""
+    if d != 3:
+        return {}
+    D1, Q, Dt = p + 1, p + 2, max(p, 1)
+    nq, nt = Q ** 3, Dt ** 3
+    sf = Q * D1 ** 3 + Q ** 2 * D1 ** 2 + Q ** 3 * D1  # one 3D interpolation (MACs)
+    rates = (6 * D1 * D1 * Q * D1 * 2 + Dt * Dt * Q * Dt          # x stage (B, G) + thermo
+             + 6 * D1 * Q * Q * D1 * 3 + Dt * Q * Q * Dt          # y stage (BB, GB, BG) + thermo
+             + nq * (6 * D1 * 3 + 3 * D1 + Dt)                    # z stage: grads, v, e at points
+             + 3 * Q * Q * Q * D1 * 3 + Q * Q * Q * Dt            # transposed z
+             + 3 * D1 * Q * Q * D1 * 3 + Dt * Q * Q * Dt          # transposed y
+             + 3 * D1 * D1 * D1 * Q * 2 + Dt * Dt * Dt * Q        # transposed x
+             + nt * nt)                                           # M_e^-1 matvec
+    valid = 3 * D1 * D1 * Q * D1 * 2 + 3 * D1 * Q * Q * D1 * 3 + nq * 3 * D1 * 3
+    return {"mass_cg": 2 * d * (2 * sf + nq) * ne, "rates": 2 * rates * ne, "validity": 2 * valid * ne}
+
+
+def fp64_peak(lib):
+    """Live fp64 FMA peak of this device (hx_fp64_peak), TFLOP/s."""
+    import ctypes
+
+    v = ctypes.c_double(0.0)
+    if lib.hx_fp64_peak(ctypes.byref(v)) != 0:
+        return None
+    return v.value
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -464,19 +496,29 @@ def main():
     layout = hy._ctx.layout()
     ab = algorithmic_bytes(d, p, mesh.num_elements, mesh.num_nodes, layout)
     traffic = ncu_traffic()
+    af = algorithmic_flops(d, p, mesh.num_elements)
+    f64pk = fp64_peak(lib) if rank == 0 else None
     kern = {}
     for name, (tot, cnt) in ktimes.items():
         avg_s = tot / cnt / 1e3
         kb = ab.get(name)
         kern[name] = {"launches": cnt, "avg_us": avg_s * 1e6, "share": tot / max(prof_ms, 1e-30),
-                      "alg_bytes": kb, "gbs": (kb / avg_s / 1e9) if kb else None}
+                      "alg_bytes": kb, "gbs": (kb / avg_s / 1e9) if kb else None,
+                      "hbm_frac": (kb / avg_s / 1e9 / pk) if kb else None}
+        if name in af:
+            tf = af[name] / avg_s / 1e12
+            kern[name].update({"alg_flops": af[name], "fp64_tflops": tf,
+                               "fp64_frac": (tf / f64pk) if f64pk else None})
     dom = max(kern, key=lambda k: ktimes[k][0]) if kern else None
     roof = None
     if dom:
         ach = kern[dom]["gbs"]
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": pk, "unit": "GB/s",
                 "frac": ach / pk if ach else None, "traffic": traffic.get(dom), "peak_source": pk_src,
-                "alg_bytes_per_launch": kern[dom]["alg_bytes"]}
+                "alg_bytes_per_launch": kern[dom]["alg_bytes"],
+                "fp64": {"achieved": kern[dom].get("fp64_tflops"), "peak": f64pk, "unit": "TFLOP/s",
+                         "frac": kern[dom].get("fp64_frac"), "alg_flops_per_launch": kern[dom].get("alg_flops"),
+                         "peak_source": "measured live (hx_fp64_peak: DFMA chains, full occupancy)"}}
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None

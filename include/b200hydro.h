@@ -229,6 +229,10 @@ int hx_energies(hx_ctx* ctx, const double* v, const double* e, const double* qda
 int hx_prof_enable(hx_ctx* ctx, int on);
 int hx_prof_read(hx_ctx* ctx, int kclass, double* total_ms, int64_t* count);
 int hx_prof_reset(hx_ctx* ctx);
+/* Diagnostic (no reference counterpart): fp64 FMA peak of the current device, measured
+ * with independent DFMA chains at full occupancy (best of 5 CUDA-event-timed launches);
+ * the denominator of the fp64 roofline fractions bench.py reports. */
+int hx_fp64_peak(double* tflops);
 
 /* ---- multi-GPU (domain decomposition; the reference's P = identity) -- */
 

@@ -97,6 +97,7 @@ _SIGS = {
     "hx_prof_enable": (C.c_int, [P, C.c_int]),
     "hx_prof_read": (C.c_int, [P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "hx_prof_reset": (C.c_int, [P]),
+    "hx_fp64_peak": (C.c_int, [C.POINTER(C.c_double)]),
     "hx_comm_init": (C.c_int, [P, P, C.c_int, C.c_int, C.c_int, P, P, P, P]),
     "hx_comm_active": (C.c_int, [P]),
 }

@@ -1845,6 +1845,57 @@ extern "C" int hx_comm_active(hx_ctx*) { return 0; }
 // ---------------------------------------------------------------------------
 // live kernel timing
 
+// fp64 FMA peak probe: 8 independent DFMA chains per thread, full occupancy
+__global__ void __launch_bounds__(256) k_fp64_probe(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) x[c] = threadIdx.x * 1e-3 + c;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[c] = fma(x[c], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += x[c];
+  if (s == 12345.678) out[threadIdx.x] = s;  // keeps the chains live
+}
+
+extern "C" int hx_fp64_peak(double* tflops) {
+  if (!tflops) return HX_EINVAL;
+  int dev = 0, sms = 0, occ = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return HX_ECUDA;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fp64_probe, 256, 0);
+  double* out = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int rc = HX_OK;
+  const unsigned blocks = (unsigned)(sms * occ);
+  const int iters = 20000;
+  float best = 1e30f;
+  if (cudaMalloc(&out, 256 * sizeof(double)) != cudaSuccess || cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+    rc = HX_ECUDA;
+  } else {
+    k_fp64_probe<<<blocks, 256, 0, st>>>(out, 100, 0.999999, 1e-7);
+    for (int r = 0; r < 5 && rc == HX_OK; ++r) {
+      cudaEventRecord(e0, st);
+      k_fp64_probe<<<blocks, 256, 0, st>>>(out, iters, 0.999999, 1e-7);
+      cudaEventRecord(e1, st);
+      if (cudaEventSynchronize(e1) != cudaSuccess) rc = HX_ECUDA;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (ms > 0.f && ms < best) best = ms;
+    }
+  }
+  if (rc == HX_OK) *tflops = 2.0 * (double)blocks * 256.0 * iters * 8.0 / (best * 1e-3) / 1e12;
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (st) cudaStreamDestroy(st);
+  if (out) cudaFree(out);
+  return rc;
+}
+
 extern "C" int hx_prof_enable(hx_ctx* ctx, int on) {
   if (!ctx) return HX_EINVAL;
   CK(cudaSetDevice(ctx->device));

@@ -18,7 +18,9 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_fp64_cycles_ac
 def details(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    name = rows[1][4] if len(rows) > 1 else "?"
+    if len(rows) < 2 or len(rows[1]) < 5:
+        return None, {}
+    name = rows[1][4]
     d = {}
     for r in rows[1:]:
         if len(r) > 14 and r[12] in KEYS and r[12] not in d:
@@ -37,7 +39,8 @@ def launches(path):
     rows = list(csv.reader(open(path)))
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in rows:
-        if len(r) > 14 and r[-3] == "gpu__time_duration.sum":
+        # k_fp64_probe: bench.py's live fp64-peak measurement, not part of the step
+        if len(r) > 14 and r[-3] == "gpu__time_duration.sum" and "k_fp64_probe" not in r[4]:
             agg[r[4][:70]][0] += 1
             agg[r[4][:70]][1] += float(r[-1])
     return agg
@@ -54,6 +57,9 @@ def main():
     lines = []
     for rep in args:
         name, d = details(rep)
+        if name is None:
+            lines.append(f"### ({rep.split('/')[-1]}: empty capture)\n")
+            continue
         lines.append(f"### `{name}`  ({rep.split('/')[-1]})\n")
         lines.append("| metric | value | unit |\n|---|---|---|")
         for k in KEYS + RAW:
