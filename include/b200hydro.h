@@ -40,7 +40,7 @@ enum {
   HX_ECG_BREAKDOWN = 3, /* CGError "p^T A p <= 0" (operators.py:354-355) */
   HX_ECG_MAXITER = 4,   /* CGError "did not converge" (operators.py:366) */
   HX_ECUDA = 5,         /* CUDA runtime error */
-  HX_ENCCL = 6,         /* NCCL error */
+  HX_ENCCL = 6,         /* multi-GPU exchange error (a peer stopped answering) */
   HX_EUNDERFLOW = 7     /* TimestepUnderflow (hydro.py:82-83, 369-372, 405) */
 };
 
@@ -236,12 +236,37 @@ int hx_fp64_peak(double* tflops);
 
 /* ---- multi-GPU (domain decomposition; the reference's P = identity) -- */
 
-/* Shared-node halo plan for this rank's subdomain: for each neighbour rank, the
- * local node ids shared with it (sorted by global id).  Halo sums use NCCL
- * grouped send/recv; scalar reductions use ncclAllReduce.  nccl_id: 128 bytes. */
-int hx_comm_init(hx_ctx* ctx, const void* nccl_id, int rank, int nranks, int n_neighbors,
-                 const int32_t* neighbor_ranks_host, const int64_t* offsets_host,
-                 const int32_t* shared_nodes_host, const uint8_t* owned_host);
+/* Device-resident exchange of the momentum CG (hx_mass_cg) over peer memory, one
+ * brick subdomain per rank (paper_2112_07075_b200/partition.py).  Each rank owns a
+ * MAILBOX (flags, scalar slots, halo receive blocks) that every rank maps; inside the
+ * CG the interface-node sums and the p.Ap / r.z world sums move by P2P stores plus
+ * release/acquire sequence flags (no host round trip, no NCCL call in the loop), summed
+ * in ascending rank order so all sharers hold identical values.  Replaces the P operator
+ * the reference leaves as identity inside cg_solve (operators.py:333-366).
+ *   snode/sdst/sidx (nsh): for every (shared node, neighbour) pair, the local node, the
+ *     neighbour rank and the node's index in the list of nodes the two ranks share
+ *     (sorted by global id: the same index on both sides), < maxh;
+ *   hnode (nh), hoff (nh+1), hsrc: interface nodes and their sharers in ascending rank,
+ *     -1 = this rank, else (rank << 24) | index;
+ *   nbr (nnbr): neighbour ranks; owned (NN host bytes): 1 where this rank owns the node;
+ *   maxh: the same on every rank (max shared-list length over all rank pairs).
+ * hx_peer_setup allocates the mailbox and returns its device pointer; hx_peer_connect
+ * takes every rank's mailbox pointer in this address space (hx_peer_ipc_open for other
+ * processes, the pointer itself for ranks sharing a process).  All ranks must then run
+ * the same sequence of hx_mass_cg calls concurrently. */
+int hx_peer_setup(hx_ctx* ctx, int rank, int nranks, int maxh, int nsh, const int32_t* snode,
+                  const int32_t* sdst, const int32_t* sidx, int nh, const int32_t* hnode,
+                  const int32_t* hoff, const int32_t* hsrc, int nnbr, const int32_t* nbr,
+                  const uint8_t* owned, void** mailbox);
+int hx_peer_connect(hx_ctx* ctx, void* const* mailboxes);
+/* CUDA IPC export / import of a mailbox (64-byte handle) for ranks in other processes. */
+int hx_peer_ipc_handle(const void* mailbox, void* handle_out);
+int hx_peer_ipc_open(const void* handle, void** ptr_out);
+int hx_peer_ipc_close(void* ptr);
+/* Diagnostic: out[0] = exchange counter, out[1] = timeout flag, out[2 + q] = last
+ * sequence number rank q posted to this rank (2 + 64 values). */
+int hx_peer_state(hx_ctx* ctx, uint64_t* out);
+/* 1 once hx_peer_connect succeeded. */
 int hx_comm_active(hx_ctx* ctx);
 
 #ifdef __cplusplus

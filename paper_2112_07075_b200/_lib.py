@@ -98,7 +98,13 @@ _SIGS = {
     "hx_prof_read": (C.c_int, [P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "hx_prof_reset": (C.c_int, [P]),
     "hx_fp64_peak": (C.c_int, [C.POINTER(C.c_double)]),
-    "hx_comm_init": (C.c_int, [P, P, C.c_int, C.c_int, C.c_int, P, P, P, P]),
+    "hx_peer_setup": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P, C.c_int, P, P, P, C.c_int, P, P,
+                                C.POINTER(C.c_void_p)]),
+    "hx_peer_connect": (C.c_int, [P, P]),
+    "hx_peer_ipc_handle": (C.c_int, [P, P]),
+    "hx_peer_ipc_open": (C.c_int, [P, C.POINTER(C.c_void_p)]),
+    "hx_peer_ipc_close": (C.c_int, [P]),
+    "hx_peer_state": (C.c_int, [P, P]),
     "hx_comm_active": (C.c_int, [P]),
 }
 

@@ -22,6 +22,7 @@
 #include "hx_brick.cuh"
 #include "hx_rates.cuh"
 #include "hx_remap.cuh"
+#include "hx_peer.cuh"
 
 using namespace hx;
 
@@ -96,6 +97,13 @@ struct hx_ctx {
   double* h_t = nullptr;
   // host-buffer entry scratch (device state)
   double *hx_x = nullptr, *hx_v = nullptr, *hx_e = nullptr, *hx_xo = nullptr, *hx_vo = nullptr, *hx_eo = nullptr;
+  // multi-GPU exchange (hx_peer_*): plan arrays + own mailbox; active once connected
+  bool peer = false;
+  PeerDev pd{};
+  double* mailbox = nullptr;
+  int* peer_plan = nullptr;      // snode|sdst|sidx|hnode|hoff|hsrc (one allocation)
+  uint8_t* peer_owned = nullptr;
+  unsigned long long* peer_ctr = nullptr;  // [0] seq, [1] err (as int)
 };
 
 struct hx_mass {
@@ -774,6 +782,10 @@ extern "C" int hx_destroy(hx_ctx* ctx) {
   if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
   if (ctx->gstream2) cudaStreamDestroy(ctx->gstream2);
   for (auto& e : ctx->prof_ev) cudaEventDestroy(e);
+  if (ctx->mailbox) cudaFree(ctx->mailbox);
+  if (ctx->peer_plan) cudaFree(ctx->peer_plan);
+  if (ctx->peer_owned) cudaFree(ctx->peer_owned);
+  if (ctx->peer_ctr) cudaFree(ctx->peer_ctr);
   delete ctx;
   return HX_OK;
 }
@@ -1062,6 +1074,7 @@ static int cg_prepare(hx_ctx* ctx, CGDev* cg, const double* D, const double* rhs
   na.negate = negate;
   na.tol = rel_tol;
   na.max_iter = max_iter;
+  na.owned = ctx->peer ? ctx->peer_owned : nullptr;
   MassArgs& ma = L.ma;
   ma = MassArgs{};
   ma.x = ctx->z;
@@ -1084,11 +1097,43 @@ static int cg_prepare(hx_ctx* ctx, CGDev* cg, const double* D, const double* rhs
   return HX_OK;
 }
 
+// multi-GPU: world sum of a CG launch's partials (k_peer_sync), see hx_peer.cuh
+template <int NV>
+static int peer_sync(hx_ctx* ctx, CGDev* g, double* parts, int* nparts) {
+  k_peer_sync<NV><<<1, 256, 0, ctx->stream>>>(ctx->pd, g, parts, nparts);
+  CKL();
+  return HX_OK;
+}
+
+// multi-GPU halo of the E-vector's interface nodes + world p.Ap (after a mass launch)
+static int peer_halo(hx_ctx* ctx, CGLaunch& L) {
+  const unsigned gp = std::max(1u, std::min<unsigned>(gblocks((long long)ctx->pd.nsh * L.nc, 256), 592));
+  const unsigned gc = std::max(1u, std::min<unsigned>(gblocks((long long)ctx->pd.nh * L.nc, 256), 592));
+  int rc = with_node_sum(ctx, L.nc, ctx->evec, [&](auto sum, auto ncc) {
+    k_halo_pack<decltype(ncc)::value><<<gp, 256, 0, ctx->stream>>>(ctx->pd, L.na.cg, sum);
+    return HX_OK;
+  });
+  if (rc) return rc;
+  CKL();
+  rc = peer_sync<1>(ctx, L.na.cg, L.na.pm, &L.na.cg->nparts_m);
+  if (rc) return rc;
+  rc = with_node_sum(ctx, L.nc, ctx->evec, [&](auto sum, auto ncc) {
+    k_halo_combine<decltype(ncc)::value><<<gc, 256, 0, ctx->stream>>>(ctx->pd, L.na.cg, sum);
+    return HX_OK;
+  });
+  CKL();
+  return rc;
+}
+
 static int cg_launch_init(hx_ctx* ctx, CGLaunch& L) {
   int rc = with_node_sum(ctx, L.nc, L.na.evec, [&](auto sum, auto ncc) {
     return launch_cg_nodes<decltype(ncc)::value>(ctx, L.na, sum, true);
   });
   if (rc) return rc;
+  if (ctx->peer) {  // world (r.z, nnz(b)) before M(1) finishes the reduction
+    rc = peer_sync<2>(ctx, L.na.cg, L.na.partials, &L.na.cg->nparts_n);
+    if (rc) return rc;
+  }
   L.na.evec = ctx->evec;
   L.na.rhs = nullptr;
   return HX_OK;
@@ -1097,9 +1142,15 @@ static int cg_launch_init(hx_ctx* ctx, CGLaunch& L) {
 static int cg_launch_iter(hx_ctx* ctx, CGLaunch& L) {
   int rc = ctx->brick ? mass_brick(ctx, L.nc, L.mb) : dispatch<LaunchMass>(ctx, L.nc, true, L.ma);
   if (rc) return rc;
-  return with_node_sum(ctx, L.nc, ctx->evec, [&](auto sum, auto ncc) {
+  if (ctx->peer) {
+    rc = peer_halo(ctx, L);
+    if (rc) return rc;
+  }
+  rc = with_node_sum(ctx, L.nc, ctx->evec, [&](auto sum, auto ncc) {
     return launch_cg_nodes<decltype(ncc)::value>(ctx, L.na, sum, false);
   });
+  if (rc || !ctx->peer) return rc;
+  return peer_sync<1>(ctx, L.na.cg, L.na.partials, &L.na.cg->nparts_n);  // world r.z before M(k+1)
 }
 
 static int cg_launch_finish(hx_ctx* ctx, CGLaunch& L) {
@@ -1112,7 +1163,7 @@ static int cg_launch_finish(hx_ctx* ctx, CGLaunch& L) {
 
 static void cg_info_from(const CGDev& g, hx_cg_info* info) {
   if (!info) return;
-  info->code = g.code == 0 ? HX_OK : (g.code == 3 ? HX_ECG_BREAKDOWN : HX_ECG_MAXITER);
+  info->code = g.code == 0 ? HX_OK : (g.code == 3 ? HX_ECG_BREAKDOWN : (g.code == 6 ? HX_ENCCL : HX_ECG_MAXITER));
   info->iterations = g.iters;
   info->n_residuals = g.nres;
 }
@@ -1833,14 +1884,138 @@ extern "C" int hx_energies(hx_ctx* ctx, const double* v, const double* e, const 
 }
 
 // ---------------------------------------------------------------------------
-// multi-GPU: not yet wired in this build (the Python layer partitions and
-// exchanges through torch.distributed); reported inactive.
+// ---------------------------------------------------------------------------
+// multi-GPU exchange over peer memory (hx_peer.cuh)
 
-extern "C" int hx_comm_init(hx_ctx* ctx, const void*, int, int, int, const int32_t*, const int64_t*, const int32_t*,
-                            const uint8_t*) {
-  return fail(ctx, HX_EINVAL, "hx_comm_init: device-side NCCL halo not built in this version");
+static constexpr size_t mailbox_doubles(int maxh) { return (size_t)MB_RECV + (size_t)HX_MAXR * maxh * 3; }
+
+extern "C" int hx_peer_setup(hx_ctx* ctx, int rank, int nranks, int maxh, int nsh, const int32_t* snode,
+                             const int32_t* sdst, const int32_t* sidx, int nh, const int32_t* hnode,
+                             const int32_t* hoff, const int32_t* hsrc, int nnbr, const int32_t* nbr,
+                             const uint8_t* owned, void** mailbox) {
+  if (!ctx || !mailbox || nranks < 1 || nranks > HX_MAXR || rank < 0 || rank >= nranks || maxh < 0 || nsh < 0 ||
+      nh < 0 || nnbr < 0 || nnbr > HX_MAXR || !owned || (nsh && (!snode || !sdst || !sidx)) ||
+      (nh && (!hnode || !hoff || !hsrc)) || (nnbr && !nbr))
+    return fail(ctx, HX_EINVAL, "hx_peer_setup: bad arguments");
+  if (maxh >= (1 << 24)) return fail(ctx, HX_EINVAL, "hx_peer_setup: halo too large");
+  CK(cudaSetDevice(ctx->device));
+  const long long nhs = nh ? hoff[nh] : 0;
+  for (int j = 0; j < nsh; ++j)
+    if (sdst[j] < 0 || sdst[j] >= nranks || sidx[j] < 0 || sidx[j] >= maxh || snode[j] < 0 || snode[j] >= ctx->nn)
+      return fail(ctx, HX_EINVAL, "hx_peer_setup: shared entry %d out of range", j);
+  for (int h = 0; h < nh; ++h)
+    if (hnode[h] < 0 || hnode[h] >= ctx->nn || hoff[h + 1] < hoff[h])
+      return fail(ctx, HX_EINVAL, "hx_peer_setup: interface node %d out of range", h);
+  for (long long s = 0; s < nhs; ++s)
+    if (hsrc[s] >= 0 && ((hsrc[s] >> 24) >= nranks || (hsrc[s] & 0xffffff) >= maxh))
+      return fail(ctx, HX_EINVAL, "hx_peer_setup: sharer entry %lld out of range", s);
+  if (ctx->mailbox) cudaFree(ctx->mailbox);
+  if (ctx->peer_plan) cudaFree(ctx->peer_plan);
+  if (ctx->peer_owned) cudaFree(ctx->peer_owned);
+  if (ctx->peer_ctr) cudaFree(ctx->peer_ctr);
+  ctx->mailbox = nullptr;
+  ctx->peer_plan = nullptr;
+  ctx->peer_owned = nullptr;
+  ctx->peer_ctr = nullptr;
+  ctx->peer = false;
+  const size_t nmb = mailbox_doubles(maxh);
+  CK(dalloc(&ctx->mailbox, nmb));
+  CK(cudaMemset(ctx->mailbox, 0, nmb * sizeof(double)));
+  const size_t nplan = 3 * (size_t)nsh + (size_t)nh + (size_t)nh + 1 + (size_t)nhs;
+  std::vector<int> plan(std::max<size_t>(nplan, 1));
+  size_t o = 0;
+  for (int j = 0; j < nsh; ++j) plan[o + j] = snode[j];
+  o += nsh;
+  for (int j = 0; j < nsh; ++j) plan[o + j] = sdst[j];
+  o += nsh;
+  for (int j = 0; j < nsh; ++j) plan[o + j] = sidx[j];
+  o += nsh;
+  for (int h = 0; h < nh; ++h) plan[o + h] = hnode[h];
+  o += nh;
+  for (int h = 0; h <= nh; ++h) plan[o + h] = nh ? hoff[h] : 0;
+  o += nh + 1;
+  for (long long q = 0; q < nhs; ++q) plan[o + q] = hsrc[q];
+  CK(dalloc(&ctx->peer_plan, plan.size()));
+  CK(cudaMemcpy(ctx->peer_plan, plan.data(), plan.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(dalloc(&ctx->peer_owned, (size_t)ctx->nn));
+  CK(cudaMemcpy(ctx->peer_owned, owned, (size_t)ctx->nn, cudaMemcpyHostToDevice));
+  CK(dalloc(&ctx->peer_ctr, 2));
+  CK(cudaMemset(ctx->peer_ctr, 0, 2 * sizeof(unsigned long long)));
+  PeerDev& pd = ctx->pd;
+  pd = PeerDev{};
+  pd.rank = rank;
+  pd.nranks = nranks;
+  pd.maxh = maxh;
+  pd.nsh = nsh;
+  pd.nh = nh;
+  pd.nnbr = nnbr;
+  pd.seq = ctx->peer_ctr;
+  pd.err = reinterpret_cast<int*>(ctx->peer_ctr + 1);
+  for (int q = 0; q < nnbr; ++q) pd.nbr[q] = nbr[q];
+  const int* P = ctx->peer_plan;
+  pd.snode = P;
+  pd.sdst = P + nsh;
+  pd.sidx = P + 2 * nsh;
+  pd.hnode = P + 3 * nsh;
+  pd.hoff = P + 3 * nsh + nh;
+  pd.hsrc = P + 3 * nsh + 2 * nh + 1;
+  pd.owned = ctx->peer_owned;
+  *mailbox = ctx->mailbox;
+  return HX_OK;
 }
-extern "C" int hx_comm_active(hx_ctx*) { return 0; }
+
+extern "C" int hx_peer_connect(hx_ctx* ctx, void* const* mailboxes) {
+  if (!ctx || !mailboxes || !ctx->mailbox) return fail(ctx, HX_EINVAL, "hx_peer_connect: call hx_peer_setup first");
+  for (int q = 0; q < ctx->pd.nranks; ++q) {
+    if (!mailboxes[q] && q != ctx->pd.rank) return fail(ctx, HX_EINVAL, "hx_peer_connect: mailbox of rank %d missing", q);
+    ctx->pd.mb[q] = q == ctx->pd.rank ? ctx->mailbox : static_cast<double*>(mailboxes[q]);
+  }
+  // load the exchange kernels now: with lazy module loading a first launch may wait for
+  // the context's running kernels -- a peer's spin-wait when ranks share a process
+  for (int nc = 1; nc <= 3; ++nc) {
+    int rc = with_node_sum(ctx, nc, ctx->evec, [&](auto sum, auto ncc) -> int {
+      cudaFuncAttributes fa;
+      CK(cudaFuncGetAttributes(&fa, k_halo_pack<decltype(ncc)::value, decltype(sum)>));
+      CK(cudaFuncGetAttributes(&fa, k_halo_combine<decltype(ncc)::value, decltype(sum)>));
+      return HX_OK;
+    });
+    if (rc) return rc;
+  }
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, k_peer_sync<1>));
+  CK(cudaFuncGetAttributes(&fa, k_peer_sync<2>));
+  ctx->peer = true;
+  return HX_OK;
+}
+
+extern "C" int hx_peer_ipc_handle(const void* mailbox, void* handle_out) {
+  if (!mailbox || !handle_out) return HX_EINVAL;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, const_cast<void*>(mailbox)) != cudaSuccess) return HX_ECUDA;
+  memcpy(handle_out, &h, sizeof h);
+  return HX_OK;
+}
+
+extern "C" int hx_peer_ipc_open(const void* handle, void** ptr_out) {
+  if (!handle || !ptr_out) return HX_EINVAL;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  if (cudaIpcOpenMemHandle(ptr_out, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return HX_ECUDA;
+  return HX_OK;
+}
+
+extern "C" int hx_peer_ipc_close(void* ptr) {
+  return cudaIpcCloseMemHandle(ptr) == cudaSuccess ? HX_OK : HX_ECUDA;
+}
+
+extern "C" int hx_comm_active(hx_ctx* ctx) { return ctx && ctx->peer ? 1 : 0; }
+
+extern "C" int hx_peer_state(hx_ctx* ctx, uint64_t* out) {
+  if (!ctx || !out || !ctx->mailbox) return HX_EINVAL;
+  CK(cudaMemcpy(out, ctx->peer_ctr, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out + 2, ctx->mailbox, HX_MAXR * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return HX_OK;
+}
 
 // ---------------------------------------------------------------------------
 // live kernel timing

@@ -91,6 +91,29 @@ struct BrickSum {
     for (int q = 0; q < 8; ++q) s += v[q];  // absent entries are +0.0: sums unchanged
     return s;
   }
+  // make the node's sum equal `total` (multi-GPU halo): the lowest element's entry takes
+  // the total, the others become +0.0, so operator() returns exactly `total` afterwards
+  __device__ __forceinline__ void patch(long long n, int c, double total) const {
+    constexpr int D1 = P + 1, NL = D1 * D1 * D1;
+    const unsigned k = b.fNxNy.div((unsigned)n);
+    const unsigned rem = (unsigned)n - k * (unsigned)b.NxNy;
+    const unsigned j = b.fNx.div(rem);
+    const int i = (int)(rem - j * (unsigned)b.Nx);
+    int ex, lx, tx, ey, ly, ty, ez, lz, tz;
+    axis_first<P>(i, b.nx, ex, lx, tx);
+    axis_first<P>((int)j, b.ny, ey, ly, ty);
+    axis_first<P>((int)k, b.nz, ez, lz, tz);
+    const unsigned p0 = ((unsigned)((ez * b.ny + ey) * b.nx + ex) * NL + (lz * D1 + ly) * D1 + lx) * NC + c;
+    double* W = const_cast<double*>(E);
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+          if (a <= tz && bb <= ty && g <= tx)
+            W[p0 + (unsigned)((a * b.dZ + bb * b.dY + g * b.dX) * NC)] = (a | bb | g) ? 0.0 : total;
+  }
 };
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
@@ -118,6 +141,11 @@ struct CsrSum {
   const int* off;
   const double* E;
   __device__ __forceinline__ double operator()(long long n, int c) const { return node_sum1<NC>(off, E, n, c); }
+  __device__ __forceinline__ void patch(long long n, int c, double total) const {
+    double* W = const_cast<double*>(E);
+    const int b = off[n], f = off[n + 1];
+    for (int k = b; k < f; ++k) W[(long long)k * NC + c] = k == b ? total : 0.0;
+  }
 };
 
 // ---------------------------------------------------------------------------

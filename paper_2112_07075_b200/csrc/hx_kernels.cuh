@@ -987,6 +987,7 @@ struct NodeArgs {
   int max_iter;
   unsigned long long cond;
   int use_cond;
+  const uint8_t* owned;  // multi-GPU: r.z counts a node on its owning rank only (null: every node)
 };
 
 // plain scatter: out = G^T evec (internal layout)
@@ -1036,7 +1037,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_init(NodeArgs a, SUM sum) {
         a.r[j] = b;
         reinterpret_cast<double2*>(a.pbuf0)[j] = make_double2(z, 0.0);  // (z_0, p_0 = 0)
         a.x[j] = 0.0;
-        rz = fma(b, z, rz);
+        if (!a.owned || a.owned[j / NC]) rz = fma(b, z, rz);
         if (b != 0.0 || b != b) nz += 1.0;
       }
     }
@@ -1123,7 +1124,7 @@ __global__ void __launch_bounds__(256, NODE_MINB) k_cg_node(NodeArgs a, SUM sum)
         a.r[j] = r;
         const double z = __dmul_rn(dj[u], r);
         reinterpret_cast<double2*>(pn)[j] = make_double2(z, p);
-        rz = fma(r, z, rz);
+        if (!a.owned || a.owned[j / NC]) rz = fma(r, z, rz);
       }
     }
   }

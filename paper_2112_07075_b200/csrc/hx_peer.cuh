@@ -1,0 +1,164 @@
+// hx_peer.cuh -- device-resident exchange of the multi-GPU momentum CG over peer memory.
+//
+// The mesh is split into bricks, one per rank (paper_2112_07075_b200/partition.py; the
+// paper's P operator, identity in the reference).  Inside the CG
+// (cg_solve operators.py:333-366 on the PA mass) two things cross subdomains:
+//   * the H1 node sums at interface nodes (halo): every sharer needs the sum of all
+//     ranks' element contributions;
+//   * the scalars p.Ap and r.z (and r.z, nnz(b) at the start): world sums.
+// Both move through a per-rank MAILBOX in device memory that every rank maps (CUDA IPC
+// across processes over NVLink, plain pointers when several ranks share a process):
+//   [flag[src] u64 x HX_MAXR | slot[parity][src][2] doubles | recv[src][maxh][nc] doubles]
+// A sender writes its data straight into the receivers' mailboxes (P2P stores), then
+// publishes a sequence number with a system-scope release store; a receiver spins on
+// its own flags with acquire loads.  Sequence numbers come from a per-rank device
+// counter that every rank advances identically (all ranks run the same launches and
+// take the same CG decisions, because they see the same world scalars), so the whole
+// loop stays on the device: no host round trip, no NCCL call inside the iteration.
+// Combination order is fixed (ascending rank, from 0.0), so every sharer of a node
+// holds bit-identical values -- deterministic, though not bit-identical to one GPU.
+#pragma once
+
+#include "hx_brick.cuh"
+
+namespace hx {
+
+#define HX_MAXR 64
+constexpr int MB_FLAG = 0;                      // u64 flag[src]
+constexpr int MB_SLOT = HX_MAXR;                // double slot[2][HX_MAXR][2]
+constexpr int MB_RECV = HX_MAXR + 4 * HX_MAXR;  // double recv[src][maxh][nc]
+constexpr unsigned long long PEER_SPIN_LIMIT = 1ull << 25;  // ~seconds: a stuck peer ends the CG with code 6
+
+struct PeerDev {
+  int rank, nranks, maxh;
+  int nsh;                      // shared (node, neighbour) entries
+  int nh;                       // interface nodes
+  int nnbr;
+  unsigned long long* seq;      // this rank's exchange counter
+  int* err;                     // set to 1 on a peer timeout
+  double* mb[HX_MAXR];          // every rank's mailbox in this address space
+  int nbr[HX_MAXR];             // neighbour ranks
+  const int* snode;             // per shared entry: local node
+  const int* sdst;              //   destination rank
+  const int* sidx;              //   index in the destination's recv block from this rank
+  const int* hnode;             // interface nodes
+  const int* hoff;              // (nh + 1) offsets into hsrc
+  const int* hsrc;              // sharers in ascending rank: -1 = this rank, else (q << 24) | index
+  const uint8_t* owned;         // (NN) lowest-rank sharer owns a node (dot products count it once)
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long* mb_flag(double* mb, int src) {
+  return reinterpret_cast<unsigned long long*>(mb) + MB_FLAG + src;
+}
+// wait until every listed rank published seq; false on timeout
+__device__ __forceinline__ bool peer_wait(const PeerDev& pd, const int* ranks, int n, unsigned long long seq) {
+  double* me = pd.mb[pd.rank];
+  for (int j = 0; j < n; ++j) {
+    const int q = ranks ? ranks[j] : j;
+    if (q == pd.rank) continue;
+    unsigned long long spins = 0;
+    while (ld_acquire_sys(mb_flag(me, q)) < seq) {
+      __nanosleep(64);
+      if (++spins > PEER_SPIN_LIMIT) return false;
+    }
+  }
+  return true;
+}
+
+// CG world scalar: fixed-order sum of this launch's per-CTA partials (NV values each,
+// stride NV), posted to every rank; after all ranks posted, the ascending-rank sum
+// replaces partial 0 and the partial count becomes 1, so the consuming CG kernel
+// (cg_mass_begin / cg_node_begin) reads the world value unchanged.  Halo data written
+// by k_halo_pack before this launch is published by the same flag.
+template <int NV>
+__global__ void __launch_bounds__(256) k_peer_sync(PeerDev pd, CGDev* g, double* parts, int* nparts) {
+  __shared__ double red[32];
+  __shared__ int ok;
+  if (g && !g->active) return;
+  const int n = *nparts;
+  double v[NV];
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += 256) acc += __ldcg(parts + (long long)i * NV + t);
+    v[t] = block_sum<256>(acc, red);
+  }
+  if (threadIdx.x == 0) {
+    const unsigned long long seq = *pd.seq + 1;
+    *pd.seq = seq;
+    const int par = (int)(seq & 1);
+    for (int q = 0; q < pd.nranks; ++q) {
+      double* s = pd.mb[q] + MB_SLOT + (par * HX_MAXR + pd.rank) * 2;
+#pragma unroll
+      for (int t = 0; t < NV; ++t) s[t] = v[t];
+    }
+    __threadfence_system();
+    for (int q = 0; q < pd.nranks; ++q) st_release_sys(mb_flag(pd.mb[q], pd.rank), seq);
+    ok = peer_wait(pd, nullptr, pd.nranks, seq) ? 1 : 0;
+    if (ok) {
+      const double* s = pd.mb[pd.rank] + MB_SLOT + par * HX_MAXR * 2;
+#pragma unroll
+      for (int t = 0; t < NV; ++t) {
+        double tot = 0.0;
+        for (int q = 0; q < pd.nranks; ++q) tot += __ldcg(s + q * 2 + t);
+        parts[t] = tot;
+      }
+      *nparts = 1;
+    } else {
+      *pd.err = 1;
+      if (g) {
+        g->code = 6;
+        g->active = 0;
+        cg_publish(g);
+      }
+    }
+  }
+}
+
+// halo, part 1: this rank's node sums at the nodes it shares, stored into each
+// neighbour's recv block (published by the following k_peer_sync)
+template <int NC, class SUM>
+__global__ void __launch_bounds__(256) k_halo_pack(PeerDev pd, const CGDev* g, SUM sum) {
+  if (g && !g->active) return;
+  const long long N = (long long)pd.nsh * NC;
+  bool wrote = false;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += (long long)gridDim.x * blockDim.x) {
+    const int e = (int)(j / NC), c = (int)(j - (long long)e * NC);
+    const int n = __ldg(pd.snode + e), q = __ldg(pd.sdst + e), i = __ldg(pd.sidx + e);
+    pd.mb[q][MB_RECV + ((long long)pd.rank * pd.maxh + i) * NC + c] = sum(n, c);
+    wrote = true;
+  }
+  if (wrote) __threadfence_system();
+}
+
+// halo, part 2 (after the flags): total = sum over the sharers in ascending rank order
+// from 0.0 (own partial from the local E-vector), written back into the E-vector so the
+// node pass's sum yields exactly the total
+template <int NC, class SUM>
+__global__ void __launch_bounds__(256) k_halo_combine(PeerDev pd, const CGDev* g, SUM sum) {
+  if (g && !g->active) return;
+  if (*pd.err) return;
+  const long long N = (long long)pd.nh * NC;
+  const double* recv = pd.mb[pd.rank] + MB_RECV;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += (long long)gridDim.x * blockDim.x) {
+    const int h = (int)(j / NC), c = (int)(j - (long long)h * NC);
+    const int n = __ldg(pd.hnode + h);
+    const double own = sum(n, c);
+    double tot = 0.0;
+    for (int s = __ldg(pd.hoff + h); s < __ldg(pd.hoff + h + 1); ++s) {
+      const int src = __ldg(pd.hsrc + s);
+      tot += src < 0 ? own : __ldcg(recv + ((long long)(src >> 24) * pd.maxh + (src & 0xffffff)) * NC + c);
+    }
+    sum.patch(n, c, tot);
+  }
+}
+
+}  // namespace hx

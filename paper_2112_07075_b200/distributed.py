@@ -20,7 +20,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-__all__ = ["Halo", "DistributedLagrange", "DeviceOps"]
+__all__ = ["Halo", "DistributedLagrange", "DeviceOps", "PeerExchange", "peer_plan", "max_shared"]
 
 
 class Halo:
@@ -130,6 +130,8 @@ class DistributedLagrange:
 
     # -- CG (cg_solve operators.py:333-366 with the wall rows of hydro.py:319-337) --
     def solve_momentum(self, rhs_v):
+        if getattr(self.ops, "peer", None) is not None:  # device-resident CG (hx_peer_*)
+            return self.ops.solve_momentum(rhs_v, self.precond, self.mask, self.tol)
         m = self.mask
         zero = torch.zeros((), dtype=torch.float64, device=self.device)
         b = torch.where(m, zero, rhs_v)
@@ -252,6 +254,14 @@ class DeviceOps:
     def energy_solve(self, rhs):
         return self.hy.solve_energy(rhs)
 
+    peer = None  # PeerExchange once connected
+
+    def solve_momentum(self, rhs, precond, mask, tol):
+        """Jacobi PCG of the whole distributed mass system on the device: interface sums
+        and world dot products move through the peer mailboxes inside the loop."""
+        x, it = self.hy.mass_pa.solve(rhs, precond_diag=precond, bc_mask=mask, rel_tol=tol, max_iter=2000)
+        return x, it
+
     def geometry_ok(self, x):
         from .fespace import InvertedElementError, compute_geometric_factors
 
@@ -260,3 +270,101 @@ class DeviceOps:
             return True
         except InvertedElementError:
             return False
+
+
+# ---------------------------------------------------------------------------
+# device-resident CG exchange (libb200hydro.so hx_peer_*, csrc/hx_peer.cuh)
+
+def max_shared(subs) -> int:
+    """Longest shared-node list over all rank pairs (the mailbox receive block size)."""
+    return max([len(ids) for s in subs for ids in s.shared.values()] + [1])
+
+
+def peer_plan(sub):
+    """Flat exchange plan of one subdomain (include/b200hydro.h, hx_peer_setup)."""
+    snode, sdst, sidx = [], [], []
+    for q in sub.neighbors:
+        ids = sub.shared[q]
+        snode.extend(int(n) for n in ids)
+        sdst.extend([q] * len(ids))
+        sidx.extend(range(len(ids)))
+    pos = {q: {int(n): i for i, n in enumerate(sub.shared[q])} for q in sub.neighbors}
+    hnode = sorted(sub.sharers)
+    hoff, hsrc = [0], []
+    for n in hnode:
+        for q in sub.sharers[n]:  # ascending rank
+            hsrc.append(-1 if q == sub.rank else (q << 24) | pos[q][n])
+        hoff.append(len(hsrc))
+    i32 = lambda a: np.ascontiguousarray(np.asarray(a, dtype=np.int32).reshape(-1))
+    return dict(snode=i32(snode), sdst=i32(sdst), sidx=i32(sidx), hnode=i32(hnode), hoff=i32(hoff),
+                hsrc=i32(hsrc), nbr=i32(sub.neighbors), owned=np.ascontiguousarray(sub.owned, dtype=np.uint8))
+
+
+class PeerExchange:
+    """Mailbox of one rank's device context; connect() maps every rank's mailbox.
+
+    Ranks in one process (tests on one GPU): connect_local([...]).  One process per GPU:
+    connect_ipc() exchanges CUDA IPC handles through torch.distributed."""
+
+    def __init__(self, ops, sub, maxh):
+        import ctypes as C
+
+        from . import _lib
+
+        from ._device import context_for
+
+        self.ops, self.sub, self.maxh = ops, sub, int(maxh)
+        self._ctx = context_for(sub.mesh, ops.quad)  # the context MassPA runs its CG in
+        lib, h = self._ctx.lib, self._ctx.h
+        self.plan = pl = peer_plan(sub)
+        ptr = lambda a: a.ctypes.data_as(C.c_void_p) if a.size else None
+        mb = C.c_void_p()
+        rc = lib.hx_peer_setup(h, sub.rank, sub.nranks, self.maxh, int(pl["snode"].size), ptr(pl["snode"]),
+                               ptr(pl["sdst"]), ptr(pl["sidx"]), int(pl["hnode"].size), ptr(pl["hnode"]),
+                               ptr(pl["hoff"]), ptr(pl["hsrc"]), int(pl["nbr"].size), ptr(pl["nbr"]),
+                               ptr(pl["owned"]), C.byref(mb))
+        self._ctx.check(rc, "hx_peer_setup")
+        self.mailbox = int(mb.value)
+        self._opened = []
+        self._C, self._lib = C, _lib
+
+    def _connect(self, ptrs):
+        C = self._C
+        arr = (C.c_void_p * len(ptrs))(*[C.c_void_p(p) for p in ptrs])
+        self._ctx.check(self._ctx.lib.hx_peer_connect(self._ctx.h, arr), "hx_peer_connect")
+        self.ops.peer = self
+
+    def _warm(self):
+        """Run one solo CG (zero right-hand side) so that every CG kernel is loaded before
+        ranks sharing a process start spinning on each other (lazy module loading)."""
+        import torch
+
+        nn, d = self.sub.mesh.num_nodes, self.sub.mesh.dim
+        z = torch.zeros((nn, d), dtype=torch.float64, device="cuda")
+        self.ops.hy.mass_pa.solve(z, precond_diag=torch.ones_like(z), bc_mask=None, rel_tol=1e-8, max_iter=8)
+        torch.cuda.synchronize()
+
+    @staticmethod
+    def connect_local(exchanges):
+        """Ranks sharing one process (and one GPU): mailboxes are plain device pointers."""
+        ptrs = [x.mailbox for x in sorted(exchanges, key=lambda x: x.sub.rank)]
+        for x in exchanges:
+            x._warm()
+            x._connect(ptrs)
+
+    def connect_ipc(self):
+        C, lib = self._C, self._ctx.lib
+        hbuf = (C.c_char * 64)()
+        self._ctx.check(lib.hx_peer_ipc_handle(C.c_void_p(self.mailbox), hbuf), "hx_peer_ipc_handle")
+        handles = [None] * self.sub.nranks
+        dist.all_gather_object(handles, bytes(hbuf))
+        ptrs = []
+        for q, hq in enumerate(handles):
+            if q == self.sub.rank:
+                ptrs.append(self.mailbox)
+                continue
+            p = C.c_void_p()
+            self._ctx.check(lib.hx_peer_ipc_open(C.create_string_buffer(hq, 64), C.byref(p)), "hx_peer_ipc_open")
+            self._opened.append(p.value)
+            ptrs.append(p.value)
+        self._connect(ptrs)

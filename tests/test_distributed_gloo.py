@@ -183,3 +183,34 @@ def test_distributed_sedov_matches_single_domain(tmp_path, name):
     assert rel(V, st["v"]) < 1e-10
     assert rel(E.reshape(-1), st["e"]) < 1e-10
     assert clamps == hy.clamps
+
+
+@pytest.mark.parametrize("d,counts,world", [(3, (4, 4, 2), 4), (3, (4, 4, 4), 8), (2, (6, 4), 2)])
+def test_peer_plan_consistent(d, counts, world):
+    """Exchange plan of the device-resident CG (distributed.peer_plan / hx_peer_setup):
+    every (node, neighbour) entry lands at an index both sides agree on, every
+    interface node lists all its sharers in ascending rank order, and exactly one rank
+    owns each global node."""
+    from paper_2112_07075_b200.distributed import max_shared, peer_plan
+    from paper_2112_07075_b200.partition import brick_partition
+
+    gm, subs = brick_partition(d, (1.0,) * d, counts, 2, world)
+    mx = max_shared(subs)
+    plans = [peer_plan(s) for s in subs]
+    owners = np.zeros(gm.num_nodes, dtype=int)
+    for s, pl in zip(subs, plans):
+        owners[s.l2g[pl["owned"].astype(bool)]] += 1
+        # sender side: entry j goes to rank sdst[j] at index sidx[j]
+        for n, q, i in zip(pl["snode"], pl["sdst"], pl["sidx"]):
+            assert 0 <= i < mx
+            assert subs[q].l2g[subs[q].shared[s.rank][i]] == s.l2g[n]
+        # receiver side: sharers ascending, -1 = self, else (q << 24) | index into q's block
+        for h, n in enumerate(pl["hnode"]):
+            srcs = pl["hsrc"][pl["hoff"][h]:pl["hoff"][h + 1]]
+            ranks = [s.rank if v < 0 else int(v) >> 24 for v in srcs]
+            assert ranks == sorted(ranks) and s.rank in ranks and len(ranks) >= 2
+            for v in srcs:
+                if v >= 0:
+                    q, i = int(v) >> 24, int(v) & 0xFFFFFF
+                    assert s.l2g[s.shared[q][i]] == s.l2g[n]
+    assert np.all(owners == 1)
