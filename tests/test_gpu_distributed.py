@@ -28,7 +28,7 @@ def _initial(case):
     return hy, hy.initial_state(*O.sedov_fns(d, case["extents"], counts)), mask
 
 
-def _worker(rank, world, port, case, out):
+def _worker(rank, world, port, case, out, peer=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
@@ -47,6 +47,10 @@ def _worker(rank, world, port, case, out):
     q0 = T(st["qdata0"][:, sub.g_elems])
     dl = DistributedLagrange(sub, DeviceOps(sub, case["gamma"], 0.5, 2.0), case["gamma"], device="cuda")
     dl.begin_phase(x, q0)
+    if peer:  # device-resident CG; mailboxes mapped across the two processes with CUDA IPC
+        from paper_2112_07075_b200.distributed import PeerExchange, max_shared
+
+        PeerExchange(dl.ops, sub, max_shared(subs)).connect_ipc()
     t, dts = 0.0, []
     for _ in range(case["steps"]):
         dt = dl.timestep_estimate(x, v, e, q0, t, case["cfl"], dt_max=1.0, t_final=10.0)
@@ -58,14 +62,15 @@ def _worker(rank, world, port, case, out):
     dist.destroy_process_group()
 
 
-def test_device_ranks_match_single_domain_oracle(tmp_path):
+@pytest.mark.parametrize("peer", [False, True], ids=["host_cg", "peer_cg"])
+def test_device_ranks_match_single_domain_oracle(tmp_path, peer):
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
     out = str(tmp_path / "res")
     world = 2
-    mp.spawn(_worker, args=(world, port, CASE, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, CASE, out, peer), nprocs=world, join=True)
     hy, st, _ = _initial(CASE)
     dts = []
     for _ in range(CASE["steps"]):
