@@ -256,9 +256,10 @@ def run_distributed(args, world, rank, local):
     import torch.distributed as dist
 
     from paper_2112_07075_b200 import problems
-    from paper_2112_07075_b200.distributed import DeviceOps, DistributedLagrange
+    from paper_2112_07075_b200.distributed import DeviceOps, DistributedLagrange, PeerExchange, max_shared
     from paper_2112_07075_b200.fespace import cartesian_mesh
-    from paper_2112_07075_b200.hydro import LagrangeHydro, MaterialModel, ViscosityModel, box_velocity_bc
+    from paper_2112_07075_b200.hydro import (HydroState, LagrangeHydro, MaterialModel, StepControls,
+                                             ViscosityModel, box_velocity_bc)
     from paper_2112_07075_b200.partition import brick_partition, rank_grid
     from paper_2112_07075_b200.tensor_basis import gauss_legendre
 
@@ -284,27 +285,36 @@ def run_distributed(args, world, rank, local):
     x, v = T(st0.x[sub.l2g]), T(st0.v[sub.l2g])
     e = T(np.asarray(st0.e).reshape(-1, nt)[sub.g_elems].reshape(-1))
     q0 = T(np.asarray(st0.qdata0)[:, sub.g_elems])
-    ops = DeviceOps(sub, 1.4, 0.5, 2.0)
-    dl = DistributedLagrange(sub, ops, 1.4, device="cuda")
-    dl.begin_phase(x, q0)
-    cg_mode = "host-driven CG (torch.distributed per iteration)"
-    if not args.host_cg:
-        # device-resident CG: interface sums + world dot products over CUDA-IPC-mapped
-        # peer mailboxes inside the loop (csrc/hx_peer.cuh)
-        from paper_2112_07075_b200.distributed import PeerExchange, max_shared
-
-        try:
-            PeerExchange(ops, sub, max_shared(subs)).connect_ipc()
-            cg_mode = "device-resident CG (peer-memory halo + world scalars, no host round trip per iteration)"
-        except Exception as exc:  # noqa: BLE001 -- reported in the JSON line
-            cg_mode = f"host-driven CG (peer mailbox setup failed: {exc})"
-    t = 0.0
+    ctl = StepControls(cfl=args.cfl, dt_max=1.0, t_final=1e9)
     V_global = d * gmesh.num_nodes
+    if args.host_cg:
+        ops = DeviceOps(sub, 1.4, 0.5, 2.0)
+        dl = DistributedLagrange(sub, ops, 1.4, device="cuda")
+        dl.begin_phase(x, q0)
+        cg_mode = "host-driven step (DistributedLagrange: torch.distributed collectives per CG iteration)"
+        t = 0.0
 
-    def step():
-        nonlocal x, v, e, t
-        dt = dl.timestep_estimate(x, v, e, q0, t, args.cfl, dt_max=1.0, t_final=1e9)
-        (x, v, e, t), _ = dl.rk2_step(x, v, e, q0, t, dt)
+        def step():
+            nonlocal x, v, e, t
+            dt = dl.timestep_estimate(x, v, e, q0, t, args.cfl, dt_max=1.0, t_final=1e9)
+            (x, v, e, t), _ = dl.rk2_step(x, v, e, q0, t, dt)
+    else:
+        # device-resident step: each rank runs the single-GPU step graph on its brick with
+        # every exchange inside (F.1 / diagonal interface sums, CG halo + world scalars,
+        # CFL / clamp / inversion status) over CUDA-IPC-mapped peer mailboxes
+        hy = LagrangeHydro(sub.mesh, gauss_legendre(p + 2), MaterialModel(1.4), ViscosityModel(0.5, 2.0),
+                           bc_mask=sub.bc_mask)
+        PeerExchange(hy, sub, max_shared(subs)).connect_ipc()
+        cur = HydroState(x, v, e, q0, 0.0)
+        hy.begin_phase(cur)
+        bufs = [(torch.empty_like(x), torch.empty_like(v), torch.empty_like(e)) for _ in range(2)]
+        cg_mode = "device-resident step graph per rank (peer-memory exchanges, one host sync per step)"
+        it = [0]
+
+        def step():
+            nonlocal cur
+            cur, _ = hy.step(cur, ctl, out=bufs[it[0] % 2])
+            it[0] += 1
 
     for _ in range(args.warmup):
         step()
@@ -322,7 +332,7 @@ def run_distributed(args, world, rank, local):
             ev1.record(stream)
             ev1.synchronize()
             tot += ev0.elapsed_time(ev1)
-    tt = torch.tensor([tot], dtype=torch.float64, device="cuda")
+    tt = torch.tensor([tot], dtype=torch.float64, device="cpu" if dist.get_backend() == "gloo" else "cuda")
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     tot = float(tt.item())
     if rank == 0:
@@ -332,8 +342,7 @@ def run_distributed(args, world, rank, local):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"3D Sedov blast Q{p}-Q{p - 1}, {n}^3 hex elements per GPU, global {counts}, "
                                    f"CFL {args.cfl}", "global_batch": V_global, "seq_len": None,
-                       "parallelism": f"domain decomposition {list(sub.grid)}: {cg_mode}; per-stage halo of "
-                                      "F.1 and CFL/inversion scalars over NCCL",
+                       "parallelism": f"domain decomposition {list(sub.grid)}: {cg_mode}",
                        "l2": "flushed before every timed step"},
             "e2e": None, "gpu_launches": None, "roofline": None, "cpu_baseline": None, "clocks": clk.summary(),
         }
@@ -347,7 +356,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=23, help="elements per direction per GPU")
+    ap.add_argument("--n", "--elems", dest="n", type=int, default=23, help="elements per direction per GPU")
     ap.add_argument("--p", type=int, default=3, help="kinematic order (Q_p - Q_{p-1})")
     ap.add_argument("--cfl", type=float, default=0.05)
     ap.add_argument("--problem", default="sedov", choices=["sedov", "tgv", "triple"])
@@ -356,7 +365,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-cg", action="store_true",
-                    help="N>1: host-driven distributed CG instead of the device-resident peer-memory CG")
+                    help="N>1: the host-driven distributed step instead of the device-resident step graph")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -371,11 +380,19 @@ def main():
 
     import torch
 
+    # HX_BENCH_ONE_GPU=1: every rank on cuda:0 with gloo host collectives -- a functional
+    # check of the N>1 path where only one GPU exists (ranks time-share it: no scaling number)
+    one_gpu = os.environ.get("HX_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     if world > 1:
         run_distributed(args, world, rank, local)

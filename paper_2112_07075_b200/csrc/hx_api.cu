@@ -1125,6 +1125,51 @@ static int peer_halo(hx_ctx* ctx, CGLaunch& L) {
   return rc;
 }
 
+// multi-GPU halo of an E-vector's interface nodes outside the CG (F.1 before the CG init)
+static int peer_evec_halo(hx_ctx* ctx, double* evec, int nc) {
+  const unsigned gp = std::max(1u, std::min<unsigned>(gblocks((long long)ctx->pd.nsh * nc, 256), 592));
+  const unsigned gc = std::max(1u, std::min<unsigned>(gblocks((long long)ctx->pd.nh * nc, 256), 592));
+  int rc = with_node_sum(ctx, nc, evec, [&](auto sum, auto ncc) {
+    k_halo_pack<decltype(ncc)::value><<<gp, 256, 0, ctx->stream>>>(ctx->pd, nullptr, sum);
+    return HX_OK;
+  });
+  if (rc) return rc;
+  CKL();
+  rc = peer_sync<0>(ctx, nullptr, nullptr, nullptr);
+  if (rc) return rc;
+  rc = with_node_sum(ctx, nc, evec, [&](auto sum, auto ncc) {
+    k_halo_combine<decltype(ncc)::value><<<gc, 256, 0, ctx->stream>>>(ctx->pd, nullptr, sum);
+    return HX_OK;
+  });
+  CKL();
+  return rc;
+}
+
+// multi-GPU world status (CFL ratio min, clamp sum, inversion) of n records
+static int peer_status(hx_ctx* ctx, StatusDev* st, int n) {
+  k_peer_status<<<1, 32, 0, ctx->stream>>>(ctx->pd, st, n);
+  CKL();
+  return HX_OK;
+}
+
+// fused rates (+ multi-GPU: world status, F.1 interface sums)
+static int rates_launch(hx_ctx* ctx, const hx_params* prm, const double* x, const double* v, const double* e,
+                        double* de, StatusDev* st) {
+  int rc = dispatch<LaunchRates>(ctx, x, v, e, ctx->evec, de, st, 0, prm->gamma, prm->q1, prm->q2);
+  if (rc || !ctx->peer) return rc;
+  rc = peer_status(ctx, st, 1);
+  if (rc) return rc;
+  return peer_evec_halo(ctx, ctx->evec, ctx->dim);
+}
+
+// geometry validity of a new state (+ multi-GPU: world inversion)
+static int validity_launch(hx_ctx* ctx, const double* x, StatusDev* st) {
+  int rc = dispatch<LaunchRates>(ctx, x, (const double*)nullptr, (const double*)nullptr, (double*)nullptr,
+                                 (double*)nullptr, st, 1, 0.0, 0.0, 0.0);
+  if (rc || !ctx->peer) return rc;
+  return peer_status(ctx, st, 1);
+}
+
 static int cg_launch_init(hx_ctx* ctx, CGLaunch& L) {
   int rc = with_node_sum(ctx, L.nc, L.na.evec, [&](auto sum, auto ncc) {
     return launch_cg_nodes<decltype(ncc)::value>(ctx, L.na, sum, true);
@@ -1402,6 +1447,16 @@ extern "C" int hx_phase_begin(hx_ctx* ctx, const double* x, const double* qdata0
   if (rc) return rc;
   rc = launch_scatter(ctx, ctx->evec2, 1, ctx->mdiag);
   if (rc) return rc;
+  if (ctx->peer) {  // multi-GPU: interface sums of the assembled diagonal
+    const unsigned gp = std::max(1u, std::min<unsigned>(gblocks(ctx->pd.nsh, 256), 592));
+    const unsigned gc = std::max(1u, std::min<unsigned>(gblocks(ctx->pd.nh, 256), 592));
+    k_halo_pack<1><<<gp, 256, 0, ctx->stream>>>(ctx->pd, nullptr, NodeVec<1>{ctx->mdiag});
+    CKL();
+    rc = peer_sync<0>(ctx, nullptr, nullptr, nullptr);
+    if (rc) return rc;
+    k_halo_combine<1><<<gc, 256, 0, ctx->stream>>>(ctx->pd, nullptr, NodeVec<1>{ctx->mdiag});
+    CKL();
+  }
   const long long nv = ctx->nn * ctx->dim;
   if (bcmask) CK(cudaMemcpyAsync(ctx->mask, bcmask, nv, cudaMemcpyDeviceToDevice, ctx->stream));
   else CK(cudaMemsetAsync(ctx->mask, 0, nv, ctx->stream));
@@ -1458,7 +1513,7 @@ static int rates_device(hx_ctx* ctx, const hx_params* prm, const double* x, cons
                         double* dv, double* de, StatusDev* st, hx_cg_info* cgi, CGDev* cg = nullptr) {
   int rc = status_reset(ctx, st);
   if (rc) return rc;
-  rc = dispatch<LaunchRates>(ctx, x, v, e, ctx->evec, de, st, 0, prm->gamma, prm->q1, prm->q2);
+  rc = rates_launch(ctx, prm, x, v, e, de, st);
   if (rc) return rc;
   // rhs = where(mask, 0, -F.1) built inside k_cg_init from the element vectors
   return run_cg(ctx, ctx->Dm, nullptr, ctx->evec, 1, ctx->has_mask ? ctx->mask : nullptr, ctx->invd,
@@ -1555,8 +1610,7 @@ static int step_impl(hx_ctx* ctx, const hx_params* prm, double t, double dt_fixe
     // validity of the new geometry (hydro.py:400-401)
     rc = status_reset(ctx, ctx->st + 2);
     if (rc) return rc;
-    rc = dispatch<LaunchRates>(ctx, (const double*)x_out, (const double*)nullptr, (const double*)nullptr,
-                               (double*)nullptr, (double*)nullptr, ctx->st + 2, 1, 0.0, 0.0, 0.0);
+    rc = validity_launch(ctx, x_out, ctx->st + 2);
     if (rc) return rc;
     CK(cudaMemcpyAsync(ctx->h_st + 1, ctx->st + 1, 2 * sizeof(StatusDev), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -1648,7 +1702,7 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
     if (r) return r;
     const uint8_t* mask = ctx->has_mask ? ctx->mask : nullptr;
     // stage 1: rates(S); its CFL ratio is timestep_estimate's
-    r = dispatch<LaunchRates>(ctx, x, v, e, ctx->evec, ctx->de0, ctx->st + 0, 0, prm->gamma, prm->q1, prm->q2);
+    r = rates_launch(ctx, prm, x, v, e, ctx->de0, ctx->st + 0);
     if (r) return r;
     CGLaunch L0;
     r = cg_prepare(ctx, ctx->cg, ctx->Dm, nullptr, ctx->evec, 1, mask, ctx->invd, prm->rel_tol, prm->max_iter,
@@ -1663,8 +1717,7 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
     k_axpy_state<<<ga, 256, 0, ctx->stream>>>(m);
     CKL();
     // stage 2: rates(mid)
-    r = dispatch<LaunchRates>(ctx, (const double*)ctx->xm, (const double*)ctx->vm, (const double*)ctx->em,
-                              ctx->evec, ctx->de1, ctx->st + 1, 0, prm->gamma, prm->q1, prm->q2);
+    r = rates_launch(ctx, prm, ctx->xm, ctx->vm, ctx->em, ctx->de1, ctx->st + 1);
     if (r) return r;
     CGLaunch L1;
     r = cg_prepare(ctx, ctx->cg + 1, ctx->Dm, nullptr, ctx->evec, 1, mask, ctx->invd, prm->rel_tol,
@@ -1676,8 +1729,7 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
     k_axpy_state<<<ga, 256, 0, ctx->stream>>>(n);
     CKL();
     // validity of the new geometry
-    r = dispatch<LaunchRates>(ctx, (const double*)x_out, (const double*)nullptr, (const double*)nullptr,
-                              (double*)nullptr, (double*)nullptr, ctx->st + 2, 1, 0.0, 0.0, 0.0);
+    r = validity_launch(ctx, x_out, ctx->st + 2);
     if (r) return r;
     CK(cudaMemcpyAsync(ctx->h_st, ctx->st, 3 * sizeof(StatusDev), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_cg, ctx->cg, 2 * sizeof(CGDev), cudaMemcpyDeviceToHost, ctx->stream));

@@ -8,7 +8,7 @@
 //   * the scalars p.Ap and r.z (and r.z, nnz(b) at the start): world sums.
 // Both move through a per-rank MAILBOX in device memory that every rank maps (CUDA IPC
 // across processes over NVLink, plain pointers when several ranks share a process):
-//   [flag[src] u64 x HX_MAXR | slot[parity][src][2] doubles | recv[src][maxh][nc] doubles]
+//   [flag[src] u64 x HX_MAXR | slot[parity][src][SLOTW] doubles | recv[src][maxh][nc] doubles]
 // A sender writes its data straight into the receivers' mailboxes (P2P stores), then
 // publishes a sequence number with a system-scope release store; a receiver spins on
 // its own flags with acquire loads.  Sequence numbers come from a per-rank device
@@ -24,9 +24,10 @@
 namespace hx {
 
 #define HX_MAXR 64
-constexpr int MB_FLAG = 0;                      // u64 flag[src]
-constexpr int MB_SLOT = HX_MAXR;                // double slot[2][HX_MAXR][2]
-constexpr int MB_RECV = HX_MAXR + 4 * HX_MAXR;  // double recv[src][maxh][nc]
+constexpr int SLOTW = 8;                               // doubles per (parity, source) slot
+constexpr int MB_FLAG = 0;                             // u64 flag[src]
+constexpr int MB_SLOT = HX_MAXR;                       // double slot[2][HX_MAXR][SLOTW]
+constexpr int MB_RECV = HX_MAXR + 2 * SLOTW * HX_MAXR; // double recv[src][maxh][nc]
 constexpr unsigned long long PEER_SPIN_LIMIT = 1ull << 25;  // ~seconds: a stuck peer ends the CG with code 6
 
 struct PeerDev {
@@ -81,37 +82,40 @@ __device__ __forceinline__ bool peer_wait(const PeerDev& pd, const int* ranks, i
 template <int NV>
 __global__ void __launch_bounds__(256) k_peer_sync(PeerDev pd, CGDev* g, double* parts, int* nparts) {
   __shared__ double red[32];
-  __shared__ int ok;
   if (g && !g->active) return;
-  const int n = *nparts;
-  double v[NV];
+  double v[NV > 0 ? NV : 1];
+  if constexpr (NV > 0) {
+    const int n = *nparts;
 #pragma unroll
-  for (int t = 0; t < NV; ++t) {
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < n; i += 256) acc += __ldcg(parts + (long long)i * NV + t);
-    v[t] = block_sum<256>(acc, red);
+    for (int t = 0; t < NV; ++t) {
+      double acc = 0.0;
+      for (int i = threadIdx.x; i < n; i += 256) acc += __ldcg(parts + (long long)i * NV + t);
+      v[t] = block_sum<256>(acc, red);
+    }
   }
   if (threadIdx.x == 0) {
     const unsigned long long seq = *pd.seq + 1;
     *pd.seq = seq;
     const int par = (int)(seq & 1);
-    for (int q = 0; q < pd.nranks; ++q) {
-      double* s = pd.mb[q] + MB_SLOT + (par * HX_MAXR + pd.rank) * 2;
+    if constexpr (NV > 0)
+      for (int q = 0; q < pd.nranks; ++q) {
+        double* s = pd.mb[q] + MB_SLOT + (par * HX_MAXR + pd.rank) * SLOTW;
 #pragma unroll
-      for (int t = 0; t < NV; ++t) s[t] = v[t];
-    }
+        for (int t = 0; t < NV; ++t) s[t] = v[t];
+      }
     __threadfence_system();
     for (int q = 0; q < pd.nranks; ++q) st_release_sys(mb_flag(pd.mb[q], pd.rank), seq);
-    ok = peer_wait(pd, nullptr, pd.nranks, seq) ? 1 : 0;
-    if (ok) {
-      const double* s = pd.mb[pd.rank] + MB_SLOT + par * HX_MAXR * 2;
+    if (peer_wait(pd, nullptr, pd.nranks, seq)) {
+      if constexpr (NV > 0) {
+        const double* s = pd.mb[pd.rank] + MB_SLOT + par * HX_MAXR * SLOTW;
 #pragma unroll
-      for (int t = 0; t < NV; ++t) {
-        double tot = 0.0;
-        for (int q = 0; q < pd.nranks; ++q) tot += __ldcg(s + q * 2 + t);
-        parts[t] = tot;
+        for (int t = 0; t < NV; ++t) {
+          double tot = 0.0;
+          for (int q = 0; q < pd.nranks; ++q) tot += __ldcg(s + q * SLOTW + t);
+          parts[t] = tot;
+        }
+        *nparts = 1;
       }
-      *nparts = 1;
     } else {
       *pd.err = 1;
       if (g) {
@@ -122,6 +126,53 @@ __global__ void __launch_bounds__(256) k_peer_sync(PeerDev pd, CGDev* g, double*
     }
   }
 }
+
+// world step status (timestep_estimate / rk2_step decisions, hydro.py:364-405): for each
+// of n StatusDev records, min of the CFL ratio, sum of the clamp counts, min of the
+// inversion key (a rank-local key: any inversion anywhere makes every rank retry)
+__global__ void k_peer_status(PeerDev pd, StatusDev* st, int n) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long seq = *pd.seq + 1;
+  *pd.seq = seq;
+  const int par = (int)(seq & 1);
+  for (int q = 0; q < pd.nranks; ++q) {
+    double* s = pd.mb[q] + MB_SLOT + (par * HX_MAXR + pd.rank) * SLOTW;
+    for (int i = 0; i < n; ++i) {
+      s[3 * i] = __longlong_as_double((long long)st[i].inv_key);
+      s[3 * i + 1] = __longlong_as_double((long long)st[i].clamps);
+      s[3 * i + 2] = st[i].min_ratio;
+    }
+  }
+  __threadfence_system();
+  for (int q = 0; q < pd.nranks; ++q) st_release_sys(mb_flag(pd.mb[q], pd.rank), seq);
+  if (!peer_wait(pd, nullptr, pd.nranks, seq)) {
+    *pd.err = 1;
+    for (int i = 0; i < n; ++i) st[i].inv_key = 0;  // report a failure: every rank stops
+    return;
+  }
+  const double* s = pd.mb[pd.rank] + MB_SLOT + par * HX_MAXR * SLOTW;
+  for (int i = 0; i < n; ++i) {
+    unsigned long long key = ~0ull, cl = 0;
+    double r = __longlong_as_double(0x7ff0000000000000ll);
+    for (int q = 0; q < pd.nranks; ++q) {
+      const unsigned long long k = (unsigned long long)__double_as_longlong(__ldcg(s + q * SLOTW + 3 * i));
+      key = k < key ? k : key;
+      cl += (unsigned long long)__double_as_longlong(__ldcg(s + q * SLOTW + 3 * i + 1));
+      r = fmin(r, __ldcg(s + q * SLOTW + 3 * i + 2));
+    }
+    st[i].inv_key = key;
+    st[i].clamps = cl;
+    st[i].min_ratio = r;
+  }
+}
+
+// node-vector view for halo sums of assembled node data (the mass diagonal)
+template <int NC>
+struct NodeVec {
+  double* v;
+  __device__ __forceinline__ double operator()(long long n, int c) const { return v[n * NC + c]; }
+  __device__ __forceinline__ void patch(long long n, int c, double total) const { v[n * NC + c] = total; }
+};
 
 // halo, part 1: this rank's node sums at the nodes it shares, stored into each
 // neighbour's recv block (published by the following k_peer_sync)

@@ -306,15 +306,21 @@ class PeerExchange:
     Ranks in one process (tests on one GPU): connect_local([...]).  One process per GPU:
     connect_ipc() exchanges CUDA IPC handles through torch.distributed."""
 
-    def __init__(self, ops, sub, maxh):
+    def __init__(self, target, sub, maxh):
+        """target: a DeviceOps (its MassPA's CG exchanges; the rest of the step stays in
+        DistributedLagrange) or a LagrangeHydro on the subdomain (its whole step graph --
+        rates, F.1 halo, CG, status, validity -- exchanges on the device).  Connect before
+        LagrangeHydro.begin_phase: the mass diagonal's interface sums are exchanged there."""
         import ctypes as C
 
         from . import _lib
-
         from ._device import context_for
 
-        self.ops, self.sub, self.maxh = ops, sub, int(maxh)
-        self._ctx = context_for(sub.mesh, ops.quad)  # the context MassPA runs its CG in
+        self.ops, self.sub, self.maxh = target, sub, int(maxh)
+        if hasattr(target, "hy"):
+            self._ctx = context_for(sub.mesh, target.quad)  # the context MassPA runs its CG in
+        else:
+            self._ctx = target._ctx  # LagrangeHydro's private context: hx_phase_begin / hx_step
         lib, h = self._ctx.lib, self._ctx.h
         self.plan = pl = peer_plan(sub)
         ptr = lambda a: a.ctypes.data_as(C.c_void_p) if a.size else None
@@ -349,7 +355,8 @@ class PeerExchange:
         """Ranks sharing one process (and one GPU): mailboxes are plain device pointers."""
         ptrs = [x.mailbox for x in sorted(exchanges, key=lambda x: x.sub.rank)]
         for x in exchanges:
-            x._warm()
+            if hasattr(x.ops, "hy"):
+                x._warm()
             x._connect(ptrs)
 
     def connect_ipc(self):
