@@ -364,6 +364,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--peer-self", action="store_true",
+                    help="N=1 with the multi-GPU exchange launches active on a one-rank partition")
     ap.add_argument("--host-cg", action="store_true",
                     help="N>1: the host-driven distributed step instead of the device-resident step graph")
     args = ap.parse_args()
@@ -418,6 +420,15 @@ def main():
         *fns, gamma = problems.triple_point_multi(d, counts, extents)
     hy = LagrangeHydro(mesh, gauss_legendre(p + 2), MaterialModel(gamma), visc, bc_mask=box_velocity_bc(mesh))
     st0 = hy.initial_state(*fns)
+    if args.peer_self:
+        # the multi-GPU exchange launches on a one-rank partition (no neighbours, flags to
+        # itself): measures what the exchanges add to a step besides the NVLink flag round trip
+        from paper_2112_07075_b200.distributed import PeerExchange
+        from paper_2112_07075_b200.partition import brick_partition
+
+        _, subs1 = brick_partition(d, extents, counts, p, 1)
+        PeerExchange.connect_local([PeerExchange(hy, subs1[0], 1)])
+        hy.begin_phase(st0)
     ctl = StepControls(cfl=args.cfl, dt_max=1.0, t_final=1e9)
     V = d * mesh.num_nodes
     lib, h = hy._ctx.lib, hy._ctx.h

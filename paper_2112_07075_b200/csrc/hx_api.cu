@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -104,6 +105,9 @@ struct hx_ctx {
   int* peer_plan = nullptr;      // snode|sdst|sidx|hnode|hoff|hsrc (one allocation)
   uint8_t* peer_owned = nullptr;
   unsigned long long* peer_ctr = nullptr;  // [0] seq, [1] err (as int)
+  int* peer_ifx = nullptr;       // (NN) interface index
+  PeerDev* pd_dev = nullptr;     // device copy read by the CG kernels
+  PeerLite pl{};                 // prologue essentials passed by value
 };
 
 struct hx_mass {
@@ -786,6 +790,8 @@ extern "C" int hx_destroy(hx_ctx* ctx) {
   if (ctx->peer_plan) cudaFree(ctx->peer_plan);
   if (ctx->peer_owned) cudaFree(ctx->peer_owned);
   if (ctx->peer_ctr) cudaFree(ctx->peer_ctr);
+  if (ctx->peer_ifx) cudaFree(ctx->peer_ifx);
+  if (ctx->pd_dev) cudaFree(ctx->pd_dev);
   delete ctx;
   return HX_OK;
 }
@@ -984,13 +990,12 @@ static int with_node_sum(hx_ctx* ctx, int nc, const double* evec, F&& f) {
 
 template <int NC, class SUM>
 static int launch_cg_nodes(hx_ctx* ctx, const NodeArgs& na, SUM sum, bool init) {
-  auto kn = k_cg_node<NC, SUM>;
+  auto kn = ctx->peer ? k_cg_node_peer<NC, SUM> : k_cg_node<NC, SUM>;
   auto ki = k_cg_init<NC, SUM>;
-  static unsigned cap_n = 0, cap_i = 0;
-  if (!cap_n) {
-    cap_n = persistent_grid(kn, 256, 0, 1ll << 40);
-    cap_i = persistent_grid(ki, 256, 0, 1ll << 40);
-  }
+  static unsigned caps_n[2] = {0, 0}, cap_i = 0;
+  unsigned& cap_n = caps_n[ctx->peer ? 1 : 0];
+  if (!cap_n) cap_n = persistent_grid(kn, 256, 0, 1ll << 40);
+  if (!cap_i) cap_i = persistent_grid(ki, 256, 0, 1ll << 40);
   const unsigned need = gblocks(ctx->nn * NC, 256);
   if (init) {
     prof_begin(ctx, K_CGINIT);
@@ -1007,9 +1012,10 @@ static int launch_cg_nodes(hx_ctx* ctx, const NodeArgs& na, SUM sum, bool init) 
 template <int P, int NC>
 static int launch_mass_brick(hx_ctx* ctx, const MassBrickArgs& a) {
   using M = MassBrickCfg<P, NC>;
-  auto k = k_mass_brick<P, NC>;
+  auto k = ctx->peer ? k_mass_brick<P, NC, true> : k_mass_brick<P, NC, false>;
   CK(smem_attr(k, M::bytes));
-  static unsigned grid = 0;
+  static unsigned grids[2] = {0, 0};
+  unsigned& grid = grids[ctx->peer ? 1 : 0];
   if (!grid) grid = persistent_grid(k, M::NT, M::bytes, 1ll << 40);
   prof_begin(ctx, K_MASS);
   k<<<std::min(grid, gblocks(ctx->ne, M::EPC)), M::NT, M::bytes, ctx->stream>>>(a);
@@ -1075,6 +1081,8 @@ static int cg_prepare(hx_ctx* ctx, CGDev* cg, const double* D, const double* rhs
   na.tol = rel_tol;
   na.max_iter = max_iter;
   na.owned = ctx->peer ? ctx->peer_owned : nullptr;
+  na.peer = ctx->peer ? ctx->pd_dev : nullptr;
+  na.pl = ctx->pl;
   MassArgs& ma = L.ma;
   ma = MassArgs{};
   ma.x = ctx->z;
@@ -1093,7 +1101,7 @@ static int cg_prepare(hx_ctx* ctx, CGDev* cg, const double* D, const double* rhs
   ma.partials = ctx->partials + preg;
   L.nc = nc;
   L.mb = MassBrickArgs{ctx->p0, ctx->p1, D, ctx->ne, ctx->evec, ctx->elem_major ? nullptr : ctx->slot, cg,
-                       ctx->partials + preg, ctx->bk};
+                       ctx->partials + preg, ctx->bk, ctx->pl};
   return HX_OK;
 }
 
@@ -1105,24 +1113,19 @@ static int peer_sync(hx_ctx* ctx, CGDev* g, double* parts, int* nparts) {
   return HX_OK;
 }
 
-// multi-GPU halo of the E-vector's interface nodes + world p.Ap (after a mass launch)
+// multi-GPU, after a mass launch: this rank's interface partials into the neighbours'
+// receive blocks; the node launch's prologue publishes them with the world p.Ap and
+// sums the interface nodes itself (peer_node_sum)
 static int peer_halo(hx_ctx* ctx, CGLaunch& L) {
+  if (ctx->pd.nsh == 0) return HX_OK;  // no neighbours: nothing to send
   const unsigned gp = std::max(1u, std::min<unsigned>(gblocks((long long)ctx->pd.nsh * L.nc, 256), 592));
-  const unsigned gc = std::max(1u, std::min<unsigned>(gblocks((long long)ctx->pd.nh * L.nc, 256), 592));
   int rc = with_node_sum(ctx, L.nc, ctx->evec, [&](auto sum, auto ncc) {
     k_halo_pack<decltype(ncc)::value><<<gp, 256, 0, ctx->stream>>>(ctx->pd, L.na.cg, sum);
     return HX_OK;
   });
   if (rc) return rc;
   CKL();
-  rc = peer_sync<1>(ctx, L.na.cg, L.na.pm, &L.na.cg->nparts_m);
-  if (rc) return rc;
-  rc = with_node_sum(ctx, L.nc, ctx->evec, [&](auto sum, auto ncc) {
-    k_halo_combine<decltype(ncc)::value><<<gc, 256, 0, ctx->stream>>>(ctx->pd, L.na.cg, sum);
-    return HX_OK;
-  });
-  CKL();
-  return rc;
+  return HX_OK;
 }
 
 // multi-GPU halo of an E-vector's interface nodes outside the CG (F.1 before the CG init)
@@ -1175,10 +1178,7 @@ static int cg_launch_init(hx_ctx* ctx, CGLaunch& L) {
     return launch_cg_nodes<decltype(ncc)::value>(ctx, L.na, sum, true);
   });
   if (rc) return rc;
-  if (ctx->peer) {  // world (r.z, nnz(b)) before M(1) finishes the reduction
-    rc = peer_sync<2>(ctx, L.na.cg, L.na.partials, &L.na.cg->nparts_n);
-    if (rc) return rc;
-  }
+
   L.na.evec = ctx->evec;
   L.na.rhs = nullptr;
   return HX_OK;
@@ -1191,11 +1191,10 @@ static int cg_launch_iter(hx_ctx* ctx, CGLaunch& L) {
     rc = peer_halo(ctx, L);
     if (rc) return rc;
   }
-  rc = with_node_sum(ctx, L.nc, ctx->evec, [&](auto sum, auto ncc) {
+  // world scalars: p.Ap in the node launch's prologue, r.z in the next mass launch's
+  return with_node_sum(ctx, L.nc, ctx->evec, [&](auto sum, auto ncc) {
     return launch_cg_nodes<decltype(ncc)::value>(ctx, L.na, sum, false);
   });
-  if (rc || !ctx->peer) return rc;
-  return peer_sync<1>(ctx, L.na.cg, L.na.partials, &L.na.cg->nparts_n);  // world r.z before M(k+1)
 }
 
 static int cg_launch_finish(hx_ctx* ctx, CGLaunch& L) {
@@ -1991,6 +1990,13 @@ extern "C" int hx_peer_setup(hx_ctx* ctx, int rank, int nranks, int maxh, int ns
   CK(cudaMemcpy(ctx->peer_plan, plan.data(), plan.size() * sizeof(int), cudaMemcpyHostToDevice));
   CK(dalloc(&ctx->peer_owned, (size_t)ctx->nn));
   CK(cudaMemcpy(ctx->peer_owned, owned, (size_t)ctx->nn, cudaMemcpyHostToDevice));
+  {
+    std::vector<int> ifx((size_t)ctx->nn, -1);
+    for (int h = 0; h < nh; ++h) ifx[hnode[h]] = h;
+    if (ctx->peer_ifx) cudaFree(ctx->peer_ifx);
+    CK(dalloc(&ctx->peer_ifx, (size_t)ctx->nn));
+    CK(cudaMemcpy(ctx->peer_ifx, ifx.data(), ifx.size() * sizeof(int), cudaMemcpyHostToDevice));
+  }
   CK(dalloc(&ctx->peer_ctr, 2));
   CK(cudaMemset(ctx->peer_ctr, 0, 2 * sizeof(unsigned long long)));
   PeerDev& pd = ctx->pd;
@@ -2012,6 +2018,7 @@ extern "C" int hx_peer_setup(hx_ctx* ctx, int rank, int nranks, int maxh, int ns
   pd.hoff = P + 3 * nsh + nh;
   pd.hsrc = P + 3 * nsh + 2 * nh + 1;
   pd.owned = ctx->peer_owned;
+  pd.ifx = ctx->peer_ifx;
   *mailbox = ctx->mailbox;
   return HX_OK;
 }
@@ -2034,8 +2041,13 @@ extern "C" int hx_peer_connect(hx_ctx* ctx, void* const* mailboxes) {
     if (rc) return rc;
   }
   cudaFuncAttributes fa;
-  CK(cudaFuncGetAttributes(&fa, k_peer_sync<1>));
-  CK(cudaFuncGetAttributes(&fa, k_peer_sync<2>));
+  CK(cudaFuncGetAttributes(&fa, k_peer_sync<0>));
+  CK(cudaFuncGetAttributes(&fa, k_peer_status));
+  if (!ctx->pd_dev) CK(dalloc(&ctx->pd_dev, 1));
+  CK(cudaMemcpy(ctx->pd_dev, &ctx->pd, sizeof(PeerDev), cudaMemcpyHostToDevice));
+  ctx->pl = PeerLite{ctx->mailbox, reinterpret_cast<double* const*>(reinterpret_cast<char*>(ctx->pd_dev) +
+                                                                     offsetof(PeerDev, mb)),
+                     ctx->peer_ctr, ctx->pd.rank, ctx->pd.nranks};
   ctx->peer = true;
   return HX_OK;
 }

@@ -203,9 +203,10 @@ struct MassBrickArgs {
   CGDev* cg;
   double* partials;
   Brick b;
+  PeerLite pl;          // multi-GPU prologue exchange (k_mass_brick<..., true>)
 };
 
-template <int P, int NC>
+template <int P, int NC, bool PEER = false>
 __global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : MASS_BRICK_MINB) * 128 / MASS_BRICK_NT) k_mass_brick(MassBrickArgs a) {
   using M = MassBrickCfg<P, NC>;
   constexpr int D1 = M::D1, Q = M::Q, QQ = M::QQ, DD = M::DD, NL = M::NL, NQ = M::NQ;
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : MASS_BRICK_MINB) 
   __shared__ double red[32];
   double beta;
   int k;
-  if (!cg_mass_begin<M::NT>(a.cg, red, beta, k)) return;
+  if (!cg_mass_begin<M::NT, PEER>(a.cg, red, beta, k, &a.pl)) return;
   const int t = threadIdx.x;
   const double* po = (k & 1) ? a.pbuf0 : a.pbuf1;
   double acc = 0.0;

@@ -318,6 +318,188 @@ __global__ void __launch_bounds__(NT) k_rates(RatesArgs a) {
 // _solve_momentum (hydro.py:323-327) and the element-wise p.Ap partial:
 //   p.Ap = sum_e sum_q D (B w_e)^2 + sum_{masked} p^2.
 
+// ---------------------------------------------------------------------------
+// multi-GPU peer-memory primitives (mailbox layout and protocol: hx_peer.cuh)
+
+#define HX_MAXR 64
+constexpr int SLOTW = 8;                               // doubles per (parity, source) slot
+constexpr int MB_FLAG = 0;                             // u64 flag[src]
+constexpr int MB_SLOT = HX_MAXR;                       // double slot[2][HX_MAXR][SLOTW]
+constexpr int MB_BCF = HX_MAXR + 2 * SLOTW * HX_MAXR;  // u64: CTA-0 broadcast flag (local, gpu scope)
+constexpr int MB_BC = MB_BCF + 8;                      // double bc[2][SLOTW]: world values for the other CTAs
+constexpr int MB_RECV = MB_BC + 2 * SLOTW;             // double recv[src][maxh][nc]
+constexpr unsigned long long PEER_SPIN_LIMIT = 1ull << 25;  // ~seconds: a stuck peer ends the CG with code 6
+
+struct PeerDev {
+  int rank, nranks, maxh;
+  int nsh;                      // shared (node, neighbour) entries
+  int nh;                       // interface nodes
+  int nnbr;
+  unsigned long long* seq;      // this rank's exchange counter
+  int* err;                     // set to 1 on a peer timeout
+  double* mb[HX_MAXR];          // every rank's mailbox in this address space
+  int nbr[HX_MAXR];             // neighbour ranks
+  const int* snode;             // per shared entry: local node
+  const int* sdst;              //   destination rank
+  const int* sidx;              //   index in the destination's recv block from this rank
+  const int* hnode;             // interface nodes
+  const int* hoff;              // (nh + 1) offsets into hsrc
+  const int* hsrc;              // sharers in ascending rank: -1 = this rank, else (q << 24) | index
+  const uint8_t* owned;         // (NN) lowest-rank sharer owns a node (dot products count it once)
+  const int* ifx;               // (NN) interface index h of a node, -1 inside the subdomain
+};
+
+// what a CG launch's prologue needs for a world sum, passed by value in the kernel
+// arguments (no dependent loads on the latency path)
+struct PeerLite {
+  double* me;               // this rank's mailbox
+  double* const* mbs;       // every rank's mailbox (device array)
+  unsigned long long* seq;  // exchange counter
+  int rank, nranks;
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+#ifndef PEER_SPIN_PURE
+#define PEER_SPIN_PURE 0
+#endif
+#ifndef PEER_SLEEP_NS
+#define PEER_SLEEP_NS 64
+#endif
+#ifndef PEER_BC_SLEEP
+#define PEER_BC_SLEEP 32
+#endif
+#ifndef PEER_FENCE_GPU
+#define PEER_FENCE_GPU 0
+#endif
+__device__ __forceinline__ void fence_acq_rel_sys() {
+#if PEER_FENCE_GPU
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#else
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+#endif
+}
+// spin until *flag >= seq: relaxed polls (pure spin first, then backing off), one
+// acquire fence after success; false after PEER_SPIN_LIMIT polls
+__device__ __forceinline__ bool spin_flag(const unsigned long long* flag, unsigned long long seq) {
+  unsigned long long spins = 0;
+  while (ld_relaxed_sys(flag) < seq) {
+    if (++spins > PEER_SPIN_PURE) __nanosleep(PEER_SLEEP_NS);
+    if (spins > PEER_SPIN_LIMIT) return false;
+  }
+  fence_acq_rel_sys();
+  return true;
+}
+__device__ __forceinline__ unsigned long long* mb_flag(double* mb, int src) {
+  return reinterpret_cast<unsigned long long*>(mb) + MB_FLAG + src;
+}
+// wait until every listed rank published seq; false on timeout
+__device__ __forceinline__ bool peer_wait(const PeerDev& pd, const int* ranks, int n, unsigned long long seq) {
+  double* me = pd.mb[pd.rank];
+  for (int j = 0; j < n; ++j) {
+    const int q = ranks ? ranks[j] : j;
+    if (q == pd.rank) continue;
+    if (!spin_flag(mb_flag(me, q), seq)) return false;
+  }
+  return true;
+}
+
+// world sum of NV values inside a CG launch's prologue (multi-GPU): block 0 posts this
+// rank's values to every rank's slot and publishes seq; every CTA waits for all ranks
+// (itself included) and sums the slots in ascending rank order, so all CTAs of all ranks
+// hold the same values.  False on a peer timeout.
+__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Block 0 alone talks to the other ranks (system scope: one release per rank, one acquire
+// fence); it then broadcasts the world values to the launch's other CTAs through its own
+// mailbox with a gpu-scope release, which they poll at gpu scope.
+template <int NV>
+__device__ __forceinline__ bool peer_world(const PeerLite& pl, unsigned long long seq, double (&v)[NV]) {
+  __shared__ double wv[NV];
+  __shared__ int wok;
+  if (threadIdx.x == 0) {
+    const int par = (int)(seq & 1);
+    unsigned long long* bcf = reinterpret_cast<unsigned long long*>(pl.me) + MB_BCF;
+    double* bc = pl.me + MB_BC + par * SLOTW;
+    int ok = 1;
+    if (blockIdx.x == 0) {
+      for (int q = 0; q < pl.nranks; ++q) {
+        double* s = pl.mbs[q] + MB_SLOT + (par * HX_MAXR + pl.rank) * SLOTW;
+#pragma unroll
+        for (int t = 0; t < NV; ++t) s[t] = v[t];
+      }
+      // the release stores order this thread's slot writes; the halo data were fenced at
+      // system scope by k_halo_pack, which completed before this launch
+      for (int q = 0; q < pl.nranks; ++q) st_release_sys(mb_flag(pl.mbs[q], pl.rank), seq);
+      *pl.seq = seq;
+      for (int q = 0; q < pl.nranks && ok; ++q) ok = spin_flag(mb_flag(pl.me, q), seq) ? 1 : 0;
+      const double* s = pl.me + MB_SLOT + par * HX_MAXR * SLOTW;
+#pragma unroll
+      for (int t = 0; t < NV; ++t) {
+        double tot = 0.0;
+        for (int q = 0; q < pl.nranks; ++q) tot += __ldcg(s + q * SLOTW + t);
+        wv[t] = tot;
+        bc[t] = tot;
+      }
+      bc[NV] = ok ? 1.0 : 0.0;
+      st_release_gpu(bcf, seq);
+    } else {
+      unsigned long long spins = 0;
+      while (ld_acquire_gpu(bcf) < seq) {
+        if (PEER_BC_SLEEP) __nanosleep(PEER_BC_SLEEP);
+        if (++spins > PEER_SPIN_LIMIT) {
+          ok = 0;
+          break;
+        }
+      }
+      if (ok) {
+#pragma unroll
+        for (int t = 0; t < NV; ++t) wv[t] = __ldcg(bc + t);
+        ok = __ldcg(bc + NV) != 0.0;
+      }
+    }
+    wok = ok;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < NV; ++t) v[t] = wv[t];
+  return wok != 0;
+}
+__device__ __forceinline__ PeerLite peer_lite(const PeerDev* pd) {
+  return PeerLite{pd->mb[pd->rank], pd->mb, pd->seq, pd->rank, pd->nranks};
+}
+
+// interface node sum (multi-GPU): the sharers' partials in ascending rank order from 0.0,
+// this rank's own from the local E-vector, the others from the receive blocks
+template <int NC>
+__device__ __forceinline__ double peer_node_sum(const PeerDev* pd, double own, int h, int c) {
+  const double* recv = pd->mb[pd->rank] + MB_RECV;
+  double tot = 0.0;
+  for (int s = __ldg(pd->hoff + h); s < __ldg(pd->hoff + h + 1); ++s) {
+    const int src = __ldg(pd->hsrc + s);
+    tot += src < 0 ? own : __ldcg(recv + ((long long)(src >> 24) * pd->maxh + (src & 0xffffff)) * NC + c);
+  }
+  return tot;
+}
+
 // Device CG state.  Each iteration k is a mass launch M(k) and a node launch N(k).
 // Grid reductions are finished by the CONSUMER launch: every CTA of N(k) sums M(k)'s
 // per-CTA p.Ap partials in the same fixed order (-> alpha_k), every CTA of M(k+1)
@@ -338,6 +520,8 @@ struct CGDev {
   unsigned int cnt[4];
   unsigned long long cond;  // cudaGraphConditionalHandle of the WHILE node (graph mode)
   int use_cond;
+  const PeerDev* peer;      // multi-GPU exchange (null on one GPU)
+  unsigned long long seq0;  // exchange counter at the start of this solve
 };
 
 // Packed element map used by the CG kernels: node id | owner<<27 | wall-mask(c)<<(28+c)
@@ -370,8 +554,9 @@ __device__ __forceinline__ double reduce_bcast(const double* parts, int n, doubl
 // mass-launch prologue of iteration k = it_m: for k >= 2 finish N(k-1)'s r.z
 // reduction, stop test (operators.py:361-362) and beta_k = rz_{k-1}/rz_{k-2}.
 // Returns false when this launch has nothing to do.
-template <int NT>
-__device__ __forceinline__ bool cg_mass_begin(CGDev* g, double* red, double& beta, int& k) {
+template <int NT, bool PEER = true>
+__device__ __forceinline__ bool cg_mass_begin(CGDev* g, double* red, double& beta, int& k,
+                                              const PeerLite* pl = nullptr) {
   if (!g->active) return false;
   k = g->it_m;
   if (k == 1) {  // finish k_cg_init's reduction: rz_0, any(b != 0)
@@ -390,6 +575,19 @@ __device__ __forceinline__ bool cg_mass_begin(CGDev* g, double* red, double& bet
     __syncthreads();
     t = b2[0];
     nz = b2[1];
+    if (PEER && g->peer) {  // world r.z_0 and nnz(b)
+      double w[2] = {t, nz};
+      if (!peer_world<2>(pl ? *pl : peer_lite(g->peer), g->seq0 + 1, w)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+          g->code = 6;
+          g->active = 0;
+          cg_publish(g);
+        }
+        return false;
+      }
+      t = w[0];
+      nz = w[1];
+    }
     const bool none = nz == 0.0, maxed = !none && g->max_iter <= 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       if (!none) {
@@ -409,7 +607,19 @@ __device__ __forceinline__ bool cg_mass_begin(CGDev* g, double* red, double& bet
     beta = 0.0;
     return !(none || maxed);
   }
-  const double rzk = reduce_bcast<NT>(g->parts_n, g->nparts_n, red);
+  double rzk = reduce_bcast<NT>(g->parts_n, g->nparts_n, red);
+  if (PEER && g->peer) {  // world r.z_{k-1}
+    double w[1] = {rzk};
+    if (!peer_world<1>(pl ? *pl : peer_lite(g->peer), g->seq0 + 2ull * k - 1, w)) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        g->code = 6;
+        g->active = 0;
+        cg_publish(g);
+      }
+      return false;
+    }
+    rzk = w[0];
+  }
   const double res = sqrt(fmax(rzk, 0.0));
   const bool conv = res <= g->tol * g->norm0;
   const bool maxed = !conv && (k - 1 >= g->max_iter);
@@ -436,11 +646,24 @@ __device__ __forceinline__ bool cg_mass_begin(CGDev* g, double* red, double& bet
 
 // node-launch prologue of iteration k = it_n: finish M(k)'s p.Ap reduction,
 // breakdown test (operators.py:354-355), alpha_k = rz_{k-1}/pAp.
-template <int NT>
-__device__ __forceinline__ bool cg_node_begin(CGDev* g, double* red, double& alpha, double& alpha_prev, int& k) {
+template <int NT, bool PEER = true>
+__device__ __forceinline__ bool cg_node_begin(CGDev* g, double* red, double& alpha, double& alpha_prev, int& k,
+                                              const PeerLite* pl = nullptr) {
   if (!g->active) return false;
   k = g->it_n;
-  const double pAp = reduce_bcast<NT>(g->parts_m, g->nparts_m, red);
+  double pAp = reduce_bcast<NT>(g->parts_m, g->nparts_m, red);
+  if (PEER && g->peer) {  // world p.Ap_k; the flag also publishes this rank's halo (k_halo_pack)
+    double w[1] = {pAp};
+    if (!peer_world<1>(pl ? *pl : peer_lite(g->peer), g->seq0 + 2ull * k, w)) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        g->code = 6;
+        g->active = 0;
+        cg_publish(g);
+      }
+      return false;
+    }
+    pAp = w[0];
+  }
   if (pAp <= 0.0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       g->code = 3;
@@ -988,6 +1211,8 @@ struct NodeArgs {
   unsigned long long cond;
   int use_cond;
   const uint8_t* owned;  // multi-GPU: r.z counts a node on its owning rank only (null: every node)
+  const PeerDev* peer;   // multi-GPU exchange (device copy) or null
+  PeerLite pl;           // its prologue essentials, by value
 };
 
 // plain scatter: out = G^T evec (internal layout)
@@ -1067,6 +1292,8 @@ __global__ void __launch_bounds__(256, 4) k_cg_init(NodeArgs a, SUM sum) {
       g->max_iter = a.max_iter;
       g->cond = a.cond;
       g->use_cond = a.use_cond;
+      g->peer = a.peer;
+      g->seq0 = a.peer ? *a.peer->seq : 0ull;
       g->active = 1;
     }
   }
@@ -1081,7 +1308,7 @@ __global__ void __launch_bounds__(256, NODE_MINB) k_cg_node(NodeArgs a, SUM sum)
   CGDev* g = a.cg;
   double alpha, alpha_prev;
   int k;
-  if (!cg_node_begin<256>(g, red, alpha, alpha_prev, k)) return;
+  if (!cg_node_begin<256, false>(g, red, alpha, alpha_prev, k)) return;
   const double beta = g->beta;
   const double* po = (k & 1) ? a.pbuf0 : a.pbuf1;
   double* pn = (k & 1) ? a.pbuf1 : a.pbuf0;
@@ -1124,7 +1351,84 @@ __global__ void __launch_bounds__(256, NODE_MINB) k_cg_node(NodeArgs a, SUM sum)
         a.r[j] = r;
         const double z = __dmul_rn(dj[u], r);
         reinterpret_cast<double2*>(pn)[j] = make_double2(z, p);
-        if (!a.owned || a.owned[j / NC]) rz = fma(r, z, rz);
+        rz = fma(r, z, rz);
+      }
+    }
+  }
+  cg_partial(a.partials, &g->nparts_n, block_sum<256>(rz, red));
+}
+
+// multi-GPU variant: the first trip's own-data loads are issued before the prologue's
+// world p.Ap handshake; interface nodes add the neighbours' partials afterwards
+template <int NC, class SUM>
+__global__ void __launch_bounds__(256, NODE_MINB) k_cg_node_peer(NodeArgs a, SUM sum) {
+  constexpr bool PEER = true;
+  __shared__ double red[32];
+  CGDev* g = a.cg;
+  if (!g->active) return;
+  const int k = g->it_n;  // the iteration cg_node_begin finishes
+  const double* po = (k & 1) ? a.pbuf0 : a.pbuf1;
+  double* pn = (k & 1) ? a.pbuf1 : a.pbuf0;
+  // x is stored every second iteration: at even k, x_k = (x_{k-2} + a_{k-1} p_{k-1}) +
+  // a_k p_k evaluated in registers -- the reference's two roundings, one store
+  // (p_{k-1} is the old pair's second half).  k_cg_finish applies a pending odd step.
+  const bool xk = (k & 1) == 0;
+  const PeerDev* pd = PEER ? g->peer : nullptr;
+  const int* ifx = PEER ? pd->ifx : nullptr;
+  // grid-stride over (node, component), U items per thread per trip so that all
+  // their loads are in flight together
+  constexpr int U = NODE_U;
+  const long long N = a.nn * NC;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long jfirst = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double2 zp[U];
+  double xj[U], rj[U], dj[U], s[U];
+  bool m[U];
+  int hh[U];
+  auto load = [&](long long j0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long j = j0 + u * stride;
+      if (j < N) {
+        const long long n = j / NC;
+        const int c = (int)(j - n * NC);
+        zp[u] = __ldcg(reinterpret_cast<const double2*>(po) + j);
+        if (xk) xj[u] = __ldcg(a.x + j);
+        rj[u] = __ldcg(a.r + j);
+        dj[u] = __ldg(a.invd + j);
+        m[u] = a.mask && a.mask[j];
+        s[u] = sum(n, c);  // own (local elements) part
+        hh[u] = PEER ? __ldg(ifx + n) : -1;
+      }
+    }
+  };
+  // the first trip's loads are in flight while the prologue finishes the p.Ap reduction
+  // (and, multi-GPU, waits for the world value and the neighbours' halo)
+  load(jfirst);
+  double alpha, alpha_prev;
+  int kk;
+  if (!cg_node_begin<256, PEER>(g, red, alpha, alpha_prev, kk, &a.pl)) return;
+  const double beta = g->beta;
+  double rz = 0.0;
+  for (long long j0 = jfirst; j0 < N; j0 += U * stride) {
+    if (j0 != jfirst) load(j0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long j = j0 + u * stride;
+      if (j < N) {
+        if constexpr (PEER) {
+          if (hh[u] >= 0) s[u] = peer_node_sum<NC>(pd, s[u], hh[u], (int)(j % NC));
+        }
+        const double p = __dadd_rn(zp[u].x, __dmul_rn(beta, zp[u].y));
+        const double ap = m[u] ? p : s[u];
+        if (xk) a.x[j] = __dadd_rn(__dadd_rn(xj[u], __dmul_rn(alpha_prev, zp[u].y)), __dmul_rn(alpha, p));
+        const double r = __dsub_rn(rj[u], __dmul_rn(alpha, ap));
+        a.r[j] = r;
+        const double z = __dmul_rn(dj[u], r);
+        reinterpret_cast<double2*>(pn)[j] = make_double2(z, p);
+        // r.z counts a node on its owning rank only (multi-GPU: only interface nodes can
+        // be owned elsewhere)
+        if (!PEER || hh[u] < 0 || a.owned[j / NC]) rz = fma(r, z, rz);
       }
     }
   }

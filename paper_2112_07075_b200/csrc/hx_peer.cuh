@@ -23,57 +23,6 @@
 
 namespace hx {
 
-#define HX_MAXR 64
-constexpr int SLOTW = 8;                               // doubles per (parity, source) slot
-constexpr int MB_FLAG = 0;                             // u64 flag[src]
-constexpr int MB_SLOT = HX_MAXR;                       // double slot[2][HX_MAXR][SLOTW]
-constexpr int MB_RECV = HX_MAXR + 2 * SLOTW * HX_MAXR; // double recv[src][maxh][nc]
-constexpr unsigned long long PEER_SPIN_LIMIT = 1ull << 25;  // ~seconds: a stuck peer ends the CG with code 6
-
-struct PeerDev {
-  int rank, nranks, maxh;
-  int nsh;                      // shared (node, neighbour) entries
-  int nh;                       // interface nodes
-  int nnbr;
-  unsigned long long* seq;      // this rank's exchange counter
-  int* err;                     // set to 1 on a peer timeout
-  double* mb[HX_MAXR];          // every rank's mailbox in this address space
-  int nbr[HX_MAXR];             // neighbour ranks
-  const int* snode;             // per shared entry: local node
-  const int* sdst;              //   destination rank
-  const int* sidx;              //   index in the destination's recv block from this rank
-  const int* hnode;             // interface nodes
-  const int* hoff;              // (nh + 1) offsets into hsrc
-  const int* hsrc;              // sharers in ascending rank: -1 = this rank, else (q << 24) | index
-  const uint8_t* owned;         // (NN) lowest-rank sharer owns a node (dot products count it once)
-};
-
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long* mb_flag(double* mb, int src) {
-  return reinterpret_cast<unsigned long long*>(mb) + MB_FLAG + src;
-}
-// wait until every listed rank published seq; false on timeout
-__device__ __forceinline__ bool peer_wait(const PeerDev& pd, const int* ranks, int n, unsigned long long seq) {
-  double* me = pd.mb[pd.rank];
-  for (int j = 0; j < n; ++j) {
-    const int q = ranks ? ranks[j] : j;
-    if (q == pd.rank) continue;
-    unsigned long long spins = 0;
-    while (ld_acquire_sys(mb_flag(me, q)) < seq) {
-      __nanosleep(64);
-      if (++spins > PEER_SPIN_LIMIT) return false;
-    }
-  }
-  return true;
-}
-
 // CG world scalar: fixed-order sum of this launch's per-CTA partials (NV values each,
 // stride NV), posted to every rank; after all ranks posted, the ascending-rank sum
 // replaces partial 0 and the partial count becomes 1, so the consuming CG kernel
