@@ -281,7 +281,11 @@ struct LaunchRates {
       if (g_rates_kernel == 1) {
         RatesPCArgs a{x, v, e, ctx->qd0, ctx->emap, ctx->elem_major ? nullptr : ctx->slot, ctx->minv, ctx->wnd,
                       ctx->psi1, gamma, q1, q2, ctx->gamma_e, ctx->ne, evec, de, st, ctx->bk, ctx->brick ? 1 : 0};
-        return mode == 0 ? launch_rates_pc<P, 0>(ctx, a) : launch_valid<P>(ctx, a);
+        // the lean validity kernel is measured faster for p <= 3 (p = 2: 44 vs 51 us,
+        // p = 3: 35 vs 40); at p = 4 its images cap it at 2 CTAs/SM and the rates kernel's
+        // geometry-only mode wins (54 vs 89 us)
+        if (mode == 0) return launch_rates_pc<P, 0>(ctx, a);
+        return P <= 3 ? launch_valid<P>(ctx, a) : launch_rates_pc<P, 1>(ctx, a);
       }
     }
     using SM = RatesSmem<DIM, P>;

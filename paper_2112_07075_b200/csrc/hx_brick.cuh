@@ -178,19 +178,14 @@ struct MassBrickCfg {
   static constexpr int D1 = P + 1, Q = P + 2, QQ = Q * Q, DD = D1 * D1, NL = D1 * DD, NQ = Q * QQ;
   static constexpr int PLN = NC * D1;          // planes per element
   static constexpr int EPC = NT / PLN;         // elements per pass
-#if MASS_ALIAS
-  // gather / staging planes live inside the T planes: each plane thread reads its own
-  // plane into registers before it overwrites it (phases 1 and 3), so one image suffices
-  static constexpr int GP = QQ;
-  static constexpr int GS = PLN * GP;
-  static constexpr int TS = PLN * QQ;
-  static constexpr size_t bytes = sizeof(double) * (size_t)EPC * (TS + (MASS_DPF ? NQ : 0));
-#else
-  static constexpr int GP = DD + 1;            // padded plane pitch of the gather / staging image
-  static constexpr int GS = PLN * GP;          // gather doubles per element
-  static constexpr int TS = PLN * QQ;          // T image doubles per element
-  static constexpr size_t bytes = sizeof(double) * (size_t)EPC * (GS + TS);
-#endif
+  // MASS_ALIAS (p >= 3, measured faster; p = 2 keeps separate images): the gather /
+  // staging planes live inside the T planes -- each plane thread reads its own plane into
+  // registers before it overwrites it (phases 1 and 3), so one image suffices
+  static constexpr bool ALIAS = MASS_ALIAS && P >= 3;
+  static constexpr int GP = ALIAS ? QQ : DD + 1;  // plane pitch of the gather / staging image
+  static constexpr int GS = PLN * GP;             // gather doubles per element
+  static constexpr int TS = PLN * QQ;             // T image doubles per element
+  static constexpr size_t bytes = sizeof(double) * (size_t)EPC * ((ALIAS ? 0 : GS) + TS + (MASS_DPF ? NQ : 0));
 };
 
 struct MassBrickArgs {
@@ -214,13 +209,9 @@ __global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : MASS_BRICK_MINB) 
   const double* cB = c_B[P - 1];
   extern __shared__ __align__(16) double smem[];
   double* sG = smem;                 // gather image [el][c][dz][dy*D1+dx] (pitch GP); reused as staging
-#if MASS_ALIAS
-  double* sT = smem;
-#else
-  double* sT = smem + EPC * GS;      // T image [el][c][dz][qy*Q+qx]
-#endif
+  double* sT = M::ALIAS ? smem : smem + EPC * GS;  // T image [el][c][dz][qy*Q+qx]
 #if MASS_DPF
-  double* sD = smem + EPC * M::TS;   // D of the pass (cp.async at the start of the pass)
+  double* sD = smem + EPC * (M::TS + (M::ALIAS ? 0 : GS));  // D of the pass (cp.async at pass start)
 #endif
   __shared__ double red[32];
   double beta;

@@ -7,7 +7,7 @@ mkdir -p $OUT
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
 KS="k_mass_brick k_cg_node k_rates_pc k_cg_init k_valid"
 for K in $KS; do
-  S=30; case $K in *rates*) S=4;; *init*) S=2;; *valid*) S=1;; esac
+  S=30; case $K in *rates*) S=1;; *init*) S=2;; *valid*) S=1;; esac
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 -o /tmp/full_${K} python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
   timeout 600 ncu --set full --cache-control none --clock-control none --import-source on -k regex:$K -s $S -c 1 -o /tmp/warm_${K} python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
 done
