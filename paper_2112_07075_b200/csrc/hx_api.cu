@@ -108,6 +108,7 @@ struct hx_ctx {
   int* peer_ifx = nullptr;       // (NN) interface index
   PeerDev* pd_dev = nullptr;     // device copy read by the CG kernels
   PeerLite pl{};                 // prologue essentials passed by value
+  int last_iters[2] = {0, 0};    // CG iterations of the last plain step's two solves (graph unroll)
 };
 
 struct hx_mass {
@@ -1247,7 +1248,7 @@ static int run_cg(hx_ctx* ctx, const double* D, const double* rhs, const double*
 }
 
 // capture the CG of one stage into the graph being captured on ctx->stream
-static int cg_capture(hx_ctx* ctx, CGLaunch& L) {
+static int cg_capture(hx_ctx* ctx, CGLaunch& L, int iters_hint = 0) {
   cudaStreamCaptureStatus cs;
   cudaGraph_t g;
   const cudaGraphNode_t* deps = nullptr;
@@ -1272,12 +1273,17 @@ static int cg_capture(hx_ctx* ctx, CGLaunch& L) {
   cudaStream_t outer = ctx->stream;
   CK(cudaStreamBeginCaptureToGraph(ctx->gstream2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   ctx->stream = ctx->gstream2;
-  // HX_CG_UNROLL iterations per WHILE body (launches past convergence exit at once)
-  static int unroll = -1;
-  if (unroll < 0) {
+  // iterations per WHILE body (launches past convergence exit at once).  Measured on the
+  // 3D Sedov Q3 bench: a body evaluation costs ~5.8 us, an iteration launched past
+  // convergence ~2.3 us, so the body holds about half of the iterations the previous plain
+  // solve of this stage needed (two bodies; drift of +-2 iterations stays cheap);
+  // HX_CG_UNROLL overrides
+  static int unroll_env = -2;
+  if (unroll_env == -2) {
     const char* v = getenv("HX_CG_UNROLL");
-    unroll = v ? std::max(1, atoi(v)) : 4;
+    unroll_env = v ? std::max(1, atoi(v)) : -1;
   }
+  const int unroll = unroll_env > 0 ? unroll_env : (iters_hint > 0 ? std::min(32, std::max(2, (iters_hint + 3) / 2)) : 4);
   for (int u = 0; u < unroll && rc == HX_OK; ++u) rc = cg_launch_iter(ctx, L);
   ctx->stream = outer;
   if (rc) return rc;
@@ -1640,6 +1646,8 @@ static int step_impl(hx_ctx* ctx, const hx_params* prm, double t, double dt_fixe
     }
     out.code = HX_OK;
     out.retries = attempt;
+    ctx->last_iters[0] = c0.iterations;
+    ctx->last_iters[1] = c1.iterations;
     out.dt = ctx->h_dt[1];
     out.min_h_over_speed = s1.min_ratio;
     out.t_new = t + ctx->h_dt[1];
@@ -1711,7 +1719,7 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
     r = cg_prepare(ctx, ctx->cg, ctx->Dm, nullptr, ctx->evec, 1, mask, ctx->invd, prm->rel_tol, prm->max_iter,
                    ctx->dv0, ctx->dim, nullptr, L0, ctx->emapf);
     if (r) return r;
-    r = cg_capture(ctx, L0);
+    r = cg_capture(ctx, L0, ctx->last_iters[0]);
     if (r) return r;
     DtArgs da{ctx->st + 0, ctx->dt, prm->cfl, prm->dt_max, prm->t_final, 0.0, dt_fixed, 0, ctx->t_dev};
     k_dt<<<1, 1, 0, ctx->stream>>>(da);
@@ -1726,7 +1734,7 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
     r = cg_prepare(ctx, ctx->cg + 1, ctx->Dm, nullptr, ctx->evec, 1, mask, ctx->invd, prm->rel_tol,
                    prm->max_iter, ctx->dv1, ctx->dim, nullptr, L1, ctx->emapf);
     if (r) return r;
-    r = cg_capture(ctx, L1);
+    r = cg_capture(ctx, L1, ctx->last_iters[1]);
     if (r) return r;
     AxpyArgs n{x, v, e, ctx->vm, ctx->dv1, ctx->de1, x_out, v_out, e_out, ctx->dt + 1, 1.0, nv, nte};
     k_axpy_state<<<ga, 256, 0, ctx->stream>>>(n);
