@@ -1260,6 +1260,19 @@ static int cg_capture(hx_ctx* ctx, CGLaunch& L, int iters_hint = 0) {
   L.na.use_cond = 1;
   int rc = cg_launch_init(ctx, L);
   if (rc) return rc;
+  // graph shape: the expected iterations (previous plain solve of this stage + 1) as plain
+  // kernel nodes ahead of a WHILE node with a 2-iteration body, which then usually
+  // evaluates once and skips (578 vs 573 Mdof*steps/s with two half-length bodies,
+  // HX_CG_SHAPE=halves)
+  static int shape = -1;
+  if (shape < 0) {
+    const char* v = getenv("HX_CG_SHAPE");
+    shape = (v && strcmp(v, "halves") == 0) ? 0 : 1;
+  }
+  const bool prefix = shape == 1 && iters_hint > 0;
+  if (prefix)
+    for (int u = 0; u < iters_hint + 1 && rc == HX_OK; ++u) rc = cg_launch_iter(ctx, L);
+  if (rc) return rc;
   CK(cudaStreamGetCaptureInfo(ctx->stream, &cs, nullptr, &g, &deps, &nd));
   cudaGraphNodeParams p = {};
   p.type = cudaGraphNodeTypeConditional;
@@ -1283,7 +1296,9 @@ static int cg_capture(hx_ctx* ctx, CGLaunch& L, int iters_hint = 0) {
     const char* v = getenv("HX_CG_UNROLL");
     unroll_env = v ? std::max(1, atoi(v)) : -1;
   }
-  const int unroll = unroll_env > 0 ? unroll_env : (iters_hint > 0 ? std::min(32, std::max(2, (iters_hint + 3) / 2)) : 4);
+  const int unroll = prefix ? 2
+                   : unroll_env > 0 ? unroll_env
+                                    : (iters_hint > 0 ? std::min(32, std::max(2, (iters_hint + 3) / 2)) : 4);
   for (int u = 0; u < unroll && rc == HX_OK; ++u) rc = cg_launch_iter(ctx, L);
   ctx->stream = outer;
   if (rc) return rc;
