@@ -163,6 +163,9 @@ struct CsrSum {
 #ifndef MASS_LD
 #define MASS_LD __ldcg
 #endif
+#ifndef MASS_CMAJOR
+#define MASS_CMAJOR 0
+#endif
 #ifndef MASS_DPF
 #define MASS_DPF 0
 #endif
@@ -226,14 +229,22 @@ __global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : MASS_BRICK_MINB) 
   constexpr int ROWI = D1 * NC;                 // pairs per node row
   constexpr int ELI = DD * ROWI;                // pairs (= E entries) per element
   constexpr int SLOTS = (ELI + M::NT - 1) / M::NT;
-  int soff[SLOTS], goff[SLOTS];
+  int soff[SLOTS], goff[SLOTS], eoff[SLOTS];
 #pragma unroll
   for (int h = 0; h < SLOTS; ++h) {
     const int it = h * M::NT + t;
     const int row = it / ROWI, s = it - row * ROWI;  // row = dz*D1 + dy
-    const int dz = row / D1, dy = row - dz * D1, dx = s / NC, c = s - dx * NC;
+#if MASS_CMAJOR
+    // component-major within a node row: the 4 nodes of one component are consecutive
+    // lanes (conflict-free shared stores / loads of a row); same 192-byte row in memory
+    const int c = s / D1, dx = s - c * D1;
+#else
+    const int dx = s / NC, c = s - dx * NC;
+#endif
+    const int dz = row / D1, dy = row - dz * D1;
     soff[h] = (c * D1 + dz) * GP + dy * D1 + dx;
     goff[h] = (dx + dy * a.b.Nx + dz * (int)a.b.NxNy) * NC + c;
+    eoff[h] = (row * D1 + dx) * NC + c;  // E entry (l, c) at l*NC + c
   }
   // balanced contiguous element range per CTA, walked in passes of up to EPC elements
   // (all CTAs finish within one pass of each other)
@@ -419,7 +430,7 @@ __global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : MASS_BRICK_MINB) 
         if (it < ELI) {
 #pragma unroll
           for (int el = 0; el < EPC; ++el)
-            if (el < nel) __stcg(out + el * ELI + it, sG[el * GS + soff[h]]);
+            if (el < nel) __stcg(out + el * ELI + eoff[h], sG[el * GS + soff[h]]);
         }
       }
     }
