@@ -377,6 +377,9 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long
 #ifndef PEER_SLEEP_NS
 #define PEER_SLEEP_NS 64
 #endif
+#ifndef PEER_ALL_CTAS
+#define PEER_ALL_CTAS 1
+#endif
 #ifndef PEER_BC_SLEEP
 #define PEER_BC_SLEEP 32
 #endif
@@ -440,6 +443,42 @@ __device__ __forceinline__ bool peer_world(const PeerLite& pl, unsigned long lon
     unsigned long long* bcf = reinterpret_cast<unsigned long long*>(pl.me) + MB_BCF;
     double* bc = pl.me + MB_BC + par * SLOTW;
     int ok = 1;
+#if PEER_ALL_CTAS
+    // every CTA reads the ranks' flags itself: relaxed polls, then one system-scope
+    // acquire load per flag (no fence, no broadcast step)
+    if (blockIdx.x == 0) {
+      for (int q = 0; q < pl.nranks; ++q) {
+        double* s = pl.mbs[q] + MB_SLOT + (par * HX_MAXR + pl.rank) * SLOTW;
+#pragma unroll
+        for (int t = 0; t < NV; ++t) s[t] = v[t];
+      }
+      for (int q = 0; q < pl.nranks; ++q) st_release_sys(mb_flag(pl.mbs[q], pl.rank), seq);
+      *pl.seq = seq;
+    }
+    for (int q = 0; q < pl.nranks && ok; ++q) {
+      unsigned long long spins = 0;
+      const unsigned long long* f = mb_flag(pl.me, q);
+      while (ld_relaxed_sys(f) < seq) {
+        __nanosleep(32);
+        if (++spins > PEER_SPIN_LIMIT) {
+          ok = 0;
+          break;
+        }
+      }
+      if (ok) (void)ld_acquire_sys(f);
+    }
+    if (ok) {
+      const double* s = pl.me + MB_SLOT + par * HX_MAXR * SLOTW;
+#pragma unroll
+      for (int t = 0; t < NV; ++t) {
+        double tot = 0.0;
+        for (int q = 0; q < pl.nranks; ++q) tot += __ldcg(s + q * SLOTW + t);
+        wv[t] = tot;
+      }
+    }
+    (void)bcf;
+    (void)bc;
+#else
     if (blockIdx.x == 0) {
       for (int q = 0; q < pl.nranks; ++q) {
         double* s = pl.mbs[q] + MB_SLOT + (par * HX_MAXR + pl.rank) * SLOTW;
@@ -476,6 +515,7 @@ __device__ __forceinline__ bool peer_world(const PeerLite& pl, unsigned long lon
         ok = __ldcg(bc + NV) != 0.0;
       }
     }
+#endif
     wok = ok;
   }
   __syncthreads();
