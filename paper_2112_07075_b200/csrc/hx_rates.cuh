@@ -565,10 +565,16 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
 // kernel: 4 elements per pass, 4 CTAs per SM, no prefetch buffers.  J is formed with
 // the same contraction order as k_rates_pc (x, y, z stages, ascending sums from 0.0)
 // and det with det_inv_fast's expression, so both kernels agree on every det J.
+#ifndef VALID_EPC
+#define VALID_EPC 4
+#endif
+#ifndef VALID_MINB
+#define VALID_MINB 4
+#endif
 template <int P>
 struct ValidCfg {
   static constexpr int D1 = P + 1, Q = P + 2, DD = D1 * D1, QQ = Q * Q, NQ = Q * QQ;
-  static constexpr int NT = 128, EPC = 4;
+  static constexpr int NT = 128, EPC = VALID_EPC;
   static constexpr int GP = DD + 1, GS = 3 * D1 * GP;         // gather image (c, dz) planes
   static constexpr int XP = 2 * Q + 1, XS = 3 * DD * XP;      // x-stage rows (c, dz, dy)
   static constexpr int PP = 3 * QQ + ((Q - 3 * QQ) % 16 + 16) % 16;
@@ -578,7 +584,7 @@ struct ValidCfg {
 };
 
 template <int P>
-__global__ void __launch_bounds__(128, 4) k_valid(RatesPCArgs a) {
+__global__ void __launch_bounds__(128, VALID_MINB) k_valid(RatesPCArgs a) {
   using V = ValidCfg<P>;
   constexpr int D1 = V::D1, Q = V::Q, DD = V::DD, QQ = V::QQ, NQ = V::NQ, NL = D1 * DD;
   constexpr int NT = V::NT, EPC = V::EPC, GP = V::GP, XP = V::XP, PP = V::PP, PER = V::PER, XS = V::XS;

@@ -144,3 +144,18 @@ def test_peer_cg_repeated_solves_stay_in_step():
     out = _solve_all(ranks)
     for r, (x, it) in zip(ranks, out):
         assert it == it_ref and rel(x, x_ref[r["sub"].l2g]) < 1e-8
+
+
+def test_peer_timeout_reports_error():
+    """A rank whose peer never joins must not hang: the bounded spin ends the CG on the
+    device and hx_mass_cg reports HX_ENCCL (code 6) within seconds."""
+    import time
+
+    from paper_2112_07075_b200._device import LibError
+
+    _, _, ranks = _setup(3, 2, (4, 2, 2), 2, seed=5)
+    r = ranks[0]  # rank 1 never calls the solver
+    t0 = time.perf_counter()
+    with pytest.raises(LibError, match="code 6"):
+        r["ops"].solve_momentum(r["rhs"], r["pre"], r["mask"], 1e-8)
+    assert time.perf_counter() - t0 < 120.0
