@@ -1996,6 +1996,10 @@ extern "C" int hx_peer_setup(hx_ctx* ctx, int rank, int nranks, int maxh, int ns
   ctx->peer_owned = nullptr;
   ctx->peer_ctr = nullptr;
   ctx->peer = false;
+  for (auto& g : ctx->graphs)  // graphs captured with the previous exchange state
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  ctx->graphs.clear();
+  ctx->step_warm = false;
   const size_t nmb = mailbox_doubles(maxh);
   CK(dalloc(&ctx->mailbox, nmb));
   CK(cudaMemset(ctx->mailbox, 0, nmb * sizeof(double)));
@@ -2072,6 +2076,11 @@ extern "C" int hx_peer_connect(hx_ctx* ctx, void* const* mailboxes) {
   CK(cudaFuncGetAttributes(&fa, k_peer_status));
   if (!ctx->pd_dev) CK(dalloc(&ctx->pd_dev, 1));
   CK(cudaMemcpy(ctx->pd_dev, &ctx->pd, sizeof(PeerDev), cudaMemcpyHostToDevice));
+  // step graphs captured before the exchange was connected lack its launches
+  for (auto& g : ctx->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  ctx->graphs.clear();
+  ctx->step_warm = false;
   ctx->pl = PeerLite{ctx->mailbox, reinterpret_cast<double* const*>(reinterpret_cast<char*>(ctx->pd_dev) +
                                                                      offsetof(PeerDev, mb)),
                      ctx->peer_ctr, ctx->pd.rank, ctx->pd.nranks};
