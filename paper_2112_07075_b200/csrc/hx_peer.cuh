@@ -17,6 +17,9 @@
 // loop stays on the device: no host round trip, no NCCL call inside the iteration.
 // Combination order is fixed (ascending rank, from 0.0), so every sharer of a node
 // holds bit-identical values -- deterministic, though not bit-identical to one GPU.
+// The spin-waits assume every rank's launch gets to run: true with one GPU per rank, and
+// for ranks sharing a GPU only while their launches fit on it together (the in-process
+// tests use small meshes); a rank that never arrives ends the spin after a bound (code 6).
 #pragma once
 
 #include "hx_brick.cuh"

@@ -375,3 +375,10 @@ class PeerExchange:
             self._opened.append(p.value)
             ptrs.append(p.value)
         self._connect(ptrs)
+
+    def close(self):
+        """Unmap the other ranks' mailboxes opened through CUDA IPC (after the last step)."""
+        C = self._C
+        for p in self._opened:
+            self._ctx.lib.hx_peer_ipc_close(C.c_void_p(p))
+        self._opened = []
