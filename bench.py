@@ -15,9 +15,13 @@ e2e    : the same steps through the C-ABI entry a host caller binds
 roofline: dominant kernel's algorithmic bytes / its average launch time (CUDA
          events recorded by the library around each launch during the timed steps)
          against MEASURED_PEAKS.json hbm_gbs.
-cpu_baseline / --impl reference: the CPU oracle (oracle/pa_oracle.py, a numpy
-         restatement of the reference, pinned to its golden vectors) on the host
-         cores, on a bounded sample of the same workload.
+cpu_baseline / --impl reference: the unmodified reference package (baseline/_ref,
+         tools/install_reference.sh) through its public API, ExecPlace.sequential()
+         with the fastest BLAS thread count on the host cores, on a bounded sample of
+         the same workload (12^3 elements); the oracle port only if it is not installed.
+window : every arm advances steps 0..HORIZON-1 of the run and restarts from the
+         initial state outside the timed region (the workload underflows at step 42
+         in the reference algorithm itself).
 """
 
 from __future__ import annotations
@@ -181,48 +185,167 @@ def ncu_traffic():
 
 
 # ---------------------------------------------------------------------------
-# CPU oracle (reference arm and cpu_baseline)
+# The timed window.  The 23^3 Q3 Sedov run (CFL 0.05) is valid for a bounded number of
+# steps in the reference algorithm itself: the oracle and the GPU both collapse dt after
+# step ~26 and underflow (TimestepUnderflow) at step 42, t = 6.579338e-04.  Every arm
+# therefore advances the SAME window of the run: steps 0 .. HORIZON-1 from the initial
+# state, restarting from the initial state (a copy outside the timed region) whenever
+# the window is exhausted.  Any --steps/--warmup is valid; `config.window` records the
+# cycle indices of the timed steps.
+
+HORIZON = 20
 
 
-def cpu_oracle_run(p, n, steps, warmup, cfl=0.05):
-    """Time the oracle's timestep_estimate + rk2_step on an n^3 Q{p} Sedov sample."""
+class Window:
+    """Step counter of the cyclic window: restart() is due when pos hits HORIZON."""
+
+    def __init__(self, horizon=HORIZON):
+        self.horizon = horizon
+        self.pos = 0
+
+    def due(self):
+        return self.pos % self.horizon == 0
+
+    def advance(self):
+        self.pos += 1
+
+    def index(self):
+        return self.pos % self.horizon
+
+
+# ---------------------------------------------------------------------------
+# CPU arms: the unmodified reference package (baseline/_ref, installed by
+# tools/install_reference.sh from /root/reference) through its own public API;
+# the oracle port only where the reference is not installed.
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def sedov_ic(d, n, energy=0.25):
+    """Sedov initial condition as the reference's initial_state callables (hydro.py:189-218):
+    rho0 = 1, v0 = 0, e = energy / V_elem in the element at the origin corner (unit cube)."""
+    cell = 1.0 / n
+    vol = cell ** d
+
+    def rho0(xq):
+        return np.ones(xq.shape[1:])
+
+    def v0(x):
+        return np.zeros_like(x)
+
+    def e0(pts):
+        at_origin = np.all(pts.mean(axis=1) < cell, axis=0)
+        return np.where(at_origin[None, :], energy / vol, 0.0) * np.ones(pts.shape[1:])
+
+    return rho0, v0, e0
+
+
+def reference_available():
+    return os.path.isdir(os.path.join(REF_DIR, "ale_minihydro"))
+
+
+def cpu_reference_run(p, n, steps, warmup, cfl, threads, window=None):
+    """Time the reference's timestep_estimate + rk2_step (hydro.py:364-405) on an n^3 Q{p}
+    Sedov sample with ExecPlace.sequential() and `threads` BLAS threads.  Returns
+    (V, per-step seconds, kind)."""
     from threadpoolctl import threadpool_limits
 
-    from oracle import pa_oracle as O
-
-    cores = os.cpu_count() or 1
     d = 3
-    with threadpool_limits(limits=cores):
-        dofmap, coords = O.box_mesh(d, (1.0,) * d, (n,) * d, p)
-        hy = O.Hydro(d, p, dofmap, coords, 1.4, 0.5, 2.0, bc_mask=O.box_mask(coords))
-        st = hy.initial_state(*O.sedov_fns(d, (1.0,) * d, (n,) * d))
+    window = window or Window()
+    with threadpool_limits(limits=threads):
+        if reference_available():
+            if REF_DIR not in sys.path:
+                sys.path.insert(0, REF_DIR)
+            from ale_minihydro.fespace import cartesian_mesh
+            from ale_minihydro.hydro import LagrangeHydro, MaterialModel, StepControls, ViscosityModel, box_velocity_bc
+            from ale_minihydro.kernel_exec import ExecPlace
+            from ale_minihydro.tensor_basis import gauss_legendre
+
+            mesh = cartesian_mesh(d, (1.0,) * d, (n,) * d, p)
+            hy = LagrangeHydro(mesh, gauss_legendre(p + 2), MaterialModel(1.4), ViscosityModel(0.5, 2.0),
+                               bc_mask=box_velocity_bc(mesh), place=ExecPlace.sequential())
+            st0 = hy.initial_state(*sedov_ic(d, n))
+            ctl = StepControls(cfl=cfl, dt_max=1.0, t_final=1e9)
+
+            def one(st):
+                dt = hy.timestep_estimate(st, ctl)
+                return hy.rk2_step(st, dt)[0]
+            V, kind = d * mesh.num_nodes, "reference"
+        else:
+            from oracle import pa_oracle as O
+
+            dofmap, coords = O.box_mesh(d, (1.0,) * d, (n,) * d, p)
+            ohy = O.Hydro(d, p, dofmap, coords, 1.4, 0.5, 2.0, bc_mask=O.box_mask(coords))
+            st0 = ohy.initial_state(*O.sedov_fns(d, (1.0,) * d, (n,) * d))
+
+            def one(st):
+                dt = ohy.timestep_estimate(st, cfl, dt_max=1.0, t_final=1e9)
+                return ohy.rk2_step(st, dt)[0]
+            V, kind = d * coords.shape[0], "port"
         times = []
+        st = st0
         for i in range(warmup + steps):
+            if window.due():
+                st = st0
             t0 = time.perf_counter()
-            dt = hy.timestep_estimate(st, cfl, dt_max=1.0, t_final=1e9)
-            st, _ = hy.rk2_step(st, dt)
+            st = one(st)
+            dtm = time.perf_counter() - t0
+            window.advance()
             if i >= warmup:
-                times.append(time.perf_counter() - t0)
-    V = d * coords.shape[0]
-    return V, times, cores
+                times.append(dtm)
+    return V, times, kind
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def best_threads(p, n, cfl):
+    """BLAS thread count the reference runs fastest with on this host (1 vs all cores vs
+    half): its dgemms are small, so more threads can be slower (the reference's own
+    ExecPlace.threaded is GIL-bound and slower still)."""
+    cores = os.cpu_count() or 1
+    cands = sorted({1, max(1, cores // 2), cores})
+    best, best_t = cores, None
+    for th in cands:
+        _, t, _ = cpu_reference_run(p, n, 1, 1, cfl, th)
+        if best_t is None or t[0] < best_t:
+            best, best_t = th, t[0]
+    return best, cands
 
 
 def run_reference(args, rank):
+    """--impl reference: the reference's own CPU path on this host's cores, rank 0 only."""
     if rank != 0:
         return
     n = args.cpu_n
-    V, times, cores = cpu_oracle_run(args.p, n, args.steps, args.warmup)
+    threads, cands = best_threads(args.p, n, args.cfl)
+    V, times, kind = cpu_reference_run(args.p, n, args.steps, args.warmup, args.cfl, threads)
     tot = sum(times)
     val = V * len(times) / tot / 1e6
-    sample = (f"3D Sedov Q{args.p}-Q{args.p - 1} {n}^3 elements ({V} velocity dofs), "
-              f"{len(times)} timed steps after {args.warmup} warm-up")
+    # the 1-core figure (OMP/OpenBLAS threads = 1) on a short sample of the same window
+    V1, t1, _ = cpu_reference_run(args.p, n, 2, 1, args.cfl, 1)
+    one_core = V1 * len(t1) / sum(t1) / 1e6
+    src = "baseline/_ref ale_minihydro, ExecPlace.sequential()" if kind == "reference" else "oracle/pa_oracle.py"
+    sample = (f"3D Sedov blast Q{args.p}-Q{args.p - 1} {n}^3 elements ({V} velocity dofs), CFL {args.cfl}, "
+              f"{len(times)} timed steps after {args.warmup} warm-up, window of {HORIZON} steps; {src}, "
+              f"{threads} BLAS threads (fastest of {cands}) on {os.cpu_count()} x {cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"3D Sedov Q{args.p}-Q{args.p - 1}, CPU sample {n}^3 elements", "global_batch": V,
-                   "seq_len": None, "parallelism": "cpu"},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "config": {"workload": f"3D Sedov blast Q{args.p}-Q{args.p - 1} (CPU sample {n}^3 elements per step)",
+                   "global_batch": V, "seq_len": None, "parallelism": "cpu", "window_steps": HORIZON},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
+                         "one_core": {"value": one_core, "unit": UNIT, "cores": 1,
+                                      "sample": f"{len(t1)} steps after 1 warm-up, BLAS threads = 1"}},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -287,17 +410,25 @@ def run_distributed(args, world, rank, local):
     q0 = T(np.asarray(st0.qdata0)[:, sub.g_elems])
     ctl = StepControls(cfl=args.cfl, dt_max=1.0, t_final=1e9)
     V_global = d * gmesh.num_nodes
+    win = Window()
     if args.host_cg:
         ops = DeviceOps(sub, 1.4, 0.5, 2.0)
         dl = DistributedLagrange(sub, ops, 1.4, device="cuda")
         dl.begin_phase(x, q0)
         cg_mode = "host-driven step (DistributedLagrange: torch.distributed collectives per CG iteration)"
+        x0, v0, e0 = x.clone(), v.clone(), e.clone()
         t = 0.0
+
+        def restart_if_due():
+            nonlocal x, v, e, t
+            if win.due():
+                x, v, e, t = x0.clone(), v0.clone(), e0.clone(), 0.0
 
         def step():
             nonlocal x, v, e, t
             dt = dl.timestep_estimate(x, v, e, q0, t, args.cfl, dt_max=1.0, t_final=1e9)
             (x, v, e, t), _ = dl.rk2_step(x, v, e, q0, t, dt)
+            win.advance()
     else:
         # device-resident step: each rank runs the single-GPU step graph on its brick with
         # every exchange inside (F.1 / diagonal interface sums, CG halo + world scalars,
@@ -305,26 +436,35 @@ def run_distributed(args, world, rank, local):
         hy = LagrangeHydro(sub.mesh, gauss_legendre(p + 2), MaterialModel(1.4), ViscosityModel(0.5, 2.0),
                            bc_mask=sub.bc_mask)
         PeerExchange(hy, sub, max_shared(subs)).connect_ipc()
-        cur = HydroState(x, v, e, q0, 0.0)
-        hy.begin_phase(cur)
+        hy.begin_phase(HydroState(x, v, e, q0, 0.0))
         bufs = [(torch.empty_like(x), torch.empty_like(v), torch.empty_like(e)) for _ in range(2)]
         cg_mode = "device-resident step graph per rank (peer-memory exchanges, one host sync per step)"
-        it = [0]
+        cur = [None, 0]
+
+        def restart_if_due():
+            if win.due():
+                for dst, src in zip(bufs[0], (x, v, e)):
+                    dst.copy_(src)
+                cur[0], cur[1] = HydroState(bufs[0][0], bufs[0][1], bufs[0][2], q0, 0.0), 0
 
         def step():
-            nonlocal cur
-            cur, _ = hy.step(cur, ctl, out=bufs[it[0] % 2])
-            it[0] += 1
+            st, _ = hy.step(cur[0], ctl, out=bufs[1 - cur[1]])
+            cur[0], cur[1] = st, 1 - cur[1]
+            win.advance()
 
     for _ in range(args.warmup):
+        restart_if_due()
         step()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
     dist.barrier()
     torch.cuda.synchronize()
     tot = 0.0
+    timed_idx = []
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
+            restart_if_due()
+            timed_idx.append(win.index())
             flush.zero_()
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record(stream)
@@ -343,7 +483,8 @@ def run_distributed(args, world, rank, local):
             "config": {"workload": f"3D Sedov blast Q{p}-Q{p - 1}, {n}^3 hex elements per GPU, global {counts}, "
                                    f"CFL {args.cfl}", "global_batch": V_global, "seq_len": None,
                        "parallelism": f"domain decomposition {list(sub.grid)}: {cg_mode}",
-                       "l2": "flushed before every timed step"},
+                       "l2": "flushed before every timed step",
+                       "window": {"horizon_steps": HORIZON, "timed_cycle_indices": timed_idx}},
             "e2e": None, "gpu_launches": None, "roofline": None, "cpu_baseline": None, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -361,7 +502,7 @@ def main():
     ap.add_argument("--cfl", type=float, default=0.05)
     ap.add_argument("--problem", default="sedov", choices=["sedov", "tgv", "triple"])
     ap.add_argument("--cpu-n", type=int, default=12, help="CPU sample: elements per direction")
-    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--peer-self", action="store_true",
@@ -402,7 +543,8 @@ def main():
 
     from paper_2112_07075_b200 import _lib, problems
     from paper_2112_07075_b200.fespace import cartesian_mesh
-    from paper_2112_07075_b200.hydro import LagrangeHydro, MaterialModel, StepControls, ViscosityModel, box_velocity_bc
+    from paper_2112_07075_b200.hydro import (HydroState, LagrangeHydro, MaterialModel, StepControls,
+                                             ViscosityModel, box_velocity_bc)
     from paper_2112_07075_b200.tensor_basis import gauss_legendre
 
     d, p, n = 3, args.p, args.n
@@ -435,41 +577,67 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
 
-    # ---- device-resident steps
-    st = hy.to_device(st0)
-    bufs = [tuple(torch.empty_like(a) for a in (st.x, st.v, st.e)) for _ in range(2)]
+    # ---- device-resident steps over the cyclic window (see Window): the state lives in
+    # two ping-pong buffer sets; a window restart copies the resident initial state into
+    # the current set outside the timed region, so the step graphs keep their buffers
+    st0d = hy.to_device(st0)
+    bufs = [tuple(torch.empty_like(a) for a in (st0d.x, st0d.v, st0d.e)) for _ in range(2)]
+    win = Window()
+    cur = [None, 0]  # state, buffer index
+
+    def restart_if_due():
+        if win.due():
+            b = bufs[0]
+            for dst, src in zip(b, (st0d.x, st0d.v, st0d.e)):
+                dst.copy_(src)
+            cur[0], cur[1] = HydroState(b[0], b[1], b[2], st0d.qdata0, st0d.t), 0
+
+    def dev_step():
+        st, info = hy.step(cur[0], ctl, out=bufs[1 - cur[1]])
+        cur[0], cur[1] = st, 1 - cur[1]
+        win.advance()
+        return info
+
     for i in range(args.warmup):
-        st, info = hy.step(st, ctl, out=bufs[i % 2])
+        restart_if_due()
+        dev_step()
     torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
+    # snapshot of the post-warm-up position: the kernel pass below replays the timed steps
+    snap = (win.pos, cur[1], tuple(a.clone() for a in bufs[cur[1]]), cur[0].t)
     launches0 = hy._ctx.launches()
-    step_ms = []
-    cg_iters = []
+    step_ms, cg_iters, dts, timed_idx = [], [], [], []
     with ClockSampler(local) as clk:
         for i in range(args.steps):
+            restart_if_due()
+            timed_idx.append(win.index())
             flush.zero_()  # L2 flush (outside the per-step events)
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record(stream)
-            st, info = hy.step(st, ctl, out=bufs[(args.warmup + i) % 2])
+            info = dev_step()
             ev1.record(stream)
             ev1.synchronize()
             step_ms.append(ev0.elapsed_time(ev1))
             cg_iters.append(info["cg_iterations"])
+            dts.append(info["dt"])
     torch.cuda.synchronize()
     launches = hy._ctx.launches() - launches0
 
-    # ---- kernel breakdown: the same steps again with CUDA events recorded by the
-    # library around every launch (plain stream launches instead of the graph)
+    # ---- kernel breakdown: the SAME timed steps replayed from the post-warm-up snapshot,
+    # launched without the CUDA graph, CUDA events recorded by the library around every launch
+    win.pos, cur[1] = snap[0], snap[1]
+    for dst, src in zip(bufs[cur[1]], snap[2]):
+        dst.copy_(src)
+    b = bufs[cur[1]]
+    cur[0] = HydroState(b[0], b[1], b[2], st0d.qdata0, snap[3])
     lib.hx_prof_enable(h, 1)
     lib.hx_prof_reset(h)
     prof_ms = 0.0
     for i in range(args.steps):
+        restart_if_due()
         flush.zero_()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        st, info = hy.step(st, ctl, out=bufs[(args.warmup + args.steps + i) % 2])
+        dev_step()
         ev1.record(stream)
         ev1.synchronize()
         prof_ms += ev0.elapsed_time(ev1)
@@ -481,18 +649,14 @@ def main():
         if cnt.value:
             ktimes[name] = (tot.value, int(cnt.value))
     total_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = V * world * args.steps / (total_ms / 1e3) / 1e6
+    value = V * args.steps / (total_ms / 1e3) / 1e6
 
     # ---- e2e through the C-ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        # same step sequence as the device-timed run: from the initial state, W warm-up steps,
-        # then K timed steps (the Sedov CG iteration counts drift with simulated time)
+        # the same window: from the initial state, W warm-up steps, then K timed steps,
+        # restarting from the initial host state (outside the timed region) as above
         hst = st0
         # the host state lives in one pinned arena (x | v | e): separately pinned small
         # blocks measured ~40% slower for H2D on this host (tools/pcie_probe.py)
@@ -501,38 +665,41 @@ def main():
         hx_ = arena[:nx].view(hst.x.shape)
         hv_ = arena[nx:nx + nvv].view(hst.v.shape)
         he_ = arena[nx + nvv:].view(hst.e.shape)
-        hx_.copy_(torch.from_numpy(np.ascontiguousarray(hst.x)))
-        hv_.copy_(torch.from_numpy(np.ascontiguousarray(hst.v)))
-        he_.copy_(torch.from_numpy(np.ascontiguousarray(hst.e)))
+        init = torch.cat([torch.from_numpy(np.ascontiguousarray(a)).reshape(-1) for a in (hst.x, hst.v, hst.e)])
         prm = hy._params(ctl)
-        t_state = hst.t
+        t_state = [hst.t]
         info_c = _lib.StepInfo()
+        hwin = Window()
+
+        def host_restart_if_due():
+            if hwin.due():
+                arena.copy_(init)
+                t_state[0] = hst.t
 
         def host_step():
-            nonlocal t_state
             hy._ctx.sync_stream()
-            rc = lib.hx_step_host(h, _lib.C.byref(prm), float(t_state), hx_.data_ptr(), hv_.data_ptr(),
+            rc = lib.hx_step_host(h, _lib.C.byref(prm), float(t_state[0]), hx_.data_ptr(), hv_.data_ptr(),
                                   he_.data_ptr(), _lib.C.byref(info_c))
             if rc != 0:
-                raise RuntimeError(f"hx_step_host failed: {rc}")
-            t_state = info_c.t_new
+                raise RuntimeError(f"hx_step_host failed: rc {rc}, info.code {info_c.code}")
+            t_state[0] = info_c.t_new
+            hwin.advance()
 
         for _ in range(args.warmup):
+            host_restart_if_due()
             host_step()
         e2e_s = 0.0
         for _ in range(args.steps):
+            host_restart_if_due()
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             host_step()
             e2e_s += time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_s = float(t.item())
         nb = 8 * (hst.x.size + hst.v.size + hst.e.size)
-        e2e = {"value": V * world * args.steps / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": nb,
-               "d2h_bytes_per_step": nb}
+        e2e = {"value": V * args.steps / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": nb,
+               "d2h_bytes_per_step": nb, "ms_per_step": 1e3 * e2e_s / args.steps,
+               "path": "hx_step_host (C-ABI) from pinned host x, v, e"}
 
     # ---- roofline of the dominant kernel
     pk, pk_src = peaks()
@@ -563,13 +730,17 @@ def main():
                          "frac": kern[dom].get("fp64_frac"), "alg_flops_per_launch": kern[dom].get("alg_flops"),
                          "peak_source": "measured live (hx_fp64_peak: DFMA chains, full occupancy)"}}
 
-    # ---- CPU baseline (rank 0, N=1 only)
+    # ---- CPU baseline (rank 0, N=1 only): the reference itself on a bounded sample
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        Vc, times, cores = cpu_oracle_run(p, args.cpu_n, args.cpu_steps, 1)
-        cpu = {"value": Vc * len(times) / sum(times) / 1e6, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"3D Sedov Q{p}-Q{p - 1} {args.cpu_n}^3 elements ({Vc} velocity dofs), "
-                         f"{len(times)} steps after 1 warm-up, oracle/pa_oracle.py"}
+    if rank == 0 and not args.no_cpu:
+        cores, _ = best_threads(p, args.cpu_n, args.cfl)
+        Vc, times, kind = cpu_reference_run(p, args.cpu_n, args.cpu_steps, 1, args.cfl, cores)
+        src = ("baseline/_ref ale_minihydro (the unmodified reference), ExecPlace.sequential()"
+               if kind == "reference" else "oracle/pa_oracle.py (reference not installed)")
+        cpu = {"value": Vc * len(times) / sum(times) / 1e6, "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": f"3D Sedov Q{p}-Q{p - 1} {args.cpu_n}^3 elements ({Vc} velocity dofs), CFL {args.cfl}, "
+                         f"{len(times)} steps after 1 warm-up; {src}; {cores} BLAS threads (the fastest count) on "
+                         f"{os.cpu_count()} x {cpu_model()}"}
 
     if rank == 0:
         line = {
@@ -577,22 +748,23 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{pname}, {V} velocity dofs per GPU, CFL {args.cfl}",
-                       "global_batch": V * world, "seq_len": None,
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "global_batch": V, "seq_len": None, "parallelism": "single",
                        "l2": "flushed (256 MiB write) before every timed step",
                        "layout": layout,
-                       "cg_iterations": cg_iters},
+                       "window": {"horizon_steps": HORIZON, "timed_cycle_indices": timed_idx,
+                                  "note": "steps 0..horizon-1 of the run from the initial state, restarted "
+                                          "from it outside the timed region (the workload underflows at "
+                                          "step 42 in the reference algorithm)"},
+                       "cg_iterations": cg_iters, "dt": dts},
             "e2e": e2e, "gpu_launches": launches, "roofline": roof, "kernels": kern,
-            "kernel_pass": {"note": "kernel times from a second pass of the same steps launched without "
-                                    "the CUDA graph, CUDA events around every launch",
+            "kernel_pass": {"note": "kernel times from a replay of the same timed steps (restored from the "
+                                    "post-warm-up snapshot) launched without the CUDA graph, CUDA events "
+                                    "around every launch",
                             "ms_per_step": prof_ms / args.steps},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
-
 
 if __name__ == "__main__":
     main()

@@ -260,6 +260,11 @@ int hx_peer_setup(hx_ctx* ctx, int rank, int nranks, int maxh, int nsh, const in
                   const uint8_t* owned, void** mailbox);
 int hx_peer_connect(hx_ctx* ctx, void* const* mailboxes);
 /* CUDA IPC export / import of a mailbox (64-byte handle) for ranks in other processes. */
+/* Detach from the exchange (after the last exchanging step, before the peers' mailboxes are
+ * unmapped or freed): synchronises the context's streams, clears the peer pointers and drops
+ * the step graphs that contain exchange launches.  Replaces no reference call (the
+ * reference's P operator is the identity). */
+int hx_peer_disconnect(hx_ctx* ctx);
 int hx_peer_ipc_handle(const void* mailbox, void* handle_out);
 int hx_peer_ipc_open(const void* handle, void** ptr_out);
 int hx_peer_ipc_close(void* ptr);

@@ -101,6 +101,7 @@ _SIGS = {
     "hx_peer_setup": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P, C.c_int, P, P, P, C.c_int, P, P,
                                 C.POINTER(C.c_void_p)]),
     "hx_peer_connect": (C.c_int, [P, P]),
+    "hx_peer_disconnect": (C.c_int, [P]),
     "hx_peer_ipc_handle": (C.c_int, [P, P]),
     "hx_peer_ipc_open": (C.c_int, [P, C.POINTER(C.c_void_p)]),
     "hx_peer_ipc_close": (C.c_int, [P]),

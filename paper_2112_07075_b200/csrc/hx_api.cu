@@ -13,9 +13,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <type_traits>
 #include <utility>
+#include <memory>
 #include <vector>
 
 #include "../../include/b200hydro.h"
@@ -74,6 +76,7 @@ struct hx_ctx {
   // host mirrors
   CGDev* h_cg = nullptr;
   StatusDev* h_st = nullptr;
+  int* h_perr = nullptr;  // pinned copy of the peer-exchange error flag (pd.err)
   double* h_dt = nullptr;
   // live per-kernel-class timing (hx_prof_*): event pairs around instrumented launches
   bool prof_on = false;
@@ -81,6 +84,20 @@ struct hx_ctx {
   std::vector<int> prof_cls;
   int prof_used = 0;
   int prof_pending = 0;
+  // graph-mode profiling: event-record nodes captured into a dedicated step graph
+  // (external events, re-recorded by every launch of that graph), each pair tagged with
+  // (CG stage, iteration) so launches past convergence are not counted
+  struct GProf {
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> cls, stage, iter;
+    int used = 0;
+    ~GProf() {
+      for (auto& e : ev) cudaEventDestroy(e);
+    }
+  };
+  bool prof_capture = false;
+  int prof_tag_stage = -1, prof_tag_iter = 0;
+  GProf* gp = nullptr;  // the profiling graph being captured
   double prof_tot[8] = {0};
   long long prof_cnt[8] = {0};
   // CUDA-graph step path (one graph per buffer/parameter set)
@@ -89,6 +106,8 @@ struct hx_ctx {
     double dt_fixed;
     hx_params prm;
     int seen = 0;
+    bool prof = false;  // captured with timing event nodes (hx_prof_enable)
+    std::shared_ptr<GProf> gprof;
     cudaGraphExec_t exec = nullptr;
   };
   std::vector<StepGraph> graphs;
@@ -178,7 +197,46 @@ static void prof_collect(hx_ctx* c) {
   c->prof_used = 0;
 }
 
+// inside a profiling-graph capture: event-record nodes on the outer capture stream only
+// (conditional WHILE bodies take no event nodes)
+static void gprof_begin(hx_ctx* c, int cls) {
+  hx_ctx::GProf* g = c->gp;
+  if (!g || c->stream != c->gstream || (size_t)(2 * g->used + 2) > g->ev.size()) return;
+  cudaEventRecordWithFlags(g->ev[2 * g->used], c->stream, cudaEventRecordExternal);
+  c->prof_pending = cls;
+}
+
+static void gprof_end(hx_ctx* c) {
+  hx_ctx::GProf* g = c->gp;
+  if (!g || c->stream != c->gstream || (size_t)(2 * g->used + 2) > g->ev.size()) return;
+  cudaEventRecordWithFlags(g->ev[2 * g->used + 1], c->stream, cudaEventRecordExternal);
+  g->cls[g->used] = c->prof_pending;
+  g->stage[g->used] = c->prof_tag_stage;
+  g->iter[g->used] = c->prof_tag_iter;
+  ++g->used;
+}
+
+// after a profiling-graph launch has completed: accumulate its event pairs; CG launches of
+// iteration k > the stage's iteration count (past convergence, exit at once) are skipped
+static void gprof_collect(hx_ctx* c, const hx_ctx::GProf* g, const int* stage_iters) {
+  for (int i = 0; i < g->used; ++i) {
+    const int st = g->stage[i], k = g->iter[i];
+    if (st >= 0 && k > 0 && k > stage_iters[st]) continue;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, g->ev[2 * i], g->ev[2 * i + 1]) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    c->prof_tot[g->cls[i]] += ms;
+    c->prof_cnt[g->cls[i]] += 1;
+  }
+}
+
 static void prof_begin(hx_ctx* c, int cls) {
+  if (c->prof_capture) {
+    gprof_begin(c, cls);
+    return;
+  }
   if (!c->prof_on) return;
   if ((size_t)(2 * c->prof_used + 2) > c->prof_ev.size()) prof_collect(c);
   cudaEventRecord(c->prof_ev[2 * c->prof_used], c->stream);
@@ -186,10 +244,29 @@ static void prof_begin(hx_ctx* c, int cls) {
 }
 
 static void prof_end(hx_ctx* c) {
+  if (c->prof_capture) {
+    gprof_end(c);
+    return;
+  }
   if (!c->prof_on) return;
   cudaEventRecord(c->prof_ev[2 * c->prof_used + 1], c->stream);
   c->prof_cls[c->prof_used] = c->prof_pending;
   ++c->prof_used;
+}
+
+// HX_GRID_CAP=n caps every persistent grid at n CTAs (test hook: small meshes then take
+// the multi-pass paths of the persistent kernels that production sizes take)
+static long long grid_cap() {
+  static long long cap = -1;
+  if (cap < 0) {
+    const char* v = getenv("HX_GRID_CAP");
+    cap = v ? std::max(0ll, atoll(v)) : 0;
+  }
+  return cap;
+}
+
+static unsigned capg(unsigned g) {
+  return grid_cap() > 0 ? (unsigned)std::max(1ll, std::min<long long>(g, grid_cap())) : g;
 }
 
 // resident-capacity grid for persistent kernels (SMs x max resident blocks)
@@ -200,6 +277,7 @@ static unsigned persistent_grid(K kernel, int threads, size_t smem, long long wo
   int per = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
   long long g = (long long)std::max(per, 1) * sms;
+  if (grid_cap() > 0) g = std::min(g, grid_cap());
   return (unsigned)std::max<long long>(1, std::min<long long>(g, work_blocks));
 }
 
@@ -472,7 +550,7 @@ struct LaunchMinv {
       const size_t wb = sizeof(double) * 8 * (D::NQ + DT * DT * Q * Q + DT * DT * DT * DT * Q);
       auto kw = k_minv_warp<P>;
       CK(smem_attr(kw, wb));
-      kw<<<std::min<unsigned>(gblocks(ctx->ne, 8), 148 * 8), 256, wb, ctx->stream>>>(ctx->Dm, ctx->ne, ctx->minv,
+      kw<<<capg(std::min<unsigned>(gblocks(ctx->ne, 8), 148 * 8)), 256, wb, ctx->stream>>>(ctx->Dm, ctx->ne, ctx->minv,
                                                                                      minv_ref);
       CKL();
       return HX_OK;
@@ -727,6 +805,8 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   ok &= cudaMallocHost((void**)&ctx->h_cg, 2 * sizeof(CGDev)) == cudaSuccess;
   ok &= cudaMallocHost((void**)&ctx->h_st, 4 * sizeof(StatusDev)) == cudaSuccess;
   ok &= cudaMallocHost((void**)&ctx->h_dt, 2 * sizeof(double)) == cudaSuccess;
+  ok &= cudaMallocHost((void**)&ctx->h_perr, sizeof(int)) == cudaSuccess;
+  if (ok) *ctx->h_perr = 0;
   if (!ok) {
     int rc = fail(ctx, HX_ECUDA, "device allocation failed");
     hx_destroy(ctx);
@@ -783,6 +863,7 @@ extern "C" int hx_destroy(hx_ctx* ctx) {
     if (p) cudaFree(p);
   if (ctx->h_cg) cudaFreeHost(ctx->h_cg);
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
+  if (ctx->h_perr) cudaFreeHost(ctx->h_perr);
   if (ctx->h_dt) cudaFreeHost(ctx->h_dt);
   if (ctx->h_t) cudaFreeHost(ctx->h_t);
   if (ctx->t_dev) cudaFree(ctx->t_dev);
@@ -861,10 +942,26 @@ extern "C" int hx_scatter_add(hx_ctx* ctx, int space, const double* E, int ncomp
 // ---------------------------------------------------------------------------
 // geometry
 
+// queue the copy of the peer-exchange error flag (a timed-out peer wait anywhere in the
+// work queued so far); checked by peer_check after the next stream sync
+static int peer_err_fetch(hx_ctx* ctx) {
+  if (!ctx->peer || !ctx->peer_ctr) return HX_OK;
+  CK(cudaMemcpyAsync(ctx->h_perr, ctx->peer_ctr + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  return HX_OK;
+}
+
+static int peer_check(hx_ctx* ctx) {
+  if (ctx->peer && ctx->peer_ctr && *ctx->h_perr)
+    return fail(ctx, HX_ENCCL, "peer exchange timed out (a rank did not arrive)");
+  return HX_OK;
+}
+
 static int read_status(hx_ctx* ctx, StatusDev* st, StatusDev* h) {
   CK(cudaMemcpyAsync(h, st, sizeof(StatusDev), cudaMemcpyDeviceToHost, ctx->stream));
+  int rc = peer_err_fetch(ctx);
+  if (rc) return rc;
   CK(cudaStreamSynchronize(ctx->stream));
-  return HX_OK;
+  return peer_check(ctx);
 }
 
 extern "C" int hx_geometry(hx_ctx* ctx, const double* x, double* jac, double* detj, double* jinv, double* wdetj,
@@ -1123,7 +1220,7 @@ static int peer_sync(hx_ctx* ctx, CGDev* g, double* parts, int* nparts) {
 // sums the interface nodes itself (peer_node_sum)
 static int peer_halo(hx_ctx* ctx, CGLaunch& L) {
   if (ctx->pd.nsh == 0) return HX_OK;  // no neighbours: nothing to send
-  const unsigned gp = std::max(1u, std::min<unsigned>(gblocks((long long)ctx->pd.nsh * L.nc, 256), 592));
+  const unsigned gp = capg(std::max(1u, std::min<unsigned>(gblocks((long long)ctx->pd.nsh * L.nc, 256), 592)));
   int rc = with_node_sum(ctx, L.nc, ctx->evec, [&](auto sum, auto ncc) {
     k_halo_pack<decltype(ncc)::value><<<gp, 256, 0, ctx->stream>>>(ctx->pd, L.na.cg, sum);
     return HX_OK;
@@ -1135,8 +1232,8 @@ static int peer_halo(hx_ctx* ctx, CGLaunch& L) {
 
 // multi-GPU halo of an E-vector's interface nodes outside the CG (F.1 before the CG init)
 static int peer_evec_halo(hx_ctx* ctx, double* evec, int nc) {
-  const unsigned gp = std::max(1u, std::min<unsigned>(gblocks((long long)ctx->pd.nsh * nc, 256), 592));
-  const unsigned gc = std::max(1u, std::min<unsigned>(gblocks((long long)ctx->pd.nh * nc, 256), 592));
+  const unsigned gp = capg(std::max(1u, std::min<unsigned>(gblocks((long long)ctx->pd.nsh * nc, 256), 592)));
+  const unsigned gc = capg(std::max(1u, std::min<unsigned>(gblocks((long long)ctx->pd.nh * nc, 256), 592)));
   int rc = with_node_sum(ctx, nc, evec, [&](auto sum, auto ncc) {
     k_halo_pack<decltype(ncc)::value><<<gp, 256, 0, ctx->stream>>>(ctx->pd, nullptr, sum);
     return HX_OK;
@@ -1204,15 +1301,20 @@ static int cg_launch_iter(hx_ctx* ctx, CGLaunch& L) {
 
 static int cg_launch_finish(hx_ctx* ctx, CGLaunch& L) {
   const long long n = ctx->nn * L.nc;
-  k_cg_finish<<<std::min<unsigned>(gblocks(n, 256), 1184), 256, 0, ctx->stream>>>(L.na.cg, ctx->p0, ctx->p1,
+  k_cg_finish<<<capg(std::min<unsigned>(gblocks(n, 256), 1184)), 256, 0, ctx->stream>>>(L.na.cg, ctx->p0, ctx->p1,
                                                                                   L.na.x, n);
   CKL();
   return HX_OK;
 }
 
+// device CG code -> C-ABI status (3 breakdown, 6 peer timeout, else max_iter)
+static int cg_code(int c) {
+  return c == 0 ? HX_OK : (c == 3 ? HX_ECG_BREAKDOWN : (c == 6 ? HX_ENCCL : HX_ECG_MAXITER));
+}
+
 static void cg_info_from(const CGDev& g, hx_cg_info* info) {
   if (!info) return;
-  info->code = g.code == 0 ? HX_OK : (g.code == 3 ? HX_ECG_BREAKDOWN : (g.code == 6 ? HX_ENCCL : HX_ECG_MAXITER));
+  info->code = cg_code(g.code);
   info->iterations = g.iters;
   info->n_residuals = g.nres;
 }
@@ -1271,7 +1373,11 @@ static int cg_capture(hx_ctx* ctx, CGLaunch& L, int iters_hint = 0) {
   }
   const bool prefix = shape == 1 && iters_hint > 0;
   if (prefix)
-    for (int u = 0; u < iters_hint + 1 && rc == HX_OK; ++u) rc = cg_launch_iter(ctx, L);
+    for (int u = 0; u < iters_hint + 1 && rc == HX_OK; ++u) {
+      ctx->prof_tag_iter = u + 1;  // iteration k = u + 1 (profiling graphs only)
+      rc = cg_launch_iter(ctx, L);
+    }
+  ctx->prof_tag_iter = 0;
   if (rc) return rc;
   CK(cudaStreamGetCaptureInfo(ctx->stream, &cs, nullptr, &g, &deps, &nd));
   cudaGraphNodeParams p = {};
@@ -1472,8 +1578,8 @@ extern "C" int hx_phase_begin(hx_ctx* ctx, const double* x, const double* qdata0
   rc = launch_scatter(ctx, ctx->evec2, 1, ctx->mdiag);
   if (rc) return rc;
   if (ctx->peer) {  // multi-GPU: interface sums of the assembled diagonal
-    const unsigned gp = std::max(1u, std::min<unsigned>(gblocks(ctx->pd.nsh, 256), 592));
-    const unsigned gc = std::max(1u, std::min<unsigned>(gblocks(ctx->pd.nh, 256), 592));
+    const unsigned gp = capg(std::max(1u, std::min<unsigned>(gblocks(ctx->pd.nsh, 256), 592)));
+    const unsigned gc = capg(std::max(1u, std::min<unsigned>(gblocks(ctx->pd.nh, 256), 592)));
     k_halo_pack<1><<<gp, 256, 0, ctx->stream>>>(ctx->pd, nullptr, NodeVec<1>{ctx->mdiag});
     CKL();
     rc = peer_sync<0>(ctx, nullptr, nullptr, nullptr);
@@ -1637,7 +1743,11 @@ static int step_impl(hx_ctx* ctx, const hx_params* prm, double t, double dt_fixe
     rc = validity_launch(ctx, x_out, ctx->st + 2);
     if (rc) return rc;
     CK(cudaMemcpyAsync(ctx->h_st + 1, ctx->st + 1, 2 * sizeof(StatusDev), cudaMemcpyDeviceToHost, ctx->stream));
+    rc = peer_err_fetch(ctx);
+    if (rc) return rc;
     CK(cudaStreamSynchronize(ctx->stream));
+    rc = peer_check(ctx);
+    if (rc) return rc;
     const StatusDev s1 = ctx->h_st[1], s2 = ctx->h_st[2];
     out.cg_iterations[0] = c0.iterations;
     out.cg_iterations[1] = c1.iterations;
@@ -1710,7 +1820,8 @@ static void l2_window(hx_ctx* ctx, cudaStream_t s) {
 static bool same_params(const hx_params& a, const hx_params& b) { return memcmp(&a, &b, sizeof a) == 0; }
 
 static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, const double* x, const double* v,
-                        const double* e, double* x_out, double* v_out, double* e_out, cudaGraphExec_t* exec) {
+                        const double* e, double* x_out, double* v_out, double* e_out, cudaGraphExec_t* exec,
+                        hx_ctx::GProf* gprof = nullptr) {
   const long long nv = ctx->nn * ctx->dim, nte = ctx->ne * ctx->nt;
   const unsigned ga = gblocks((std::max(nv, nte) + 1) / 2, 256);  // 2 entries per thread
   cudaStream_t user = ctx->stream;
@@ -1718,6 +1829,18 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
   const long long launches = ctx->launches;
   ctx->prof_on = false;
   ctx->stream = ctx->gstream;
+  if (gprof) {
+    if (gprof->ev.empty()) {
+      gprof->ev.resize(1024);
+      gprof->cls.resize(512);
+      gprof->stage.resize(512);
+      gprof->iter.resize(512);
+      for (auto& ev : gprof->ev) CK(cudaEventCreate(&ev));
+    }
+    gprof->used = 0;
+    ctx->gp = gprof;
+    ctx->prof_capture = true;
+  }
   cudaGraph_t graph = nullptr;
   int rc = HX_OK;
   l2_window(ctx, ctx->gstream);
@@ -1728,14 +1851,17 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
     if (r) return r;
     const uint8_t* mask = ctx->has_mask ? ctx->mask : nullptr;
     // stage 1: rates(S); its CFL ratio is timestep_estimate's
+    ctx->prof_tag_stage = -1;
     r = rates_launch(ctx, prm, x, v, e, ctx->de0, ctx->st + 0);
     if (r) return r;
+    ctx->prof_tag_stage = 0;
     CGLaunch L0;
     r = cg_prepare(ctx, ctx->cg, ctx->Dm, nullptr, ctx->evec, 1, mask, ctx->invd, prm->rel_tol, prm->max_iter,
                    ctx->dv0, ctx->dim, nullptr, L0, ctx->emapf);
     if (r) return r;
     r = cg_capture(ctx, L0, ctx->last_iters[0]);
     if (r) return r;
+    ctx->prof_tag_stage = -1;
     DtArgs da{ctx->st + 0, ctx->dt, prm->cfl, prm->dt_max, prm->t_final, 0.0, dt_fixed, 0, ctx->t_dev};
     k_dt<<<1, 1, 0, ctx->stream>>>(da);
     CKL();
@@ -1745,12 +1871,14 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
     // stage 2: rates(mid)
     r = rates_launch(ctx, prm, ctx->xm, ctx->vm, ctx->em, ctx->de1, ctx->st + 1);
     if (r) return r;
+    ctx->prof_tag_stage = 1;
     CGLaunch L1;
     r = cg_prepare(ctx, ctx->cg + 1, ctx->Dm, nullptr, ctx->evec, 1, mask, ctx->invd, prm->rel_tol,
                    prm->max_iter, ctx->dv1, ctx->dim, nullptr, L1, ctx->emapf);
     if (r) return r;
     r = cg_capture(ctx, L1, ctx->last_iters[1]);
     if (r) return r;
+    ctx->prof_tag_stage = -1;
     AxpyArgs n{x, v, e, ctx->vm, ctx->dv1, ctx->de1, x_out, v_out, e_out, ctx->dt + 1, 1.0, nv, nte};
     k_axpy_state<<<ga, 256, 0, ctx->stream>>>(n);
     CKL();
@@ -1760,6 +1888,8 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
     CK(cudaMemcpyAsync(ctx->h_st, ctx->st, 3 * sizeof(StatusDev), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_cg, ctx->cg, 2 * sizeof(CGDev), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_dt, ctx->dt, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    r = peer_err_fetch(ctx);
+    if (r) return r;
     CK(cudaStreamEndCapture(ctx->stream, &graph));
     return HX_OK;
   };
@@ -1775,6 +1905,9 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
   }
   ctx->stream = user;
   ctx->prof_on = prof;
+  ctx->prof_capture = false;
+  ctx->gp = nullptr;
+  ctx->prof_tag_stage = -1;
   ctx->launches = launches;
   if (rc) return rc;
   cudaError_t ce = cudaGraphInstantiate(exec, graph, 0);
@@ -1793,12 +1926,14 @@ static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_
     const char* s = getenv("HX_GRAPH");
     g_use_graph = (s && s[0] == '0') ? 0 : 1;
   }
-  if (!g_use_graph || ctx->prof_on) return step_impl(ctx, prm, t, dt_fixed, x, v, e, x_out, v_out, e_out, info);
+  if (!g_use_graph) return step_impl(ctx, prm, t, dt_fixed, x, v, e, x_out, v_out, e_out, info);
   CK(cudaSetDevice(ctx->device));
   const void* key[6] = {x, v, e, x_out, v_out, e_out};
   hx_ctx::StepGraph* sg = nullptr;
+  const bool prof = ctx->prof_on;
   for (auto& g : ctx->graphs)
-    if (!memcmp(g.key, key, sizeof key) && g.dt_fixed == dt_fixed && same_params(g.prm, *prm)) sg = &g;
+    if (!memcmp(g.key, key, sizeof key) && g.dt_fixed == dt_fixed && same_params(g.prm, *prm) && g.prof == prof)
+      sg = &g;
   if (!sg) {
     if (ctx->graphs.size() >= 8) {
       for (auto& g : ctx->graphs)
@@ -1810,6 +1945,7 @@ static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_
     memcpy(sg->key, key, sizeof key);
     sg->dt_fixed = dt_fixed;
     sg->prm = *prm;
+    sg->prof = prof;
   }
   // the context's very first step runs as plain launches (warms every lazy init: kernel
   // attributes, occupancy queries, workspace sizes); every later new buffer/parameter set is
@@ -1820,16 +1956,28 @@ static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_
   }
   ++sg->seen;
   if (!sg->exec) {
-    int rc = capture_step(ctx, prm, dt_fixed, x, v, e, x_out, v_out, e_out, &sg->exec);
+    if (prof) sg->gprof = std::make_shared<hx_ctx::GProf>();
+    int rc = capture_step(ctx, prm, dt_fixed, x, v, e, x_out, v_out, e_out, &sg->exec, sg->gprof.get());
     if (rc) return rc;
   }
   *ctx->h_t = t;
   CK(cudaMemcpyAsync(ctx->t_dev, ctx->h_t, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaGraphLaunch(sg->exec, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  {
+    const int prc = peer_check(ctx);  // before the status: a timed-out status exchange reads as an inversion
+    if (prc) {
+      if (info) info->code = prc;
+      return prc;
+    }
+  }
   const StatusDev s0 = ctx->h_st[0], s1 = ctx->h_st[1], s2 = ctx->h_st[2];
   const CGDev c0 = ctx->h_cg[0], c1 = ctx->h_cg[1];
   ctx->launches += 11 + 2 * (long long)(c0.iters + c1.iters);
+  if (prof && sg->gprof) {
+    const int it[2] = {c0.iters, c1.iters};
+    gprof_collect(ctx, sg->gprof.get(), it);
+  }
   hx_step_info out{};
   const bool estimate = dt_fixed < 0.0;
   long long clamps = 0;
@@ -1862,7 +2010,7 @@ static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_
   }
   clamps += (long long)s0.clamps;
   if (c0.code) {
-    out.code = c0.code == 3 ? HX_ECG_BREAKDOWN : HX_ECG_MAXITER;
+    out.code = cg_code(c0.code);
     if (info) *info = out;
     return out.code;
   }
@@ -1875,7 +2023,7 @@ static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_
   }
   clamps += (long long)s1.clamps;
   if (c1.code) {
-    out.code = c1.code == 3 ? HX_ECG_BREAKDOWN : HX_ECG_MAXITER;
+    out.code = cg_code(c1.code);
     if (info) *info = out;
     return out.code;
   }
@@ -2085,6 +2233,24 @@ extern "C" int hx_peer_connect(hx_ctx* ctx, void* const* mailboxes) {
                                                                      offsetof(PeerDev, mb)),
                      ctx->peer_ctr, ctx->pd.rank, ctx->pd.nranks};
   ctx->peer = true;
+  return HX_OK;
+}
+
+// detach the context from the exchange: waits for its queued work, drops the peer
+// pointers and every step graph that contains exchange launches.  Phase data built with
+// interface sums (mass diagonal) stay; call hx_phase_begin again before solo steps.
+extern "C" int hx_peer_disconnect(hx_ctx* ctx) {
+  if (!ctx) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaStreamSynchronize(ctx->gstream));
+  for (auto& g : ctx->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  ctx->graphs.clear();
+  ctx->step_warm = false;
+  ctx->peer = false;
+  for (int q = 0; q < HX_MAXR; ++q) ctx->pd.mb[q] = nullptr;
+  if (ctx->pd_dev) CK(cudaMemcpy(ctx->pd_dev, &ctx->pd, sizeof(PeerDev), cudaMemcpyHostToDevice));
   return HX_OK;
 }
 

@@ -618,7 +618,7 @@ __device__ __forceinline__ bool cg_mass_begin(CGDev* g, double* red, double& bet
     if (PEER && g->peer) {  // world r.z_0 and nnz(b)
       double w[2] = {t, nz};
       if (!peer_world<2>(pl ? *pl : peer_lite(g->peer), g->seq0 + 1, w)) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (threadIdx.x == 0) {  // any block that timed out stops the CG
           g->code = 6;
           g->active = 0;
           cg_publish(g);
@@ -651,7 +651,7 @@ __device__ __forceinline__ bool cg_mass_begin(CGDev* g, double* red, double& bet
   if (PEER && g->peer) {  // world r.z_{k-1}
     double w[1] = {rzk};
     if (!peer_world<1>(pl ? *pl : peer_lite(g->peer), g->seq0 + 2ull * k - 1, w)) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (threadIdx.x == 0) {  // any block that timed out stops the CG (same values from every block)
         g->code = 6;
         g->active = 0;
         cg_publish(g);
@@ -695,7 +695,7 @@ __device__ __forceinline__ bool cg_node_begin(CGDev* g, double* red, double& alp
   if (PEER && g->peer) {  // world p.Ap_k; the flag also publishes this rank's halo (k_halo_pack)
     double w[1] = {pAp};
     if (!peer_world<1>(pl ? *pl : peer_lite(g->peer), g->seq0 + 2ull * k, w)) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (threadIdx.x == 0) {  // any block that timed out stops the CG (same values from every block)
         g->code = 6;
         g->active = 0;
         cg_publish(g);

@@ -377,8 +377,16 @@ class PeerExchange:
         self._connect(ptrs)
 
     def close(self):
-        """Unmap the other ranks' mailboxes opened through CUDA IPC (after the last step)."""
+        """Leave the exchange after the last step: wait for this rank's queued work, detach
+        the context (hx_peer_disconnect: peer pointers and exchange graphs dropped), wait
+        for every rank to get here, then unmap the other ranks' IPC mailboxes.  Steps on
+        this context afterwards run solo (call begin_phase again first)."""
         C = self._C
+        self._ctx.check(self._ctx.lib.hx_peer_disconnect(self._ctx.h), "hx_peer_disconnect")
+        if self.ops is not None and getattr(self.ops, "peer", None) is self:
+            self.ops.peer = None
+        if self._opened and dist.is_available() and dist.is_initialized():
+            dist.barrier()  # no rank unmaps (or frees) a mailbox another rank may still write
         for p in self._opened:
             self._ctx.lib.hx_peer_ipc_close(C.c_void_p(p))
         self._opened = []

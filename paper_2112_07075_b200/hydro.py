@@ -356,6 +356,7 @@ class LagrangeHydro:
             self._ctx.check(rc, "rates")
         self._raise(info, "rates")
         self.clamp_warnings += int(info.clamped)
+        self.last_cg_iterations = int(info.cg_iterations[0])  # diagnostics (not in the reference)
         dx = state.v.clone() if is_torch(state.v) else state.v.copy()
         return _Rates(dx=dx, dv=like(dv, state.v), de=like(de, state.e),
                       min_h_over_speed=float(info.min_h_over_speed), clamped=int(info.clamped))
@@ -382,8 +383,10 @@ class LagrangeHydro:
         Xo, Vo, Eo = torch.empty_like(X), torch.empty_like(V), torch.empty_like(E)
         info = _lib.StepInfo()
         prm = self._params(max_retries=max_retries)
-        self._call(self._ctx.lib.hx_rk2_step, C.byref(prm), float(state.t), float(dt), _lib.ptr(X), _lib.ptr(V),
-                   _lib.ptr(E), _lib.ptr(Xo), _lib.ptr(Vo), _lib.ptr(Eo), C.byref(info))
+        rc = self._call(self._ctx.lib.hx_rk2_step, C.byref(prm), float(state.t), float(dt), _lib.ptr(X),
+                        _lib.ptr(V), _lib.ptr(E), _lib.ptr(Xo), _lib.ptr(Vo), _lib.ptr(Eo), C.byref(info))
+        if rc != _lib.HX_OK and info.code == _lib.HX_OK:
+            self._ctx.check(rc, "rk2_step")  # failed before the step info was written
         if info.code == _lib.HX_EUNDERFLOW:
             self.clamp_warnings += int(info.clamped)
             raise TimestepUnderflow(f"step rejected {max_retries + 1} times from dt = {dt:.3e}")
@@ -407,8 +410,10 @@ class LagrangeHydro:
             Xo, Vo, Eo = out
         info = _lib.StepInfo()
         prm = self._params(controls, max_retries=max_retries)
-        self._call(self._ctx.lib.hx_step, C.byref(prm), float(state.t), _lib.ptr(X), _lib.ptr(V), _lib.ptr(E),
-                   _lib.ptr(Xo), _lib.ptr(Vo), _lib.ptr(Eo), C.byref(info))
+        rc = self._call(self._ctx.lib.hx_step, C.byref(prm), float(state.t), _lib.ptr(X), _lib.ptr(V),
+                        _lib.ptr(E), _lib.ptr(Xo), _lib.ptr(Vo), _lib.ptr(Eo), C.byref(info))
+        if rc != _lib.HX_OK and info.code == _lib.HX_OK:
+            self._ctx.check(rc, "step")  # failed before the step info was written
         if info.code == _lib.HX_EUNDERFLOW:
             self.clamp_warnings += int(info.clamped)
             if info.failed_stage == 0 and info.retries == 0:

@@ -28,3 +28,16 @@ def rel(a, b):
 @pytest.fixture
 def gold():
     return golden
+
+
+def entry_err(a, b, floor=1e-6):
+    """Largest per-entry error relative to |b_i| + floor * max|b| (an entry-wise check with
+    an absolute floor: a norm-wise error can hide large errors in small entries)."""
+    a = np.asarray(a, float).reshape(-1)
+    b = np.asarray(b, float).reshape(-1)
+    if b.size == 0:
+        return 0.0
+    s = float(np.max(np.abs(b)))
+    if s == 0.0:
+        return float(np.max(np.abs(a)))
+    return float(np.max(np.abs(a - b) / (np.abs(b) + floor * s)))
