@@ -46,34 +46,23 @@ K_NAMES = ["rates", "mass_cg", "cg_node", "cg_init", "axpy", "validity", "other"
 
 
 def algorithmic_bytes(d, p, ne, nn, layout="brick"):
-    """Per-launch algorithmic bytes of each kernel class.
-
-    `brick`: the structured-brick kernels (index-free gathers, element-major E-vectors);
-    `csr`: the generic kernels (element map, node-sorted E-vector + transpose map)."""
+    """Per-launch algorithmic bytes of each kernel class: SURVEY.md section 8(d)'s per-unit
+    figures (the HBM traffic the operation must move at minimum, index maps included,
+    layout-specific intermediates such as the element-major E-vector excluded):
+      mass     B_mass = 8 NE nq + 16 V + 4 NE nl
+      cg_node  the rest of a CG iteration's vector traffic: B_CG,vec/iter - 16 V = 80 V
+      rates    fused qpoint + F.1 + F^T v + energy solve, D_F kept on chip:
+               x, v (16 V) + e + qdata0 + index map in, F.1 (8 V) out,
+               M_e^-1 (8 NE nt^2) in, de (8 NE nt) out
+      cg_init  F.1 in, r, (z, p), x out: 48 V;  axpy: x, v, e and rates in, new state out
+      validity x in + index map"""
     nl, nq, nt = (p + 1) ** d, (p + 2) ** d, max(p, 1) ** d
     V = d * nn
-    E = 8 * d * ne * nl  # one E-vector of d components
-    if layout == "brick":
-        return {
-            # (z, p_{k-1}) pairs gathered + D_M in; element-major E-vector out
-            "mass_cg": 16 * V + 8 * ne * nq + E,
-            # E-vector + (z, p) + r + 1/diag + mask in; (z, p) + r out; x read+written every 2nd iteration
-            "cg_node": E + 16 * V + 8 * V + 8 * V + V + 16 * V + 8 * V + 8 * V,
-            # x, v gathered + e + qdata0 + M_e^{-1} in; F.1 E-vector + de out
-            "rates": 16 * V + 8 * ne * nt + 8 * ne * nq + 8 * ne * nt * nt + E + 8 * ne * nt,
-            # E-vector + 1/diag + mask in; r, (z, p), x out
-            "cg_init": E + 8 * V + V + 8 * V + 16 * V + 8 * V,
-            "axpy": 3 * 2 * 8 * V + 3 * 8 * ne * nt,
-            "validity": 8 * V,
-        }
     return {
-        # D_M + gathered z, p_{k-1} + packed element map + node-sorted E-vector out (slot map)
-        "mass_cg": 8 * ne * nq + 16 * V + 4 * ne * nl + 4 * ne * nl + E,
-        # E-vector + transpose map + (z, p), r, 1/diag, mask in; (z, p), r out; x every 2nd iteration
-        "cg_node": E + 4 * (nn + 1) + 16 * V + 8 * V + 8 * V + V + 16 * V + 8 * V + 8 * V,
-        # x, v gathered + e + qdata0 + element map + M_e^{-1} in; F.1 E-vector (slot map) + de out
-        "rates": 16 * V + 8 * ne * nt + 8 * ne * nq + 4 * ne * nl + 8 * ne * nt * nt + 4 * ne * nl + E + 8 * ne * nt,
-        "cg_init": E + 4 * (nn + 1) + 8 * V + V + 8 * V + 16 * V + 8 * V,
+        "mass_cg": 8 * ne * nq + 16 * V + 4 * ne * nl,
+        "cg_node": 80 * V,
+        "rates": 24 * V + 16 * ne * nt + 8 * ne * nq + 4 * ne * nl + 8 * ne * nt * nt,
+        "cg_init": 48 * V,
         "axpy": 3 * 2 * 8 * V + 3 * 8 * ne * nt,
         "validity": 8 * V + 4 * ne * nl,
     }
@@ -379,16 +368,13 @@ def run_distributed(args, world, rank, local):
     import torch.distributed as dist
 
     from paper_2112_07075_b200 import problems
-    from paper_2112_07075_b200.distributed import DeviceOps, DistributedLagrange, PeerExchange, max_shared
-    from paper_2112_07075_b200.fespace import cartesian_mesh
-    from paper_2112_07075_b200.hydro import (HydroState, LagrangeHydro, MaterialModel, StepControls,
-                                             ViscosityModel, box_velocity_bc)
-    from paper_2112_07075_b200.partition import brick_partition, rank_grid
+    from paper_2112_07075_b200.distributed import DeviceOps, DistributedLagrange, PeerExchange
+    from paper_2112_07075_b200.hydro import HydroState, LagrangeHydro, MaterialModel, StepControls, ViscosityModel
+    from paper_2112_07075_b200.partition import brick_partition, max_shared_nodes
     from paper_2112_07075_b200.tensor_basis import gauss_legendre
 
     d, p, n = 3, args.p, args.n
     # choose global counts so that every brick is n^3
-    counts = [n, n, n]
     gg = [1, 1, 1]
     f = world
     ax = 0
@@ -397,19 +383,22 @@ def run_distributed(args, world, rank, local):
         f //= 2
         ax += 1
     counts = [n * gg[a] for a in range(3)]
-    gmesh = cartesian_mesh(d, (1.0,) * d, counts, p)
-    mask = box_velocity_bc(gmesh)
-    ghy = LagrangeHydro(gmesh, gauss_legendre(p + 2), MaterialModel(1.4), ViscosityModel(0.5, 2.0), bc_mask=mask)
-    st0 = ghy.initial_state(*problems.sedov(d, (1.0,) * d, counts))
-    _, subs = brick_partition(d, (1.0,) * d, counts, p, world, bc_mask_global=mask)
+    # each rank builds only its own brick (no global mesh): local coordinates, numbering
+    # maps and the global box's wall mask come from the brick layout; the initial state is
+    # sampled on the brick, which equals the global sampling restricted to it (the Sedov
+    # source element is found by position)
+    t_setup = time.perf_counter()
+    _, subs = brick_partition(d, (1.0,) * d, counts, p, world, ranks=[rank], build_global=False)
     sub = subs[rank]
-    nt = max(p, 1) ** d
+    maxh = max_shared_nodes(d, counts, p, world)
+    lhy = LagrangeHydro(sub.mesh, gauss_legendre(p + 2), MaterialModel(1.4), ViscosityModel(0.5, 2.0),
+                        bc_mask=sub.bc_mask)
+    st0 = lhy.initial_state(*problems.sedov(d, (1.0,) * d, counts))
     T = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
-    x, v = T(st0.x[sub.l2g]), T(st0.v[sub.l2g])
-    e = T(np.asarray(st0.e).reshape(-1, nt)[sub.g_elems].reshape(-1))
-    q0 = T(np.asarray(st0.qdata0)[:, sub.g_elems])
+    x, v, e, q0 = T(st0.x), T(st0.v), T(st0.e), T(st0.qdata0)
+    setup_s = time.perf_counter() - t_setup
     ctl = StepControls(cfl=args.cfl, dt_max=1.0, t_final=1e9)
-    V_global = d * gmesh.num_nodes
+    V_global = d * int(np.prod([c * p + 1 for c in counts]))
     win = Window()
     if args.host_cg:
         ops = DeviceOps(sub, 1.4, 0.5, 2.0)
@@ -433,10 +422,9 @@ def run_distributed(args, world, rank, local):
         # device-resident step: each rank runs the single-GPU step graph on its brick with
         # every exchange inside (F.1 / diagonal interface sums, CG halo + world scalars,
         # CFL / clamp / inversion status) over CUDA-IPC-mapped peer mailboxes
-        hy = LagrangeHydro(sub.mesh, gauss_legendre(p + 2), MaterialModel(1.4), ViscosityModel(0.5, 2.0),
-                           bc_mask=sub.bc_mask)
-        PeerExchange(hy, sub, max_shared(subs)).connect_ipc()
-        hy.begin_phase(HydroState(x, v, e, q0, 0.0))
+        hy = lhy
+        PeerExchange(hy, sub, maxh).connect_ipc()
+        hy.begin_phase(HydroState(x, v, e, q0, 0.0))  # again: the mass diagonal's interface sums
         bufs = [(torch.empty_like(x), torch.empty_like(v), torch.empty_like(e)) for _ in range(2)]
         cg_mode = "device-resident step graph per rank (peer-memory exchanges, one host sync per step)"
         cur = [None, 0]
@@ -484,7 +472,8 @@ def run_distributed(args, world, rank, local):
                                    f"CFL {args.cfl}", "global_batch": V_global, "seq_len": None,
                        "parallelism": f"domain decomposition {list(sub.grid)}: {cg_mode}",
                        "l2": "flushed before every timed step",
-                       "window": {"horizon_steps": HORIZON, "timed_cycle_indices": timed_idx}},
+                       "window": {"horizon_steps": HORIZON, "timed_cycle_indices": timed_idx},
+                       "setup_s_rank0": setup_s},
             "e2e": None, "gpu_launches": None, "roofline": None, "cpu_baseline": None, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -622,32 +611,54 @@ def main():
     torch.cuda.synchronize()
     launches = hy._ctx.launches() - launches0
 
-    # ---- kernel breakdown: the SAME timed steps replayed from the post-warm-up snapshot,
-    # launched without the CUDA graph, CUDA events recorded by the library around every launch
-    win.pos, cur[1] = snap[0], snap[1]
-    for dst, src in zip(bufs[cur[1]], snap[2]):
-        dst.copy_(src)
-    b = bufs[cur[1]]
-    cur[0] = HydroState(b[0], b[1], b[2], st0d.qdata0, snap[3])
-    lib.hx_prof_enable(h, 1)
-    lib.hx_prof_reset(h)
-    prof_ms = 0.0
-    for i in range(args.steps):
-        restart_if_due()
-        flush.zero_()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        dev_step()
-        ev1.record(stream)
-        ev1.synchronize()
-        prof_ms += ev0.elapsed_time(ev1)
-    lib.hx_prof_enable(h, 0)
+    # ---- kernel breakdown by duplication: the SAME timed steps replayed from the
+    # post-warm-up snapshot through step graphs in which every launch of one kernel class
+    # runs twice (hx_prof_dup; the CG node pass's twin is a dry copy writing to scratch).
+    # A class's in-step cost per launch = (T_dup - T_plain) / (duplicates that did work),
+    # both timed with CUDA events around whole steps on the launching stream, L2 flushed
+    # before every step as in the timed region.  Unlike events around single launches in
+    # a graph (which stall the pipeline between kernels) this leaves the step unperturbed.
+    def restore():
+        win.pos, cur[1] = snap[0], snap[1]
+        for dst, src in zip(bufs[cur[1]], snap[2]):
+            dst.copy_(src)
+        b = bufs[cur[1]]
+        cur[0] = HydroState(b[0], b[1], b[2], st0d.qdata0, snap[3])
+
+    def replay(dup):
+        lib.hx_prof_dup(h, dup)
+        restore()
+        for _ in range(2):  # capture this variant's graphs (both buffer sets) untimed
+            restart_if_due()
+            dev_step()
+        restore()
+        torch.cuda.synchronize()
+        lib.hx_prof_reset(h)
+        tot = 0.0
+        for _ in range(args.steps):
+            restart_if_due()
+            flush.zero_()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            dev_step()
+            ev1.record(stream)
+            ev1.synchronize()
+            tot += ev0.elapsed_time(ev1)
+        cnt = 0
+        if dup >= 0:
+            t_, c_ = _lib.C.c_double(), _lib.C.c_int64()
+            lib.hx_prof_read(h, dup, _lib.C.byref(t_), _lib.C.byref(c_))
+            cnt = int(c_.value)
+        lib.hx_prof_dup(h, -1)
+        return tot, cnt
+
+    prof_base, _ = replay(-1)
     ktimes = {}
-    for k, name in enumerate(K_NAMES):
-        tot, cnt = _lib.C.c_double(), _lib.C.c_int64()
-        lib.hx_prof_read(h, k, _lib.C.byref(tot), _lib.C.byref(cnt))
-        if cnt.value:
-            ktimes[name] = (tot.value, int(cnt.value))
+    for k, name in enumerate(K_NAMES[:6]):
+        tot, cnt = replay(k)
+        if cnt:
+            ktimes[name] = (max(tot - prof_base, 0.0), cnt)  # ms over the K steps, working launches
+    prof_ms = prof_base
     total_ms = sum(step_ms)
     ms_per_step = total_ms / args.steps
     value = V * args.steps / (total_ms / 1e3) / 1e6
@@ -757,10 +768,11 @@ def main():
                                           "step 42 in the reference algorithm)"},
                        "cg_iterations": cg_iters, "dt": dts},
             "e2e": e2e, "gpu_launches": launches, "roofline": roof, "kernels": kern,
-            "kernel_pass": {"note": "kernel times from a replay of the same timed steps (restored from the "
-                                    "post-warm-up snapshot) launched without the CUDA graph, CUDA events "
-                                    "around every launch",
-                            "ms_per_step": prof_ms / args.steps},
+            "kernel_pass": {"note": "per-launch kernel cost in the step graph by duplication: the same timed "
+                                    "steps replayed from the post-warm-up snapshot with every launch of one "
+                                    "class doubled (CG node pass: dry twin writing to scratch); avg_us = "
+                                    "(T_dup - T_plain) / working duplicates, CUDA events around whole steps",
+                            "ms_per_step_plain_replay": prof_ms / args.steps},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }

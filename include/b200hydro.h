@@ -229,6 +229,13 @@ int hx_energies(hx_ctx* ctx, const double* v, const double* e, const double* qda
 int hx_prof_enable(hx_ctx* ctx, int on);
 int hx_prof_read(hx_ctx* ctx, int kclass, double* total_ms, int64_t* count);
 int hx_prof_reset(hx_ctx* ctx);
+/* Step graphs captured after this call duplicate every launch of kernel class `kclass`
+ * (0 rates, 1 mass, 2 CG node pass, 3 CG init, 4 state update, 5 validity; -1 restores
+ * plain graphs).  The CG node pass's duplicate is a dry copy writing to scratch.  A
+ * class's in-step cost is (step time with duplicates - plain step time) / the number of
+ * duplicates that did work, which hx_prof_read(kclass) counts (bench.py).  Measurement
+ * hook; replaces no reference call. */
+int hx_prof_dup(hx_ctx* ctx, int kclass);
 /* Diagnostic (no reference counterpart): fp64 FMA peak of the current device, measured
  * with independent DFMA chains at full occupancy (best of 5 CUDA-event-timed launches);
  * the denominator of the fp64 roofline fractions bench.py reports. */

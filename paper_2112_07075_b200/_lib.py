@@ -97,6 +97,7 @@ _SIGS = {
     "hx_prof_enable": (C.c_int, [P, C.c_int]),
     "hx_prof_read": (C.c_int, [P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "hx_prof_reset": (C.c_int, [P]),
+    "hx_prof_dup": (C.c_int, [P, C.c_int]),
     "hx_fp64_peak": (C.c_int, [C.POINTER(C.c_double)]),
     "hx_peer_setup": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P, C.c_int, P, P, P, C.c_int, P, P,
                                 C.POINTER(C.c_void_p)]),

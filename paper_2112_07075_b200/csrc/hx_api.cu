@@ -84,20 +84,20 @@ struct hx_ctx {
   std::vector<int> prof_cls;
   int prof_used = 0;
   int prof_pending = 0;
-  // graph-mode profiling: event-record nodes captured into a dedicated step graph
-  // (external events, re-recorded by every launch of that graph), each pair tagged with
-  // (CG stage, iteration) so launches past convergence are not counted
+  // graph-mode kernel timing by duplication (hx_prof_dup): a step graph in which every
+  // launch of one kernel class is followed by a second, equivalent launch (the same
+  // node; for the non-idempotent CG node pass a dry copy whose stores go to scratch).
+  // The class's cost in the step is then (T_dup - T_plain) / (working duplicates),
+  // measured with events around whole steps.  Each duplicate is tagged with its
+  // (CG stage, iteration) so launches past convergence are not counted.
   struct GProf {
-    std::vector<cudaEvent_t> ev;
-    std::vector<int> cls, stage, iter;
-    int used = 0;
-    ~GProf() {
-      for (auto& e : ev) cudaEventDestroy(e);
-    }
+    std::vector<int> stage, iter;
   };
   bool prof_capture = false;
+  int dup_class = -1;               // class duplicated in graphs captured now (-1: none)
   int prof_tag_stage = -1, prof_tag_iter = 0;
-  GProf* gp = nullptr;  // the profiling graph being captured
+  GProf* gp = nullptr;              // the duplicating graph being captured
+  double* dup_scratch = nullptr;    // dry node-pass outputs (x, r, pairs x2, partials)
   double prof_tot[8] = {0};
   long long prof_cnt[8] = {0};
   // CUDA-graph step path (one graph per buffer/parameter set)
@@ -106,7 +106,7 @@ struct hx_ctx {
     double dt_fixed;
     hx_params prm;
     int seen = 0;
-    bool prof = false;  // captured with timing event nodes (hx_prof_enable)
+    int dup = -1;  // duplicated kernel class (hx_prof_dup), -1 for the plain graph
     std::shared_ptr<GProf> gprof;
     cudaGraphExec_t exec = nullptr;
   };
@@ -197,44 +197,21 @@ static void prof_collect(hx_ctx* c) {
   c->prof_used = 0;
 }
 
-// inside a profiling-graph capture: event-record nodes on the outer capture stream only
-// (conditional WHILE bodies take no event nodes)
-static void gprof_begin(hx_ctx* c, int cls) {
-  hx_ctx::GProf* g = c->gp;
-  if (!g || c->stream != c->gstream || (size_t)(2 * g->used + 2) > g->ev.size()) return;
-  cudaEventRecordWithFlags(g->ev[2 * g->used], c->stream, cudaEventRecordExternal);
-  c->prof_pending = cls;
-}
+static int dup_last_node(hx_ctx* c, int cls);
 
-static void gprof_end(hx_ctx* c) {
-  hx_ctx::GProf* g = c->gp;
-  if (!g || c->stream != c->gstream || (size_t)(2 * g->used + 2) > g->ev.size()) return;
-  cudaEventRecordWithFlags(g->ev[2 * g->used + 1], c->stream, cudaEventRecordExternal);
-  g->cls[g->used] = c->prof_pending;
-  g->stage[g->used] = c->prof_tag_stage;
-  g->iter[g->used] = c->prof_tag_iter;
-  ++g->used;
-}
-
-// after a profiling-graph launch has completed: accumulate its event pairs; CG launches of
-// iteration k > the stage's iteration count (past convergence, exit at once) are skipped
+// after a duplicating graph's launch: count the duplicates that did work (CG launches of
+// iteration k > the stage's iteration count exit at once)
 static void gprof_collect(hx_ctx* c, const hx_ctx::GProf* g, const int* stage_iters) {
-  for (int i = 0; i < g->used; ++i) {
+  for (size_t i = 0; i < g->stage.size(); ++i) {
     const int st = g->stage[i], k = g->iter[i];
     if (st >= 0 && k > 0 && k > stage_iters[st]) continue;
-    float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, g->ev[2 * i], g->ev[2 * i + 1]) != cudaSuccess) {
-      cudaGetLastError();
-      continue;
-    }
-    c->prof_tot[g->cls[i]] += ms;
-    c->prof_cnt[g->cls[i]] += 1;
+    c->prof_cnt[c->dup_class] += 1;
   }
 }
 
 static void prof_begin(hx_ctx* c, int cls) {
   if (c->prof_capture) {
-    gprof_begin(c, cls);
+    c->prof_pending = cls;
     return;
   }
   if (!c->prof_on) return;
@@ -245,7 +222,12 @@ static void prof_begin(hx_ctx* c, int cls) {
 
 static void prof_end(hx_ctx* c) {
   if (c->prof_capture) {
-    gprof_end(c);
+    // duplicate on the outer capture stream only (a WHILE body takes no duplicates)
+    if (c->prof_pending == c->dup_class && c->stream == c->gstream && c->gp &&
+        dup_last_node(c, c->prof_pending) == HX_OK) {
+      c->gp->stage.push_back(c->prof_tag_stage);
+      c->gp->iter.push_back(c->prof_tag_iter);
+    }
     return;
   }
   if (!c->prof_on) return;
@@ -864,6 +846,7 @@ extern "C" int hx_destroy(hx_ctx* ctx) {
   if (ctx->h_cg) cudaFreeHost(ctx->h_cg);
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
   if (ctx->h_perr) cudaFreeHost(ctx->h_perr);
+  if (ctx->dup_scratch) cudaFree(ctx->dup_scratch);
   if (ctx->h_dt) cudaFreeHost(ctx->h_dt);
   if (ctx->h_t) cudaFreeHost(ctx->h_t);
   if (ctx->t_dev) cudaFree(ctx->t_dev);
@@ -1092,7 +1075,10 @@ static int with_node_sum(hx_ctx* ctx, int nc, const double* evec, F&& f) {
 
 template <int NC, class SUM>
 static int launch_cg_nodes(hx_ctx* ctx, const NodeArgs& na, SUM sum, bool init) {
-  auto kn = ctx->peer ? k_cg_node_peer<NC, SUM> : k_cg_node<NC, SUM>;
+#ifndef NODE_PF
+#define NODE_PF 0
+#endif
+  auto kn = ctx->peer ? k_cg_node_peer<NC, SUM, true> : (NODE_PF ? k_cg_node_peer<NC, SUM, false> : k_cg_node<NC, SUM>);
   auto ki = k_cg_init<NC, SUM>;
   static unsigned caps_n[2] = {0, 0}, cap_i = 0;
   unsigned& cap_n = caps_n[ctx->peer ? 1 : 0];
@@ -1111,8 +1097,24 @@ static int launch_cg_nodes(hx_ctx* ctx, const NodeArgs& na, SUM sum, bool init) 
   return HX_OK;
 }
 
+#ifndef MASS_PIPE
+#define MASS_PIPE 0
+#endif
 template <int P, int NC>
 static int launch_mass_brick(hx_ctx* ctx, const MassBrickArgs& a) {
+  if (MASS_PIPE) {
+    using M = MassPipeCfg<P, NC>;
+    auto k = ctx->peer ? k_mass_brick2<P, NC, true> : k_mass_brick2<P, NC, false>;
+    CK(smem_attr(k, M::bytes));
+    static unsigned grids[2] = {0, 0};
+    unsigned& grid = grids[ctx->peer ? 1 : 0];
+    if (!grid) grid = persistent_grid(k, M::NT, M::bytes, 1ll << 40);
+    prof_begin(ctx, K_MASS);
+    k<<<std::min(grid, gblocks(ctx->ne, M::EPC)), M::NT, M::bytes, ctx->stream>>>(a);
+    prof_end(ctx);
+    CKL();
+    return HX_OK;
+  }
   using M = MassBrickCfg<P, NC>;
   auto k = ctx->peer ? k_mass_brick<P, NC, true> : k_mass_brick<P, NC, false>;
   CK(smem_attr(k, M::bytes));
@@ -1830,14 +1832,8 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
   ctx->prof_on = false;
   ctx->stream = ctx->gstream;
   if (gprof) {
-    if (gprof->ev.empty()) {
-      gprof->ev.resize(1024);
-      gprof->cls.resize(512);
-      gprof->stage.resize(512);
-      gprof->iter.resize(512);
-      for (auto& ev : gprof->ev) CK(cudaEventCreate(&ev));
-    }
-    gprof->used = 0;
+    gprof->stage.clear();
+    gprof->iter.clear();
     ctx->gp = gprof;
     ctx->prof_capture = true;
   }
@@ -1866,7 +1862,9 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
     k_dt<<<1, 1, 0, ctx->stream>>>(da);
     CKL();
     AxpyArgs m{x, v, e, v, ctx->dv0, ctx->de0, ctx->xm, ctx->vm, ctx->em, ctx->dt + 1, 0.5, nv, nte};
+    prof_begin(ctx, K_AXPY);
     k_axpy_state<<<ga, 256, 0, ctx->stream>>>(m);
+    prof_end(ctx);
     CKL();
     // stage 2: rates(mid)
     r = rates_launch(ctx, prm, ctx->xm, ctx->vm, ctx->em, ctx->de1, ctx->st + 1);
@@ -1880,7 +1878,9 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
     if (r) return r;
     ctx->prof_tag_stage = -1;
     AxpyArgs n{x, v, e, ctx->vm, ctx->dv1, ctx->de1, x_out, v_out, e_out, ctx->dt + 1, 1.0, nv, nte};
+    prof_begin(ctx, K_AXPY);
     k_axpy_state<<<ga, 256, 0, ctx->stream>>>(n);
+    prof_end(ctx);
     CKL();
     // validity of the new geometry
     r = validity_launch(ctx, x_out, ctx->st + 2);
@@ -1926,16 +1926,16 @@ static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_
     const char* s = getenv("HX_GRAPH");
     g_use_graph = (s && s[0] == '0') ? 0 : 1;
   }
-  if (!g_use_graph) return step_impl(ctx, prm, t, dt_fixed, x, v, e, x_out, v_out, e_out, info);
+  if (!g_use_graph || ctx->prof_on) return step_impl(ctx, prm, t, dt_fixed, x, v, e, x_out, v_out, e_out, info);
   CK(cudaSetDevice(ctx->device));
   const void* key[6] = {x, v, e, x_out, v_out, e_out};
   hx_ctx::StepGraph* sg = nullptr;
-  const bool prof = ctx->prof_on;
+  const int dup = ctx->dup_class;
   for (auto& g : ctx->graphs)
-    if (!memcmp(g.key, key, sizeof key) && g.dt_fixed == dt_fixed && same_params(g.prm, *prm) && g.prof == prof)
+    if (!memcmp(g.key, key, sizeof key) && g.dt_fixed == dt_fixed && same_params(g.prm, *prm) && g.dup == dup)
       sg = &g;
   if (!sg) {
-    if (ctx->graphs.size() >= 8) {
+    if (ctx->graphs.size() >= 16) {
       for (auto& g : ctx->graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
       ctx->graphs.clear();
@@ -1945,7 +1945,7 @@ static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_
     memcpy(sg->key, key, sizeof key);
     sg->dt_fixed = dt_fixed;
     sg->prm = *prm;
-    sg->prof = prof;
+    sg->dup = dup;
   }
   // the context's very first step runs as plain launches (warms every lazy init: kernel
   // attributes, occupancy queries, workspace sizes); every later new buffer/parameter set is
@@ -1956,7 +1956,7 @@ static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_
   }
   ++sg->seen;
   if (!sg->exec) {
-    if (prof) sg->gprof = std::make_shared<hx_ctx::GProf>();
+    if (dup >= 0) sg->gprof = std::make_shared<hx_ctx::GProf>();
     int rc = capture_step(ctx, prm, dt_fixed, x, v, e, x_out, v_out, e_out, &sg->exec, sg->gprof.get());
     if (rc) return rc;
   }
@@ -1974,7 +1974,7 @@ static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_
   const StatusDev s0 = ctx->h_st[0], s1 = ctx->h_st[1], s2 = ctx->h_st[2];
   const CGDev c0 = ctx->h_cg[0], c1 = ctx->h_cg[1];
   ctx->launches += 11 + 2 * (long long)(c0.iters + c1.iters);
-  if (prof && sg->gprof) {
+  if (dup >= 0 && sg->gprof) {
     const int it[2] = {c0.iters, c1.iters};
     gprof_collect(ctx, sg->gprof.get(), it);
   }
@@ -2335,6 +2335,58 @@ extern "C" int hx_fp64_peak(double* tflops) {
   if (st) cudaStreamDestroy(st);
   if (out) cudaFree(out);
   return rc;
+}
+
+// duplicate the kernel node just captured on ctx->stream and make it the capture's new
+// tail.  The node pass (K_CGNODE) is not idempotent (r -= alpha Ap): its duplicate is a
+// dry copy whose outputs (x, r, (z, p) pairs, r.z partials) go to scratch buffers -- the
+// same loads, arithmetic and store volume; its CG-state writes repeat the original's.
+static int dup_last_node(hx_ctx* c, int cls) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  if (cudaStreamGetCaptureInfo(c->stream, &cs, nullptr, &g, &deps, &nd) != cudaSuccess || nd != 1)
+    return HX_ECUDA;
+  cudaGraphNode_t last = deps[0];
+  cudaGraphNodeType ty;
+  if (cudaGraphNodeGetType(last, &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel) return HX_ECUDA;
+  cudaKernelNodeParams kp;
+  if (cudaGraphKernelNodeGetParams(last, &kp) != cudaSuccess) return HX_ECUDA;
+  NodeArgs dry;
+  void* args2[2];
+  if (cls == K_CGNODE) {
+    const long long nv = c->nn * 3;
+    if (!c->dup_scratch) return HX_ECUDA;  // allocated by hx_prof_dup (no cudaMalloc while capturing)
+    memcpy(&dry, kp.kernelParams[0], sizeof dry);
+    dry.x = c->dup_scratch;
+    dry.r = c->dup_scratch + nv;
+    dry.pbuf0 = c->dup_scratch + 2 * nv;
+    dry.pbuf1 = c->dup_scratch + 4 * nv;
+    dry.partials = c->dup_scratch + 6 * nv;
+    args2[0] = &dry;
+    args2[1] = kp.kernelParams[1];
+    kp.kernelParams = args2;
+  }
+  cudaGraphNode_t node;
+  if (cudaGraphAddKernelNode(&node, g, &last, 1, &kp) != cudaSuccess) return HX_ECUDA;
+  cudaGraphKernelNodeCopyAttributes(node, last);  // L2 access-policy window of the original
+  cudaGetLastError();
+  if (cudaStreamUpdateCaptureDependencies(c->stream, &node, 1, cudaStreamSetCaptureDependencies) != cudaSuccess)
+    return HX_ECUDA;
+  return HX_OK;
+}
+
+// step graphs captured from now on duplicate every launch of kernel class `cls`
+// (-1: plain graphs); hx_prof_read(cls) then counts the duplicates that did work
+extern "C" int hx_prof_dup(hx_ctx* ctx, int cls) {
+  if (!ctx || cls < -1 || cls > K_OTHER) return HX_EINVAL;
+  if (cls == K_CGNODE && !ctx->dup_scratch) {
+    CK(cudaSetDevice(ctx->device));
+    CK(dalloc(&ctx->dup_scratch, (size_t)6 * ctx->nn * 3 + 2 * (size_t)ctx->preg));
+  }
+  ctx->dup_class = cls;
+  return HX_OK;
 }
 
 extern "C" int hx_prof_enable(hx_ctx* ctx, int on) {

@@ -439,4 +439,256 @@ __global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : MASS_BRICK_MINB) 
   cg_partial(a.partials, &a.cg->nparts_m, block_sum<M::NT>(acc, red));
 }
 
+
+// ---------------------------------------------------------------------------
+// Pipelined variant (MASS_PIPE): the (z, p) pairs of a pass are staged raw into a
+// separate shared pair image with cp.async (16-byte copies, no registers), one pass
+// ahead: pass 0's copies are issued before the CG prologue (the r.z reduction and stop
+// test of cg_mass_begin) and pass s+1's as soon as phase 1 of pass s has consumed the
+// image, so the gather latency hides behind the prologue and phases 2-4.  Phase 1 forms
+// p_k = z + beta p_{k-1} from the pair image.  The staging image aliases the T planes
+// (each plane thread reads its own plane into registers before overwriting it).
+#ifndef MASS_PIPE_NT
+#define MASS_PIPE_NT 128
+#endif
+#ifndef MASS_PIPE_MINB
+#define MASS_PIPE_MINB 4
+#endif
+#ifndef MASS_PIPE_D
+#define MASS_PIPE_D 0
+#endif
+template <int P, int NC>
+struct MassPipeCfg {
+  static constexpr int NT = MASS_PIPE_NT;
+  static constexpr int D1 = P + 1, Q = P + 2, QQ = Q * Q, DD = D1 * D1, NL = D1 * DD, NQ = Q * QQ;
+  static constexpr int PLN = NC * D1;          // planes per element
+  static constexpr int EPC = NT / PLN;         // elements per pass
+  static constexpr int ROWI = D1 * NC;         // pairs per node row
+  static constexpr int ELI = DD * ROWI;        // pairs per element (= E entries)
+  static constexpr int GP = QQ, GS = PLN * GP; // staging (in the T planes)
+  static constexpr int TS = PLN * QQ;
+  // pair image padding (in pairs): phase 1's 16-byte reads of 8 consecutive plane lanes
+  // (c, dz) hit distinct 16-byte bank groups when the dz stride is = ZM (mod 8) and the
+  // element stride = 1 (mod 8)
+  static constexpr int ZM = P == 2 ? 3 : (P == 3 ? 2 : 5);
+  static constexpr int up8(int v, int m) { return v + (((m - v) % 8) + 8) % 8; }
+  static constexpr int ZS = up8(D1 * ROWI, ZM);
+  static constexpr int ELIP = up8(D1 * ZS, 1);
+  static constexpr int DS = MASS_PIPE_D ? NQ : 0;  // D of the pass staged too
+  static constexpr size_t bytes = sizeof(double) * ((size_t)EPC * (TS + 2 * ELIP) + (size_t)EPC * DS);
+};
+
+template <int P, int NC, bool PEER = false>
+__global__ void __launch_bounds__(MASS_PIPE_NT, MASS_PIPE_MINB * 128 / MASS_PIPE_NT) k_mass_brick2(MassBrickArgs a) {
+  using M = MassPipeCfg<P, NC>;
+  constexpr int D1 = M::D1, Q = M::Q, QQ = M::QQ, DD = M::DD, NL = M::NL, NQ = M::NQ;
+  constexpr int PLN = M::PLN, EPC = M::EPC, GP = M::GP, GS = M::GS, ROWI = M::ROWI, ELI = M::ELI;
+  constexpr int ZS = M::ZS, ELIP = M::ELIP;
+  constexpr int SLOTS = (ELI + M::NT - 1) / M::NT;
+  const double* cB = c_B[P - 1];
+  extern __shared__ __align__(16) double smem[];
+  double* sT = smem;                                          // T image [el][c][dz][qy*Q+qx]
+  double* sG = smem;                                          // staging (aliases T)
+  double2* sP = reinterpret_cast<double2*>(smem + EPC * M::TS);  // pair image [el][dz][dy][dx][c]
+#if MASS_PIPE_D
+  double* sD = smem + EPC * (M::TS + 2 * ELIP);                     // D of the pass
+#endif
+  __shared__ double red[32];
+  CGDev* g = a.cg;
+  if (!g->active) return;
+  const int t = threadIdx.x;
+  const int k0 = g->it_m;
+  const double2* po = reinterpret_cast<const double2*>((k0 & 1) ? a.pbuf0 : a.pbuf1);
+  // per-thread slots (pass invariant): global pair offset from the element's first node,
+  // and the element-major E offset of the same slot
+  int goff[SLOTS], eoff[SLOTS], poff[SLOTS], soff[SLOTS];
+#pragma unroll
+  for (int h = 0; h < SLOTS; ++h) {
+    const int it = h * M::NT + t;
+    const int row = it / ROWI, s = it - row * ROWI;  // row = dz*D1 + dy
+    const int dx = s / NC, c = s - dx * NC;
+    const int dz = row / D1, dy = row - dz * D1;
+    goff[h] = (dx + dy * a.b.Nx + dz * (int)a.b.NxNy) * NC + c;
+    eoff[h] = (row * D1 + dx) * NC + c;
+    poff[h] = dz * ZS + dy * ROWI + s;
+    soff[h] = (c * D1 + dz) * GP + dy * D1 + dx;
+  }
+  const int ebeg = (int)(a.ne * blockIdx.x / gridDim.x);
+  const int len = (int)(a.ne * (blockIdx.x + 1) / gridDim.x) - ebeg;
+  const int npass = (len + EPC - 1) / EPC;
+  auto pass_range = [&](int ps, int& e0, int& nel) {
+    e0 = ebeg + len * ps / npass;
+    nel = ebeg + len * (ps + 1) / npass - e0;
+  };
+  auto element_base = [&](unsigned e) {
+    const unsigned ez = a.b.fnxy.div(e);
+    const unsigned r2 = e - ez * (unsigned)(a.b.nx * a.b.ny);
+    const unsigned ey = a.b.fnx.div(r2), ex = r2 - ey * (unsigned)a.b.nx;
+    return (int)(ex * P + (ey * P) * (unsigned)a.b.Nx + (ez * P) * (unsigned)a.b.NxNy);
+  };
+  // cp.async of a pass's pairs (element bases computed per (slot, element): no barrier)
+  auto issue = [&](int ps) {
+    int e0, nel;
+    pass_range(ps, e0, nel);
+    for (int el = 0; el < nel; ++el) {
+      const int base = element_base((unsigned)(e0 + el));
+#pragma unroll
+      for (int h = 0; h < SLOTS; ++h) {
+        const int it = h * M::NT + t;
+        if (it < ELI)
+          cp_async16d(reinterpret_cast<double*>(sP + el * ELIP + poff[h]),
+                      reinterpret_cast<const double*>(po + (base * NC + goff[h])));
+      }
+    }
+#if MASS_PIPE_D
+    cp_span<M::NT>(sD, a.D + (long long)e0 * NQ, nel * NQ, t);
+#endif
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (npass > 0) issue(0);
+  double beta;
+  int k;
+  if (!cg_mass_begin<M::NT, PEER>(g, red, beta, k, &a.pl)) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
+  }
+  double acc = 0.0;
+  const int pe = t / PLN, pr = t - pe * PLN;
+  const int pc = pr / D1, pz = pr - pc * D1;  // plane (c, dz)
+  for (int ps = 0; ps < npass; ++ps) {
+    int e0, nel;
+    pass_range(ps, e0, nel);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    // ---- phase 1 (planes): p = z + beta p_{k-1} from the pair image; x, y contractions
+    const bool pact = pe < nel;
+    if (pact) {
+      double u[DD];
+      const double2* pp = sP + pe * ELIP + pz * ZS + pc;
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < D1; ++dx) {
+          const double2 q = pp[dy * ROWI + dx * NC];
+          u[dy * D1 + dx] = __dadd_rn(q.x, __dmul_rn(beta, q.y));
+        }
+      double v[D1][Q];
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx) {
+          double s = 0.0;
+#pragma unroll
+          for (int dx = 0; dx < D1; ++dx) s = fma(cB[qx * D1 + dx], u[dy * D1 + dx], s);
+          v[dy][qx] = s;
+        }
+      double* T = sT + pe * M::TS + pr * QQ;
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy)
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx) {
+          double s = 0.0;
+#pragma unroll
+          for (int dy = 0; dy < D1; ++dy) s = fma(cB[qy * D1 + dy], v[dy][qx], s);
+          T[qy * Q + qx] = s;
+        }
+    }
+    __syncthreads();
+#if !MASS_PIPE_D
+    if (ps + 1 < npass) issue(ps + 1);  // the pair image is dead until the next pass
+#endif
+    // ---- phase 2 (columns): z, D, z^T for all components of a (qx, qy) column
+    for (int it = t; it < nel * QQ; it += M::NT) {
+      const int ce = it / QQ, l = it - ce * QQ;
+      double Dq[Q];
+#pragma unroll
+      for (int qz = 0; qz < Q; ++qz)
+#if MASS_PIPE_D
+        Dq[qz] = sD[ce * NQ + qz * QQ + l];
+#else
+        Dq[qz] = __ldg(a.D + (long long)(e0 + ce) * NQ + qz * QQ + l);
+#endif
+      double* base = sT + ce * M::TS + l;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        double col[D1];
+#pragma unroll
+        for (int dz = 0; dz < D1; ++dz) col[dz] = base[(c * D1 + dz) * QQ];
+        double w[Q];
+#pragma unroll
+        for (int qz = 0; qz < Q; ++qz) {
+          double s = 0.0;
+#pragma unroll
+          for (int dz = 0; dz < D1; ++dz) s = fma(cB[qz * D1 + dz], col[dz], s);
+          const double du = s * Dq[qz];
+          acc = fma(du, s, acc);
+          w[qz] = du;
+        }
+#pragma unroll
+        for (int dz = 0; dz < D1; ++dz) {
+          double s = 0.0;
+#pragma unroll
+          for (int qz = 0; qz < Q; ++qz) s = fma(cB[qz * D1 + dz], w[qz], s);
+          base[(c * D1 + dz) * QQ] = s;
+        }
+      }
+    }
+    __syncthreads();
+#if MASS_PIPE_D
+    if (ps + 1 < npass) issue(ps + 1);  // pair image and D of this pass are dead
+#endif
+    // ---- phase 3 (planes): y^T, x^T -> staging (own T plane, read into registers first)
+    if (pact) {
+      const double* T = sT + pe * M::TS + pr * QQ;
+      double Tq[QQ];
+#pragma unroll
+      for (int kk = 0; kk < QQ; ++kk) Tq[kk] = T[kk];
+      double v[D1][Q];
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx) {
+          double s = 0.0;
+#pragma unroll
+          for (int qy = 0; qy < Q; ++qy) s = fma(cB[qy * D1 + dy], Tq[qy * Q + qx], s);
+          v[dy][qx] = s;
+        }
+      double* o = sG + pe * GS + pr * GP;
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < D1; ++dx) {
+          double s = 0.0;
+#pragma unroll
+          for (int qx = 0; qx < Q; ++qx) s = fma(cB[qx * D1 + dx], v[dy][qx], s);
+          o[dy * D1 + dx] = s;
+        }
+    }
+    __syncthreads();
+    // ---- phase 4: copy-out (element-major, or node-sorted through the slot map)
+    if (a.slot) {
+      const int* sl = a.slot + e0 * NL;
+      for (int it = t; it < nel * NL; it += M::NT) {
+        const int el = it / NL, l = it - el * NL;
+        const int dz = l / DD, kk = l - dz * DD;
+        const long long pos = (long long)__ldg(sl + it) * NC;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) __stcg(a.evec + pos + c, sG[el * GS + (c * D1 + dz) * GP + kk]);
+      }
+    } else {
+      double* out = a.evec + e0 * (NL * NC);
+#pragma unroll
+      for (int h = 0; h < SLOTS; ++h) {
+        const int it = h * M::NT + t;
+        if (it < ELI) {
+#pragma unroll
+          for (int el = 0; el < EPC; ++el)
+            if (el < nel) __stcg(out + el * ELI + eoff[h], sG[el * GS + soff[h]]);
+        }
+      }
+    }
+  }
+  cg_partial(a.partials, &g->nparts_m, block_sum<M::NT>(acc, red));
+}
+
 }  // namespace hx

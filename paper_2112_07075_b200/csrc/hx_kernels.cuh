@@ -1400,9 +1400,9 @@ __global__ void __launch_bounds__(256, NODE_MINB) k_cg_node(NodeArgs a, SUM sum)
 
 // multi-GPU variant: the first trip's own-data loads are issued before the prologue's
 // world p.Ap handshake; interface nodes add the neighbours' partials afterwards
-template <int NC, class SUM>
+// (PEER = false: the same prologue overlap on one GPU, NODE_PF)
+template <int NC, class SUM, bool PEER = true>
 __global__ void __launch_bounds__(256, NODE_MINB) k_cg_node_peer(NodeArgs a, SUM sum) {
-  constexpr bool PEER = true;
   __shared__ double red[32];
   CGDev* g = a.cg;
   if (!g->active) return;
