@@ -463,6 +463,22 @@ def run_distributed(args, world, rank, local):
     tt = torch.tensor([tot], dtype=torch.float64, device="cpu" if dist.get_backend() == "gloo" else "cuda")
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     tot = float(tt.item())
+    if args.ktime == "dup":
+        kpass = {"method": "dup",
+                 "note": "per-launch kernel cost in the step graph by duplication: the same timed steps replayed "
+                         "from the post-warm-up snapshot with every launch of one class doubled (CG node pass: "
+                         "dry twin writing to scratch); avg_us = (T_dup - T_plain) / working duplicates, CUDA "
+                         "events around whole steps",
+                 "ms_per_step_plain_replay": prof_ms / args.steps}
+    else:
+        kpass = {"method": "events",
+                 "note": "the same timed steps replayed from the post-warm-up snapshot as plain stream launches; "
+                         "the library records a CUDA event pair on the launching stream around every launch; "
+                         "share = class time / replay step time",
+                 "ms_per_step_replay": prof_ms / args.steps}
+        if ktimes_dup:
+            kpass["graph_dup_avg_us"] = {k: 1e3 * t / c for k, (t, c) in ktimes_dup.items()}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": V_global * args.steps / (tot / 1e3) / 1e6, "unit": UNIT, "n_gpus": world,
@@ -496,6 +512,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--peer-self", action="store_true",
                     help="N=1 with the multi-GPU exchange launches active on a one-rank partition")
+    ap.add_argument("--ktime", default="events", choices=["events", "dup", "both"],
+                    help="per-kernel timing: CUDA events around every launch of a plain-launch replay of "
+                         "the timed steps (events), in-graph duplication (dup), or both")
     ap.add_argument("--host-cg", action="store_true",
                     help="N>1: the host-driven distributed step instead of the device-resident step graph")
     args = ap.parse_args()
@@ -652,13 +671,46 @@ def main():
         lib.hx_prof_dup(h, -1)
         return tot, cnt
 
-    prof_base, _ = replay(-1)
-    ktimes = {}
-    for k, name in enumerate(K_NAMES[:6]):
-        tot, cnt = replay(k)
-        if cnt:
-            ktimes[name] = (max(tot - prof_base, 0.0), cnt)  # ms over the K steps, working launches
-    prof_ms = prof_base
+    # ---- kernel breakdown by CUDA events around every launch: the same timed steps
+    # replayed from the snapshot as plain stream launches (HX graph off while profiling),
+    # the library recording an event pair on the launching stream around each launch
+    def replay_events():
+        restore()
+        torch.cuda.synchronize()
+        lib.hx_prof_enable(h, 1)
+        lib.hx_prof_reset(h)
+        tot = 0.0
+        for _ in range(args.steps):
+            restart_if_due()
+            flush.zero_()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            dev_step()
+            ev1.record(stream)
+            ev1.synchronize()
+            tot += ev0.elapsed_time(ev1)
+        out = {}
+        for k, name in enumerate(K_NAMES):
+            t_, c_ = _lib.C.c_double(), _lib.C.c_int64()
+            lib.hx_prof_read(h, k, _lib.C.byref(t_), _lib.C.byref(c_))
+            if c_.value:
+                out[name] = (float(t_.value), int(c_.value))
+        lib.hx_prof_enable(h, 0)
+        return tot, out
+
+    ev_ms, ev_times = replay_events()
+    ktimes_dup = {}
+    prof_base = None
+    if args.ktime in ("dup", "both"):
+        prof_base, _ = replay(-1)
+        for k, name in enumerate(K_NAMES[:6]):
+            tot, cnt = replay(k)
+            if cnt:
+                ktimes_dup[name] = (max(tot - prof_base, 0.0), cnt)  # ms over the K steps, working launches
+    if args.ktime == "dup":
+        ktimes, prof_ms = ktimes_dup, prof_base
+    else:
+        ktimes, prof_ms = ev_times, ev_ms
     total_ms = sum(step_ms)
     ms_per_step = total_ms / args.steps
     value = V * args.steps / (total_ms / 1e3) / 1e6
@@ -753,6 +805,22 @@ def main():
                          f"{len(times)} steps after 1 warm-up; {src}; {cores} BLAS threads (the fastest count) on "
                          f"{os.cpu_count()} x {cpu_model()}"}
 
+    if args.ktime == "dup":
+        kpass = {"method": "dup",
+                 "note": "per-launch kernel cost in the step graph by duplication: the same timed steps replayed "
+                         "from the post-warm-up snapshot with every launch of one class doubled (CG node pass: "
+                         "dry twin writing to scratch); avg_us = (T_dup - T_plain) / working duplicates, CUDA "
+                         "events around whole steps",
+                 "ms_per_step_plain_replay": prof_ms / args.steps}
+    else:
+        kpass = {"method": "events",
+                 "note": "the same timed steps replayed from the post-warm-up snapshot as plain stream launches; "
+                         "the library records a CUDA event pair on the launching stream around every launch; "
+                         "share = class time / replay step time",
+                 "ms_per_step_replay": prof_ms / args.steps}
+        if ktimes_dup:
+            kpass["graph_dup_avg_us"] = {k: 1e3 * t / c for k, (t, c) in ktimes_dup.items()}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -768,11 +836,7 @@ def main():
                                           "step 42 in the reference algorithm)"},
                        "cg_iterations": cg_iters, "dt": dts},
             "e2e": e2e, "gpu_launches": launches, "roofline": roof, "kernels": kern,
-            "kernel_pass": {"note": "per-launch kernel cost in the step graph by duplication: the same timed "
-                                    "steps replayed from the post-warm-up snapshot with every launch of one "
-                                    "class doubled (CG node pass: dry twin writing to scratch); avg_us = "
-                                    "(T_dup - T_plain) / working duplicates, CUDA events around whole steps",
-                            "ms_per_step_plain_replay": prof_ms / args.steps},
+            "kernel_pass": kpass,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }

@@ -26,6 +26,8 @@
 #include "hx_rates.cuh"
 #include "hx_remap.cuh"
 #include "hx_peer.cuh"
+#include "hx_tma.cuh"
+#include "hx_node.cuh"
 
 using namespace hx;
 
@@ -73,6 +75,9 @@ struct hx_ctx {
   // stage buffers for the step driver
   double *xm = nullptr, *vm = nullptr, *em = nullptr;
   double *dv0 = nullptr, *dv1 = nullptr, *de0 = nullptr, *de1 = nullptr;
+  // TMA tensor maps over the CG pair buffers (p0, p1) per component count (k_mass_tma)
+  CUtensorMap tm_pair[4][2];
+  int tm_state[4] = {0, 0, 0, 0};  // 0 not built, 1 ok, -1 unavailable
   // host mirrors
   CGDev* h_cg = nullptr;
   StatusDev* h_st = nullptr;
@@ -1073,8 +1078,53 @@ static int with_node_sum(hx_ctx* ctx, int nc, const double* evec, F&& f) {
   return f(CsrSum<3>{ctx->off, evec}, IC<3>());
 }
 
+template <class S>
+struct BrickOrder {
+  static constexpr int value = 0;
+};
+template <int P, int NC>
+struct BrickOrder<BrickSum<P, NC>> {
+  static constexpr int value = P;
+};
+
+// HX_NODE_ROW=1: the warp-per-row-segment brick node pass (k_cg_node_row).  Measured on the
+// 3D Sedov Q3 bench: 20.0 us vs 16.5 us for k_cg_node (same instruction count, fewer loads
+// in flight per thread), so opt-in
+static int g_node_row = -1;
+
+// single-GPU brick node pass, one warp per node-row segment (hx_node.cuh)
+template <int P, int NC>
+static bool launch_node_row(hx_ctx* ctx, const NodeArgs& na, int* rc) {
+  if (g_node_row < 0) {
+    const char* v = getenv("HX_NODE_ROW");
+    g_node_row = (v && v[0] == '1') ? 1 : 0;
+  }
+  constexpr int MS = 4;
+  constexpr int SEGMAX = 32 * MS / NC;
+  if (!g_node_row || ctx->peer) return false;
+  const int Nx = ctx->bk.Nx;
+  const int nseg_row = (Nx + SEGMAX - 1) / SEGMAX;
+  const int seg = (Nx + nseg_row - 1) / nseg_row;
+  auto k = k_cg_node_row<P, NC, MS>;
+  static unsigned cap = 0;
+  if (!cap) cap = persistent_grid(k, 256, 0, 1ll << 40);
+  const long long nrows = (long long)ctx->bk.Ny * (ctx->bk.nz * P + 1);
+  const unsigned need = gblocks(nrows * nseg_row, 8);
+  prof_begin(ctx, K_CGNODE);
+  k<<<std::min(need, cap), 256, 0, ctx->stream>>>(na, ctx->bk, seg, nseg_row);
+  prof_end(ctx);
+  const cudaError_t e = cudaGetLastError();
+  *rc = e == cudaSuccess ? HX_OK : fail(ctx, HX_ECUDA, "k_cg_node_row launch: %s", cudaGetErrorString(e));
+  ++ctx->launches;
+  return true;
+}
+
 template <int NC, class SUM>
 static int launch_cg_nodes(hx_ctx* ctx, const NodeArgs& na, SUM sum, bool init) {
+  if constexpr (BrickOrder<SUM>::value > 0) {
+    int rc = HX_OK;
+    if (!init && launch_node_row<BrickOrder<SUM>::value, NC>(ctx, na, &rc)) return rc;
+  }
 #ifndef NODE_PF
 #define NODE_PF 0
 #endif
@@ -1101,7 +1151,14 @@ static int launch_cg_nodes(hx_ctx* ctx, const NodeArgs& na, SUM sum, bool init) 
 #define MASS_PIPE 0
 #endif
 template <int P, int NC>
+static bool launch_mass_tma(hx_ctx* ctx, const MassBrickArgs& a, int* rc);
+
+template <int P, int NC>
 static int launch_mass_brick(hx_ctx* ctx, const MassBrickArgs& a) {
+  {
+    int rc = HX_OK;
+    if (launch_mass_tma<P, NC>(ctx, a, &rc)) return rc;
+  }
   if (MASS_PIPE) {
     using M = MassPipeCfg<P, NC>;
     auto k = ctx->peer ? k_mass_brick2<P, NC, true> : k_mass_brick2<P, NC, false>;
@@ -1126,6 +1183,87 @@ static int launch_mass_brick(hx_ctx* ctx, const MassBrickArgs& a) {
   prof_end(ctx);
   CKL();
   return HX_OK;
+}
+
+// ---- TMA-staged brick mass (hx_tma.cuh): tensor maps over the (z, p) pair buffers
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)f;
+    cudaGetLastError();
+  }
+  return fn;
+}
+
+// pair array (NN, NC, 2) doubles viewed as (Nx*NC*2, Ny, Nz); box = one pass's node box
+template <int P, int NC>
+static bool pair_maps(hx_ctx* ctx) {
+  int& stt = ctx->tm_state[NC];
+  if (stt) return stt > 0;
+  stt = -1;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  using M = MassTmaCfg<P, NC>;
+  const cuuint64_t row = (cuuint64_t)ctx->bk.Nx * NC * 2;
+  const cuuint64_t gdim[3] = {row, (cuuint64_t)ctx->bk.Ny, (cuuint64_t)(ctx->bk.nz * P + 1)};
+  const cuuint64_t gstr[2] = {row * 8, row * 8 * (cuuint64_t)ctx->bk.Ny};
+  const cuuint32_t box[3] = {(cuuint32_t)M::ROWD, (cuuint32_t)M::D1, (cuuint32_t)M::D1};
+  const cuuint32_t est[3] = {1, 1, 1};
+  double* bufs[2] = {ctx->p0, ctx->p1};
+  for (int b = 0; b < 2; ++b)
+    if (enc(&ctx->tm_pair[NC][b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, bufs[b], gdim, gstr, box, est,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  stt = 1;
+  return true;
+}
+
+// HX_MASS_TMA=1: the TMA-staged brick mass kernel (k_mass_tma).  Measured on the 3D Sedov
+// Q3 bench (profiles/r2/r2f_*, r2g_*): 27.4 us vs 26.0 us for k_mass_brick, so opt-in
+static int g_mass_tma = -1;
+
+template <int P, int NC>
+static bool launch_mass_tma(hx_ctx* ctx, const MassBrickArgs& a, int* rc) {
+  if (g_mass_tma < 0) {
+    const char* v = getenv("HX_MASS_TMA");
+    g_mass_tma = (v && v[0] == '1') ? 1 : 0;
+  }
+  if constexpr (NC != 3) {
+    return false;
+  } else {
+  if (!g_mass_tma || a.slot || ((unsigned long long)a.D & 15ull)) return false;
+  if (!pair_maps<P, NC>(ctx)) return false;
+  using M = MassTmaCfg<P, NC>;
+  auto k = ctx->peer ? k_mass_tma<P, NC, true> : k_mass_tma<P, NC, false>;
+  *rc = HX_OK;
+  if (smem_attr(k, M::bytes) != cudaSuccess) {
+    *rc = fail(ctx, HX_ECUDA, "k_mass_tma: shared memory attribute");
+    return true;
+  }
+  static unsigned grids[2] = {0, 0};
+  unsigned& grid = grids[ctx->peer ? 1 : 0];
+  if (!grid) grid = persistent_grid(k, M::NT, M::bytes, 1ll << 40);
+  const int nseg = (ctx->bk.nx + M::EPC - 1) / M::EPC;
+  const long long units = (long long)nseg * ctx->bk.ny * ctx->bk.nz;
+  prof_begin(ctx, K_MASS);
+  k<<<(unsigned)std::min<long long>(grid, units), M::NT, M::bytes, ctx->stream>>>(a, ctx->tm_pair[NC][0],
+                                                                                   ctx->tm_pair[NC][1], nseg);
+  prof_end(ctx);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) *rc = fail(ctx, HX_ECUDA, "k_mass_tma launch: %s", cudaGetErrorString(e));
+  else ++ctx->launches;
+  return true;
+  }
 }
 
 static int mass_brick(hx_ctx* ctx, int nc, const MassBrickArgs& a) {
@@ -1332,7 +1470,9 @@ static int run_cg(hx_ctx* ctx, const double* D, const double* rhs, const double*
   rc = cg_launch_init(ctx, L);
   if (rc) return rc;
   int done_iters = 0;
-  int chunk = 8;
+  // profiling (hx_prof_enable): one iteration per poll, so that no launch past
+  // convergence (an early-exit launch) enters the per-kernel averages
+  int chunk = ctx->prof_on ? 1 : 8;
   while (true) {
     for (int i = 0; i < chunk; ++i) {
       rc = cg_launch_iter(ctx, L);
@@ -1343,7 +1483,7 @@ static int run_cg(hx_ctx* ctx, const double* D, const double* rhs, const double*
     CK(cudaStreamSynchronize(ctx->stream));
     if (!ctx->h_cg->active) break;
     if (done_iters > max_iter + 1) break;
-    chunk = std::min(chunk * 2, 64);
+    if (!ctx->prof_on) chunk = std::min(chunk * 2, 64);
   }
   rc = cg_launch_finish(ctx, L);
   if (rc) return rc;
