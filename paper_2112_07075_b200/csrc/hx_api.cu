@@ -70,6 +70,7 @@ struct hx_ctx {
   double* minv = nullptr;     // (NE, nt, nt)
   double* mdiag = nullptr;    // (NN)
   double* invd = nullptr;     // (NN, d)
+  double* invdn = nullptr;    // (NN) 1/mass-diagonal per node (node passes read it with the mask)
   uint8_t* mask = nullptr;    // (NN, d) phase mask
   bool has_mask = false;
   // stage buffers for the step driver
@@ -784,6 +785,7 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   ok &= dalloc(&ctx->qd0, (size_t)ne * nq) == cudaSuccess;
   ok &= dalloc(&ctx->minv, (size_t)ne * ctx->nt * ctx->nt) == cudaSuccess;
   ok &= dalloc(&ctx->mdiag, nn) == cudaSuccess;
+  ok &= dalloc(&ctx->invdn, nn) == cudaSuccess;
   ok &= dalloc(&ctx->xm, nv) == cudaSuccess;
   ok &= dalloc(&ctx->vm, nv) == cudaSuccess;
   ok &= dalloc(&ctx->em, (size_t)ne * ctx->nt) == cudaSuccess;
@@ -843,7 +845,7 @@ extern "C" int hx_destroy(hx_ctx* ctx) {
   cudaSetDevice(ctx->device);
   void* dev[] = {ctx->B,  ctx->G,    ctx->Bt,   ctx->wnd,  ctx->psi1, ctx->emap, ctx->off,   ctx->idx,
                  ctx->own, ctx->slot, ctx->emapf, ctx->emapf_api, ctx->arena, ctx->evec2, ctx->z, ctx->partials,
-                 ctx->hist, ctx->cg,  ctx->st,   ctx->dt,   ctx->scal, ctx->qd0,   ctx->minv,
+                 ctx->hist, ctx->cg,  ctx->st,   ctx->dt,   ctx->scal, ctx->qd0,   ctx->minv, ctx->invdn,
                  ctx->mdiag, ctx->xm, ctx->vm,   ctx->em, ctx->gamma_e,
                  ctx->de0, ctx->de1, ctx->hx_x, ctx->hx_v, ctx->hx_e, ctx->hx_xo, ctx->hx_vo, ctx->hx_eo};
   for (void* p : dev)
@@ -979,6 +981,7 @@ extern "C" int hx_geometry(hx_ctx* ctx, const double* x, double* jac, double* de
 // ---------------------------------------------------------------------------
 // mass
 
+__global__ void k_recip(const double* in, long long n, double* out);
 __global__ void k_invdiag(const double* diag, const uint8_t* mask, int nc, long long nn, double* invd) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nn * nc) return;
@@ -1159,6 +1162,30 @@ static int launch_mass_brick(hx_ctx* ctx, const MassBrickArgs& a) {
     int rc = HX_OK;
     if (launch_mass_tma<P, NC>(ctx, a, &rc)) return rc;
   }
+  {
+    static int w2 = -1;  // HX_MASS_W2=1: warp-independent pair kernel (k_mass_w2)
+    if (w2 < 0) {
+      const char* v = getenv("HX_MASS_W2");
+      w2 = v ? atoi(v) : 0;
+    }
+    if (w2 && !a.slot && NC * (P + 1) * 2 <= 32) {
+      using M = MassW2Cfg<P, NC>;
+      const bool pf = w2 == 2;  // HX_MASS_W2=2: with the cp.async prefetch of the next pair
+      auto k = pf ? (ctx->peer ? k_mass_w2<P, NC, true, true> : k_mass_w2<P, NC, false, true>)
+                  : (ctx->peer ? k_mass_w2<P, NC, true> : k_mass_w2<P, NC, false>);
+      const size_t bytes = pf ? M::bytes_pf : M::bytes;
+      CK(smem_attr(k, bytes));
+      static unsigned grids[4] = {0, 0, 0, 0};
+      unsigned& grid = grids[(ctx->peer ? 1 : 0) + (pf ? 2 : 0)];
+      if (!grid) grid = persistent_grid(k, M::NT, bytes, 1ll << 40);
+      const long long pairs = (ctx->ne + 1) / 2;
+      prof_begin(ctx, K_MASS);
+      k<<<(unsigned)std::min<long long>(grid, (pairs + M::WARPS - 1) / M::WARPS), M::NT, bytes, ctx->stream>>>(a);
+      prof_end(ctx);
+      CKL();
+      return HX_OK;
+    }
+  }
   if (MASS_PIPE) {
     using M = MassPipeCfg<P, NC>;
     auto k = ctx->peer ? k_mass_brick2<P, NC, true> : k_mass_brick2<P, NC, false>;
@@ -1257,7 +1284,7 @@ static bool launch_mass_tma(hx_ctx* ctx, const MassBrickArgs& a, int* rc) {
   const long long units = (long long)nseg * ctx->bk.ny * ctx->bk.nz;
   prof_begin(ctx, K_MASS);
   k<<<(unsigned)std::min<long long>(grid, units), M::NT, M::bytes, ctx->stream>>>(a, ctx->tm_pair[NC][0],
-                                                                                   ctx->tm_pair[NC][1], nseg);
+      a.pbuf1 == a.pbuf0 ? ctx->tm_pair[NC][0] : ctx->tm_pair[NC][1], nseg);
   prof_end(ctx);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) *rc = fail(ctx, HX_ECUDA, "k_mass_tma launch: %s", cudaGetErrorString(e));
@@ -1307,6 +1334,15 @@ static int cg_prepare(hx_ctx* ctx, CGDev* cg, const double* D, const double* rhs
   na.evec = evec_rhs ? evec_rhs : ctx->evec;
   na.mask = mask;
   na.invd = invd;
+  // the phase's momentum solve: per-node 1/diag (bit-identical z; a third of the bytes)
+  static int inode = -1, inplace = -1;
+  if (inode < 0) {
+    const char* v = getenv("HX_INVD_NODE");
+    inode = (v && v[0] == '0') ? 0 : 1;
+    const char* w = getenv("HX_PAIRS_INPLACE");
+    inplace = (w && w[0] == '0') ? 0 : 1;
+  }
+  na.invdn = (inode && invd == ctx->invd && nc == ctx->dim) ? ctx->invdn : nullptr;
   na.x = x;
   na.r = ctx->r;
   na.z = ctx->z;
@@ -1344,6 +1380,14 @@ static int cg_prepare(hx_ctx* ctx, CGDev* cg, const double* D, const double* rhs
   L.nc = nc;
   L.mb = MassBrickArgs{ctx->p0, ctx->p1, D, ctx->ne, ctx->evec, ctx->elem_major ? nullptr : ctx->slot, cg,
                        ctx->partials + preg, ctx->bk, ctx->pl};
+  // (z, p) pairs updated in place (HX_PAIRS_INPLACE=0: ping-pong): within a node launch
+  // every pair is read and rewritten by the same thread, and the mass launches read them
+  // only between node launches -- one 16 B/dof buffer less in the L2 working set
+  if (inplace) {
+    na.pbuf1 = na.pbuf0;
+    ma.pbuf1 = ma.pbuf0;
+    L.mb.pbuf1 = L.mb.pbuf0;
+  }
   return HX_OK;
 }
 
@@ -1441,8 +1485,8 @@ static int cg_launch_iter(hx_ctx* ctx, CGLaunch& L) {
 
 static int cg_launch_finish(hx_ctx* ctx, CGLaunch& L) {
   const long long n = ctx->nn * L.nc;
-  k_cg_finish<<<capg(std::min<unsigned>(gblocks(n, 256), 1184)), 256, 0, ctx->stream>>>(L.na.cg, ctx->p0, ctx->p1,
-                                                                                  L.na.x, n);
+  k_cg_finish<<<capg(std::min<unsigned>(gblocks(n, 256), 1184)), 256, 0, ctx->stream>>>(L.na.cg, L.na.pbuf0,
+                                                                                  L.na.pbuf1, L.na.x, n);
   CKL();
   return HX_OK;
 }
@@ -1734,6 +1778,8 @@ extern "C" int hx_phase_begin(hx_ctx* ctx, const double* x, const double* qdata0
   else CK(cudaMemsetAsync(ctx->mask, 0, nv, ctx->stream));
   ctx->has_mask = bcmask != nullptr;
   k_invdiag<<<gblocks(nv, 256), 256, 0, ctx->stream>>>(ctx->mdiag, ctx->mask, ctx->dim, ctx->nn, ctx->invd);
+  CKL();
+  k_recip<<<gblocks(ctx->nn, 256), 256, 0, ctx->stream>>>(ctx->mdiag, ctx->nn, ctx->invdn);
   CKL();
   rc = build_emapf(ctx, ctx->has_mask ? ctx->mask : nullptr, ctx->dim, ctx->emapf);
   if (rc) return rc;

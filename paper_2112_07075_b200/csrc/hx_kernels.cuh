@@ -1233,6 +1233,8 @@ struct NodeArgs {
   const double* evec;   // (NE, nl, NC)
   const uint8_t* mask;
   const double* invd;   // (NN, NC) 1/diag (masked rows -> 1)
+  const double* invdn;  // or null; else (NN) 1/diag per node, masked components -> 1 (the
+                        // same value for every unmasked component, a third of the bytes)
   double* x;
   double* r;
   double* z;            // unused by the CG (z lives in the (z, p) pairs)
@@ -1288,8 +1290,8 @@ __global__ void __launch_bounds__(256, 4) k_cg_init(NodeArgs a, SUM sum) {
         const long long n = j / NC;
         const int c = (int)(j - n * NC);
         s[u] = a.rhs ? a.rhs[j] : sum(n, c);
-        d[u] = a.invd[j];
         m[u] = a.mask && a.mask[j];
+        d[u] = a.invdn ? (m[u] ? 1.0 : __ldg(a.invdn + n)) : a.invd[j];
       }
     }
 #pragma unroll
@@ -1375,8 +1377,8 @@ __global__ void __launch_bounds__(256, NODE_MINB) k_cg_node(NodeArgs a, SUM sum)
         zp[u] = __ldcg(reinterpret_cast<const double2*>(po) + j);
         if (xk) xj[u] = __ldcg(a.x + j);
         rj[u] = __ldcg(a.r + j);
-        dj[u] = __ldg(a.invd + j);
         m[u] = a.mask && a.mask[j];
+        dj[u] = a.invdn ? (m[u] ? 1.0 : __ldg(a.invdn + n)) : __ldg(a.invd + j);
         s[u] = sum(n, c);
       }
     }
@@ -1435,8 +1437,8 @@ __global__ void __launch_bounds__(256, NODE_MINB) k_cg_node_peer(NodeArgs a, SUM
         zp[u] = __ldcg(reinterpret_cast<const double2*>(po) + j);
         if (xk) xj[u] = __ldcg(a.x + j);
         rj[u] = __ldcg(a.r + j);
-        dj[u] = __ldg(a.invd + j);
         m[u] = a.mask && a.mask[j];
+        dj[u] = a.invdn ? (m[u] ? 1.0 : __ldg(a.invdn + n)) : __ldg(a.invd + j);
         s[u] = sum(n, c);  // own (local elements) part
         hh[u] = PEER ? __ldg(ifx + n) : -1;
       }

@@ -71,8 +71,8 @@ __global__ void __launch_bounds__(256, NODE_ROW_MINB) k_cg_node_row(NodeArgs a, 
           zp[u] = __ldcg(reinterpret_cast<const double2*>(po) + j);
           if (xk) xj[u] = __ldcg(a.x + j);
           rj[u] = __ldcg(a.r + j);
-          dj[u] = __ldg(a.invd + j);
           msk[u] = a.mask && a.mask[j];
+          dj[u] = a.invdn ? (msk[u] ? 1.0 : __ldg(a.invdn + (j0 / NC + dn))) : __ldg(a.invd + j);
           int ex, lx, tx;
           axis_first<P>(i0 + dn, b.nx, ex, lx, tx);
           const unsigned p0 = (ebase + (unsigned)ex * NL + (unsigned)lx) * NC + (unsigned)c;

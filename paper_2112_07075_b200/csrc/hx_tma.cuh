@@ -311,3 +311,238 @@ __global__ void __launch_bounds__(MassTmaCfg<P, NC>::NT, MassTmaCfg<P, NC>::MINB
 }
 
 }  // namespace hx
+
+namespace hx {
+
+// ---------------------------------------------------------------------------
+// Warp-independent CG mass action on a brick (MASS_W2): every warp owns a contiguous
+// range of element PAIRS and runs all phases of a pair on its own -- the gather of the
+// pair's node rows into registers, the x/y plane stage, the z column stage and the
+// transposed plane stage -- with __syncwarp between phases and no CTA-wide barrier
+// (other warps of the SM keep the pipes busy while one waits on its gather).  Lane
+// (el, c, dz) < 24 owns a plane of the pair; the column stage runs 50 columns over the
+// 32 lanes.  Per-warp shared memory is the pair's T image (2 x NC*D1 planes of Q*Q),
+// reused as the staging image for coalesced E stores.  Same per-element arithmetic as
+// k_mass_brick (bit-identical E).
+#ifndef MASS_W2_WARPS
+#define MASS_W2_WARPS 4
+#endif
+#ifndef MASS_W2_MINB
+#define MASS_W2_MINB 4
+#endif
+template <int P, int NC>
+struct MassW2Cfg {
+  static constexpr int D1 = P + 1, Q = P + 2, QQ = Q * Q, DD = D1 * D1, NL = D1 * DD, NQ = Q * QQ;
+  static constexpr int PLN = NC * D1, EPW = 2;  // elements per warp pass
+  static_assert(EPW * PLN <= 32, "one lane per plane");
+  static constexpr int TP = QQ + (QQ % 2 == 0 ? 1 : 0);  // plane pitch (odd: conflict-free lanes)
+  static constexpr int TS = PLN * TP;                     // T image doubles per element
+  static constexpr int WS = EPW * TS;                     // per warp
+  static constexpr int WARPS = MASS_W2_WARPS, NT = 32 * WARPS;
+  // MASS_W2 prefetch variant: the next pair's node-row pairs (lane-private plane slots)
+  // and point data land by cp.async while the current pair is contracted
+  static constexpr int GB = EPW * PLN * DD * 2;     // gather buffer doubles ((z, p) pairs)
+  static constexpr int DB = ((EPW * NQ + 1) & ~1);  // D buffer doubles
+  static constexpr int WSP = WS + (WS & 1) + GB + DB;
+  static constexpr size_t bytes = sizeof(double) * (size_t)WARPS * WS;
+  static constexpr size_t bytes_pf = sizeof(double) * (size_t)WARPS * WSP;
+};
+
+template <int P, int NC, bool PEER = false, bool PF = false>
+__global__ void __launch_bounds__(MassW2Cfg<P, NC>::NT, MASS_W2_MINB) k_mass_w2(MassBrickArgs a) {
+  using M = MassW2Cfg<P, NC>;
+  constexpr int D1 = M::D1, Q = M::Q, QQ = M::QQ, DD = M::DD, NL = M::NL, NQ = M::NQ, PLN = M::PLN;
+  constexpr int TP = M::TP, TS = M::TS, EPW = M::EPW, NT = M::NT, ELI = NL * NC;
+  const double* cB = c_B[P - 1];
+  extern __shared__ __align__(16) double smem_w2[];
+  __shared__ double red[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* sT = smem_w2 + wid * (PF ? M::WSP : M::WS);
+  double2* sG = reinterpret_cast<double2*>(sT + M::WS + (M::WS & 1));  // PF: [el][plane][DD] pairs
+  double* sDb = sT + M::WS + (M::WS & 1) + M::GB;                       // PF: the pair's D
+  const int gw = blockIdx.x * M::WARPS + wid, nw = gridDim.x * M::WARPS;
+  const long long npairs = (a.ne + EPW - 1) / EPW;
+  const long long pb = npairs * gw / nw, pe_ = npairs * (gw + 1) / nw;
+  const int el = lane / PLN, pr = lane - el * PLN;
+  const int pc = pr / D1, pz = pr - pc * D1;  // plane (c, dz)
+  const bool lact = lane < EPW * PLN;
+  // node-row pair source of this lane's plane for the pair starting at element e0
+  auto plane_src = [&](const double* pbuf, long long e0) {
+    const unsigned e = (unsigned)(e0 + el);
+    const unsigned ez = a.b.fnxy.div(e);
+    const unsigned r2 = e - ez * (unsigned)(a.b.nx * a.b.ny);
+    const unsigned ey = a.b.fnx.div(r2), ex = r2 - ey * (unsigned)a.b.nx;
+    const unsigned n0 = ex * P + (ey * P) * (unsigned)a.b.Nx + (ez * P + pz) * (unsigned)a.b.NxNy;
+    return reinterpret_cast<const double2*>(pbuf) + (size_t)n0 * NC + pc;
+  };
+  auto nel_of = [&](long long e0) { return (int)(a.ne - e0 < EPW ? a.ne - e0 : EPW); };
+  auto issue_gather = [&](const double* pbuf, long long pi) {  // PF: lane-private plane slots
+    const long long e0 = pi * EPW;
+    if (lact && el < nel_of(e0)) {
+      const double2* src = plane_src(pbuf, e0);
+      double2* dst = sG + (el * PLN + pr) * DD;
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < D1; ++dx)
+          cp_async16d(reinterpret_cast<double*>(dst + dy * D1 + dx),
+                      reinterpret_cast<const double*>(src + (dy * a.b.Nx + dx) * NC));
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto issue_d = [&](long long pi) {  // PF: the pair's D (contiguous; 16-byte chunks when aligned)
+    const long long e0 = pi * EPW;
+    const int n = nel_of(e0) * NQ;
+    cp_span<32>(sDb, a.D + e0 * NQ, n, lane);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if constexpr (PF) {
+    if (!a.cg->active) return;
+    const int k0 = a.cg->it_m;
+    if (pb < pe_) {
+      issue_gather((k0 & 1) ? a.pbuf0 : a.pbuf1, pb);  // lands during the prologue
+      issue_d(pb);
+    }
+  }
+  double beta;
+  int k;
+  if (!cg_mass_begin<NT, PEER>(a.cg, red, beta, k, &a.pl)) {
+    if constexpr (PF) asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
+  }
+  const double* po = (k & 1) ? a.pbuf0 : a.pbuf1;
+  double acc = 0.0;
+  for (long long pi = pb; pi < pe_; ++pi) {
+    const long long e0 = pi * EPW;
+    const int nel = nel_of(e0);
+    const bool pact = lact && el < nel;
+    if constexpr (PF) {
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncwarp();
+    }
+    // ---- phase 1 (lane = plane): the plane's node row pairs, p = z + beta p_{k-1},
+    // x and y contractions -> T
+    if (pact) {
+      double2 q[DD];
+      if constexpr (PF) {
+        const double2* g = sG + (el * PLN + pr) * DD;
+#pragma unroll
+        for (int i = 0; i < DD; ++i) q[i] = g[i];
+      } else {
+        const double2* src = plane_src(po, e0);
+#pragma unroll
+        for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+          for (int dx = 0; dx < D1; ++dx) q[dy * D1 + dx] = __ldcg(src + (dy * a.b.Nx + dx) * NC);
+      }
+      double u[DD];
+#pragma unroll
+      for (int i = 0; i < DD; ++i) u[i] = __dadd_rn(q[i].x, __dmul_rn(beta, q[i].y));
+      double v[D1][Q];
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx) {
+          double s = 0.0;
+#pragma unroll
+          for (int dx = 0; dx < D1; ++dx) s = fma(cB[qx * D1 + dx], u[dy * D1 + dx], s);
+          v[dy][qx] = s;
+        }
+      double* T = sT + el * TS + pr * TP;
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy)
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx) {
+          double s = 0.0;
+#pragma unroll
+          for (int dy = 0; dy < D1; ++dy) s = fma(cB[qy * D1 + dy], v[dy][qx], s);
+          T[qy * Q + qx] = s;
+        }
+    }
+    __syncwarp();
+    if constexpr (PF) {
+      if (pi + 1 < pe_) issue_gather(po, pi + 1);  // the gather slots are consumed
+    }
+    // ---- phase 2 (lane = column): z, D, z^T for all components of a (qx, qy) column
+    for (int it = lane; it < nel * QQ; it += 32) {
+      const int ce = it / QQ, l = it - ce * QQ;
+      double Dq[Q];
+      if constexpr (PF) {
+#pragma unroll
+        for (int qz = 0; qz < Q; ++qz) Dq[qz] = sDb[ce * NQ + qz * QQ + l];
+      } else {
+        const double* Dp = a.D + (e0 + ce) * NQ + l;
+#pragma unroll
+        for (int qz = 0; qz < Q; ++qz) Dq[qz] = __ldg(Dp + qz * QQ);
+      }
+      double* base = sT + ce * TS + l;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        double col[D1];
+#pragma unroll
+        for (int dz = 0; dz < D1; ++dz) col[dz] = base[(c * D1 + dz) * TP];
+        double ww[Q];
+#pragma unroll
+        for (int qz = 0; qz < Q; ++qz) {
+          double s = 0.0;
+#pragma unroll
+          for (int dz = 0; dz < D1; ++dz) s = fma(cB[qz * D1 + dz], col[dz], s);
+          const double du = s * Dq[qz];
+          acc = fma(du, s, acc);
+          ww[qz] = du;
+        }
+#pragma unroll
+        for (int dz = 0; dz < D1; ++dz) {
+          double s = 0.0;
+#pragma unroll
+          for (int qz = 0; qz < Q; ++qz) s = fma(cB[qz * D1 + dz], ww[qz], s);
+          base[(c * D1 + dz) * TP] = s;
+        }
+      }
+    }
+    __syncwarp();
+    if constexpr (PF) {
+      if (pi + 1 < pe_) issue_d(pi + 1);  // the D buffer is consumed
+    }
+    // ---- phase 3 (lane = plane): y^T, x^T -> staging over the lane's own plane
+    if (pact) {
+      double* T = sT + el * TS + pr * TP;
+      double Tq[QQ];
+#pragma unroll
+      for (int kk = 0; kk < QQ; ++kk) Tq[kk] = T[kk];
+      double v[D1][Q];
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx) {
+          double s = 0.0;
+#pragma unroll
+          for (int qy = 0; qy < Q; ++qy) s = fma(cB[qy * D1 + dy], Tq[qy * Q + qx], s);
+          v[dy][qx] = s;
+        }
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < D1; ++dx) {
+          double s = 0.0;
+#pragma unroll
+          for (int qx = 0; qx < Q; ++qx) s = fma(cB[qx * D1 + dx], v[dy][qx], s);
+          T[dy * D1 + dx] = s;
+        }
+    }
+    __syncwarp();
+    // ---- copy-out: the pair's E block (element-major [e][l][c], contiguous) from the
+    // plane images, coalesced stores
+    double* out = a.evec + e0 * ELI;
+    for (int it = lane; it < nel * ELI; it += 32) {
+      const int ce = it / ELI, r = it - ce * ELI;
+      const int l = r / NC, c = r - l * NC;
+      const int dz = l / DD, kk = l - dz * DD;
+      __stcg(out + it, sT[ce * TS + (c * D1 + dz) * TP + kk]);
+    }
+    __syncwarp();
+  }
+  cg_partial(a.partials, &a.cg->nparts_m, block_sum<NT>(acc, red));
+}
+
+}  // namespace hx
