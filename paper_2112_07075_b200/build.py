@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "hx_api.cu")
-DEPS = [os.path.join(HERE, "csrc", f) for f in ("hx_api.cu", "hx_core.cuh", "hx_kernels.cuh", "hx_brick.cuh", "hx_rates.cuh", "hx_remap.cuh", "hx_peer.cuh", "hx_tma.cuh", "hx_node.cuh")] + [
+DEPS = [os.path.join(HERE, "csrc", f) for f in ("hx_api.cu", "hx_core.cuh", "hx_kernels.cuh", "hx_brick.cuh", "hx_rates.cuh", "hx_remap.cuh", "hx_peer.cuh", "hx_tma.cuh", "hx_node.cuh", "hx_async.cuh")] + [
     os.path.join(ROOT, "include", "b200hydro.h")]
 OUT = os.path.join(HERE, "libb200hydro.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -67,7 +67,8 @@ struct hx_ctx {
   bool phase = false;
   double* Dm = nullptr;       // (NE, nq)
   double* qd0 = nullptr;      // (NE, nq)
-  double* minv = nullptr;     // (NE, nt, nt)
+  double* minv = nullptr;     // (NE, nt, nt), or packed lower triangles (NE, nt (nt + 1) / 2)
+  int minv_packed = 0;        // minv_packed<dim, p>(): the packed symmetric layout
   double* mdiag = nullptr;    // (NN)
   double* invd = nullptr;     // (NN, d)
   double* invdn = nullptr;    // (NN) 1/mass-diagonal per node (node passes read it with the mask)
@@ -533,7 +534,7 @@ template <int DIM, int P>
 struct LaunchMinv {
   static int run(hx_ctx* ctx, double* minv_ref) {
     using D = Disc<DIM, P>;
-    if constexpr (DIM == 3 && P <= 3) {
+    if constexpr (minv_packed<DIM, P>()) {  // k_minv_warp writes the packed layout
       constexpr int Q = P + 2, DT = P;
       const size_t wb = sizeof(double) * 8 * (D::NQ + DT * DT * Q * Q + DT * DT * DT * DT * Q);
       auto kw = k_minv_warp<P>;
@@ -783,7 +784,8 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   ok &= dalloc(&ctx->dt, 2) == cudaSuccess;
   ok &= dalloc(&ctx->scal, 16) == cudaSuccess;
   ok &= dalloc(&ctx->qd0, (size_t)ne * nq) == cudaSuccess;
-  ok &= dalloc(&ctx->minv, (size_t)ne * ctx->nt * ctx->nt) == cudaSuccess;
+  ctx->minv_packed = (ctx->dim == 3 && ctx->p <= 3) ? 1 : 0;  // == minv_packed<DIM, P>()
+  ok &= dalloc(&ctx->minv, (size_t)ne * (ctx->minv_packed ? tri(ctx->nt) : ctx->nt * ctx->nt)) == cudaSuccess;
   ok &= dalloc(&ctx->mdiag, nn) == cudaSuccess;
   ok &= dalloc(&ctx->invdn, nn) == cudaSuccess;
   ok &= dalloc(&ctx->xm, nv) == cudaSuccess;
@@ -1820,7 +1822,7 @@ extern "C" int hx_energy_solve(hx_ctx* ctx, const double* rhs, double* out) {
   if (!ctx || !rhs || !out || !ctx->phase) return HX_EINVAL;
   CK(cudaSetDevice(ctx->device));
   const long long n = ctx->ne * ctx->nt;
-  k_energy_solve<<<gblocks(n, 256), 256, 0, ctx->stream>>>(ctx->minv, rhs, ctx->nt, ctx->ne, out);
+  k_energy_solve<<<gblocks(n, 256), 256, 0, ctx->stream>>>(ctx->minv, rhs, ctx->nt, ctx->ne, out, ctx->minv_packed);
   CKL();
   return HX_OK;
 }

@@ -35,6 +35,14 @@ __device__ __forceinline__ void load_tables(const Tables& t, double* sB, double*
   for (int i = threadIdx.x; i < Q * DT; i += blockDim.x) sBt[i] = t.Bt[i];
 }
 
+// Packed symmetric storage of the inverse thermodynamic mass (3D, p <= 3, i.e. whenever
+// k_minv_warp builds it): the lower triangle row by row, entry (i, j <= i) at
+// i (i + 1) / 2 + j, nt (nt + 1) / 2 doubles per element (hydro.py:229-232: M_e is SPD, so
+// its inverse is symmetric; 378 instead of 729 doubles at nt = 27).
+template <int DIM, int P>
+__host__ __device__ constexpr bool minv_packed() { return DIM == 3 && P <= 3; }
+__host__ __device__ constexpr int tri(int i) { return i * (i + 1) / 2; }
+
 struct StatusDev {
   unsigned long long inv_key;  // min over det<=0 points of q*NE+e (~0ull if none)
   unsigned long long clamps;   // e<0 clamps (hydro.py:275-278)
@@ -303,10 +311,11 @@ __global__ void __launch_bounds__(NT) k_rates(RatesArgs a) {
     a.evec[pos] = fout[c * NL + l];
   }
   // de = M_e^{-1} (F^T v)_e   (einsum "eij,ej->ei", hydro.py:343)
-  const double* mi = a.minv + e * NTH * NTH;
+  constexpr bool PK = minv_packed<DIM, P>();
+  const double* mi = a.minv + e * (PK ? tri(NTH) : NTH * NTH);
   for (int i = tid; i < NTH; i += NT) {
     double s = 0.0;
-    for (int j = 0; j < NTH; ++j) s = fma(mi[i * NTH + j], fv[j], s);
+    for (int j = 0; j < NTH; ++j) s = fma(mi[PK ? (j <= i ? tri(i) + j : tri(j) + i) : i * NTH + j], fv[j], s);
     a.de[e * NTH + i] = s;
   }
   (void)rMV;
@@ -1999,7 +2008,7 @@ __global__ void __launch_bounds__(256) k_minv_warp(const double* Dm /*(NE,nq)*/,
     if (lane < N) {
 #pragma unroll
       for (int i = 0; i < N; ++i) {
-        minv[(e * N + i) * N + lane] = col[i];
+        if (lane <= i) minv[e * tri(N) + tri(i) + lane] = col[i];  // packed lower triangle
         if (minv_ref) minv_ref[(e * N + i) * N + lane] = col[i];
       }
     }
@@ -2086,15 +2095,21 @@ __global__ void __launch_bounds__(128) k_minv(const double* Dm /*(NE,nq)*/, cons
 }
 
 // solve_energy: out[e,i] = sum_j minv[e,i,j] rhs[e,j]
-__global__ void k_energy_solve(const double* minv, const double* rhs, int nt, long long ne, double* out) {
+// (packed: the symmetric lower-triangle storage of minv_packed)
+__global__ void k_energy_solve(const double* minv, const double* rhs, int nt, long long ne, double* out, int packed) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= ne * nt) return;
   const long long e = t / nt;
   const int i = (int)(t % nt);
-  const double* m = minv + (e * nt + i) * nt;
   const double* r = rhs + e * nt;
   double s = 0.0;
-  for (int j = 0; j < nt; ++j) s = fma(m[j], r[j], s);
+  if (packed) {
+    const double* m = minv + e * tri(nt);
+    for (int j = 0; j < nt; ++j) s = fma(m[j <= i ? tri(i) + j : tri(j) + i], r[j], s);
+  } else {
+    const double* m = minv + (e * nt + i) * nt;
+    for (int j = 0; j < nt; ++j) s = fma(m[j], r[j], s);
+  }
   out[t] = s;
 }
 

@@ -6,10 +6,14 @@
 // A CTA of 256 threads runs EPC elements per pass.  Every sum-factorisation stage is
 // its own phase with one thread per 1D line, so no thread carries more than one
 // line of one stage (short dependency chains, modest registers, all lanes busy):
-//   A   gather x, v node rows (6 fields) and e -> G image
+//   A   prefetch one pass ahead: x, v node rows (6 fields) by cp.async -> G image;
+//       e, qd0 and the packed M_e^{-1} (contiguous per pass) by bulk copies (TMA engine,
+//       cp.async.bulk on an mbarrier)
 //   B1  x stage, thread per (field, z, y) row: B_x u, G_x u          -> X image
+//       (+ thermo rows B_x e -> the T image's thermo area)
 //   B2  y stage, thread per (field, z, qx) line: B_y B_x, G_y B_x, B_y G_x -> T image
-//   C1  z stage + point physics, thread per quadrature point: J, grad v, v, e at q,
+//   C1  z stage + point physics, thread per quadrature point: J, grad v, v, e at q
+//       (e's y and z stages inline from the thermo rows),
 //       EOS, tensor viscosity, CFL ratio, D_F; F.1 and F^T v integrands -> W image
 //   C2  transposed z stage, thread per (comp, qx, qy) column           -> Z image
 //   D1  transposed y stage, thread per (comp, z, qx) line              -> Y image
@@ -19,6 +23,7 @@
 // Shared images alias once dead: W over G+X, Z over T, Y over X, staging over G.
 #pragma once
 
+#include "hx_async.cuh"
 #include "hx_brick.cuh"
 
 namespace hx {
@@ -30,29 +35,39 @@ struct RatesPC {
   static constexpr int THREADS = 256;
   static constexpr int EPC = THREADS / NQ > 0 ? THREADS / NQ : 1;
   static constexpr int XPL = 6 * D1;                   // field planes
-  static constexpr int GP = DD + 1, EP = DTT + 1;      // gather pitches (field / thermo plane)
-  static constexpr int GS = XPL * GP + DT * EP;        // G image
-  static constexpr int XP = 2 * Q + 1;                 // row pitch of the x / y-transposed images
-  static constexpr int XFS = XPL * D1 * XP;            // X image, field rows
-  static constexpr int XS = XFS + DTT * Q;             // + thermo rows
+  // G image: the node rows of x and of v as they lie in memory (D1 nodes x 3 comps per
+  // row, 3 D1 contiguous doubles), rows padded to RP so that the x-stage threads (one per
+  // (comp, z, y) row) read distinct bank pairs
+  static constexpr int RP = 3 * D1 + 1, GRP = DD * RP;  // row pitch, field-group pitch
+  static constexpr int GS = 2 * GRP;                    // G image (x rows, v rows)
+  // X / Y images: row (plane, y) pitch XP, plane pitch XPP = Q (mod 16): the y-stage lines
+  // (plane, qx) of consecutive planes fall on consecutive bank pairs
+  static constexpr int XP = 2 * Q + 2;
+  static constexpr int XPP = D1 * XP + ((Q - D1 * XP) % 16 + 16) % 16;
+  static constexpr int XFS = XPL * XPP;                 // X image, field rows
+  static constexpr int XS = XFS;                       // (thermo rows live in the T image)
   // plane pitch of the T and Z images: >= 3 QQ and = Q (mod 16) so that the lines of
   // consecutive planes (Q doubles each) fall on consecutive bank pairs
   static constexpr int PP = 3 * QQ + ((Q - 3 * QQ) % 16 + 16) % 16;
   static constexpr int TFS = XPL * PP;                 // T image, field planes
-  static constexpr int TS = TFS + DT * QQ;             // + thermo planes
+  static constexpr int TS = TFS + DTT * Q;             // + thermo x-stage rows (dz, dy, qx)
   static constexpr int WS = 10 * NQ;                   // W image (aliases G+X)
   static constexpr int ZS = 3 * D1 * PP + DT * QQ;     // Z image (aliases T)
-  static constexpr int YFS = 3 * D1 * D1 * XP;         // Y image (aliases X)
+  static constexpr int MN = minv_packed<3, P>() ? tri(NT) : NT * NT;  // M_e^{-1} doubles per element
+  static constexpr int YFS = 3 * D1 * XPP;             // Y image (aliases X)
   static constexpr int YS = YFS + DTT * Q;
-  static constexpr int OS = 3 * NL + NT;               // staging (aliases T)
-  // prefetch buffer (double-buffered, filled by cp.async one pass ahead):
-  // [G images EPC x GS | qd0 EPC x NQ | M_e^{-1} EPC x NT^2], regions 16-byte aligned
+  // staging: per component DD rows of D1 nodes, row pitch OR (conflict-free x^T stage
+  // stores), then the thermo F^T v block
+  static constexpr int OR = D1 + 1, OPL = DD * OR;
+  static constexpr int OS = 3 * OPL + NT;              // staging (aliases T)
+  // prefetch buffer (double-buffered, filled one pass ahead):
+  // [G images EPC x GS | e EPC x NT | qd0 EPC x NQ | M_e^{-1} EPC x MN], regions 16-byte aligned
   static constexpr int ev(int n) { return (n + 1) & ~1; }
-  static constexpr int FQ = ev(EPC * GS), FM = FQ + ev(EPC * NQ), FS = FM + ev(EPC * NT * NT);
+  static constexpr int FE = ev(EPC * GS), FQ = FE + ev(EPC * NT), FM = FQ + ev(EPC * NQ), FS = FM + ev(EPC * MN);
   static constexpr int XR = (XS > WS ? (XS > YS ? XS : YS) : (WS > YS ? WS : YS));  // X / W / Y region
   static_assert(ZS <= TS && OS <= TS, "image aliasing");
   static constexpr int PER = XR + TS;                  // working images per element
-  static constexpr size_t bytes = sizeof(double) * (2 * (size_t)FS + (size_t)EPC * PER + 2 * NQ);
+  static constexpr size_t bytes = sizeof(double) * (2 * (size_t)FS + (size_t)EPC * PER + 2 * NQ) + 16;
 };
 
 struct RatesPCArgs {
@@ -62,7 +77,7 @@ struct RatesPCArgs {
   const double* qd0;   // (NE, nq)
   const int* emap;     // (NE, nl) (generic meshes)
   const int* slot;     // null: element-major E out; else node-sorted position
-  const double* minv;  // (NE, nt, nt)
+  const double* minv;  // (NE, nt, nt), or packed lower triangles (minv_packed)
   const double* wnd;   // (nq)
   const double* psi1;  // (nq)
   double gamma, q1, q2;
@@ -142,8 +157,9 @@ template <int P, int MODE>
 __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
   using R = RatesPC<P>;
   constexpr int D1 = R::D1, Q = R::Q, DT = R::DT, DD = R::DD, QQ = R::QQ, NL = R::NL, NQ = R::NQ;
-  constexpr int NTH = R::NT, DTT = R::DTT, EPC = R::EPC, GP = R::GP, EP = R::EP;
-  constexpr int XPL = R::XPL, PER = R::PER, XP = R::XP, XFS = R::XFS, TFS = R::TFS, YFS = R::YFS, PP = R::PP;
+  constexpr int NTH = R::NT, DTT = R::DTT, EPC = R::EPC, RP = R::RP, GRP = R::GRP;
+  constexpr int PER = R::PER, XP = R::XP, XPP = R::XPP, TFS = R::TFS, YFS = R::YFS, PP = R::PP;
+  constexpr int OR = R::OR, OPL = R::OPL;
   constexpr int FS = R::FS, XR = R::XR;
   constexpr int NT = R::THREADS;
   constexpr int NF = MODE == 0 ? 6 : 3;  // fields gathered / contracted
@@ -154,16 +170,28 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
   double* work = smem + 2 * FS;  // per element: X/W/Y region, T/Z/O region
   double* sw = work + EPC * PER;       // tensor weights
   double* sp = sw + NQ;                // psi1
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sp + NQ);  // one per prefetch buffer
+  constexpr int MN = R::MN;
+  constexpr bool PK = minv_packed<3, P>();
   const int t = threadIdx.x;
   for (int i = t; i < NQ; i += NT) {
     sw[i] = a.wnd[i];
     sp[i] = a.psi1[i];
   }
+  if constexpr (MODE == 0) {
+    if (t == 0) {
+      mbar_init(bar, 1);
+      mbar_init(bar + 1, 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+  }
+  unsigned ph0 = 0, ph1 = 0;  // mbarrier phase parity per buffer
   double rmin = __longlong_as_double(0x7ff0000000000000ll);
   long long clamps = 0;
   unsigned long long key = ~0ull;
-  // A (prefetch): cp.async x, v node values, e, qd0 and M_e^{-1} of the pass at f0
-  // into prefetch buffer b (G image layout: field planes, padded)
+  // A (prefetch): cp.async x, v node rows, bulk copies of e, qd0 and M_e^{-1} of the pass
+  // at f0 into prefetch buffer b (G image: node rows as in memory, padded to RP)
   auto prefetch = [&](int b, long long f0) {
     if (f0 < a.ne) {
       const int fel = (int)((a.ne - f0) < EPC ? (a.ne - f0) : EPC);
@@ -184,18 +212,23 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
         } else {
           n = __ldg(a.emap + e * NL + row * D1 + dx);
         }
-        double* g = fb + el * R::GS;
-        cp_async8(g + (c * D1 + dz) * GP + dy * D1 + dx, a.x + n * 3 + c);
-        if constexpr (MODE == 0) cp_async8(g + ((3 + c) * D1 + dz) * GP + dy * D1 + dx, a.v + n * 3 + c);
+        double* g = fb + el * R::GS + row * RP + sidx;
+        cp_async8(g, a.x + n * 3 + c);
+        if constexpr (MODE == 0) cp_async8(g + GRP, a.v + n * 3 + c);
       }
       if constexpr (MODE == 0) {
-        for (int it = t; it < fel * NTH; it += NT) {
-          const int el = it / NTH, i = it - el * NTH;
-          const int dz = i / DTT, k = i - dz * DTT;
-          cp_async8(fb + el * R::GS + XPL * GP + dz * EP + k, a.e + (f0 + el) * NTH + i);
+        // e, qd0, M_e^{-1} of the pass are contiguous: bulk copies on buffer b's mbarrier
+        const double* se = a.e + f0 * NTH;
+        const double* sq = a.qd0 + f0 * NQ;
+        const double* sm = a.minv + f0 * MN;
+        if (t == 0) {
+          fence_proxy_async_smem();  // the generic reads of this buffer's last use are done
+          mbar_expect_tx(bar + b, span_bulk_bytes(se, fel * NTH) + span_bulk_bytes(sq, fel * NQ) +
+                                      span_bulk_bytes(sm, fel * MN));
         }
-        cp_span<NT>(fb + R::FQ, a.qd0 + f0 * NQ, fel * NQ, t);
-        cp_span<NT>(fb + R::FM, a.minv + f0 * (NTH * NTH), fel * NTH * NTH, t);
+        span_bulk<NT>(fb + R::FE, se, fel * NTH, t, bar + b);
+        span_bulk<NT>(fb + R::FQ, sq, fel * NQ, t, bar + b);
+        span_bulk<NT>(fb + R::FM, sm, fel * MN, t, bar + b);
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -208,6 +241,10 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
     const int nel = (int)((a.ne - e0) < EPC ? (a.ne - e0) : EPC);
     const double* gcur = smem + buf * FS;
     asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if constexpr (MODE == 0) {
+      mbar_wait(bar + buf, buf ? ph1 : ph0);  // this pass's bulk copies landed
+      if (buf) ph1 ^= 1; else ph0 ^= 1;
+    }
     __syncthreads();  // this pass's prefetch landed; previous pass done with every image
     prefetch(buf ^ 1, e0 + stride);  // overlaps this pass's compute
     // ---- B1: x stage, thread per row
@@ -223,10 +260,12 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
         double* X = work + el * PER;
         if (k < FR) {
           const int pl = k / D1, dy = k - pl * D1;  // pl = f*D1 + dz
+          const int f = pl / D1, dz = pl - f * D1;
+          const int grp = f >= 3, c = f - 3 * grp;
           double u[D1];
 #pragma unroll
-          for (int dx = 0; dx < D1; ++dx) u[dx] = g[pl * GP + dy * D1 + dx];
-          double* o = X + k * XP;
+          for (int dx = 0; dx < D1; ++dx) u[dx] = g[grp * GRP + (dz * D1 + dy) * RP + dx * 3 + c];
+          double* o = X + pl * XPP + dy * XP;
 #pragma unroll
           for (int qx = 0; qx < Q; ++qx) {
             double sb = 0.0, sg = 0.0;
@@ -242,13 +281,14 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
           const int r = k - FR;  // dz_t * DT + dy_t
           double u[DT];
 #pragma unroll
-          for (int dx = 0; dx < DT; ++dx) u[dx] = g[XPL * GP + (r / DT) * EP + (r % DT) * DT + dx];
+          for (int dx = 0; dx < DT; ++dx) u[dx] = gcur[R::FE + el * NTH + r * DT + dx];
+          double* Th = work + el * PER + XR + TFS;  // thermo x-rows (the T image's thermo area)
 #pragma unroll
           for (int qx = 0; qx < Q; ++qx) {
             double s = 0.0;
 #pragma unroll
             for (int dx = 0; dx < DT; ++dx) s = fma(cBt[qx * DT + dx], u[dx], s);
-            X[XFS + r * Q + qx] = s;
+            Th[r * Q + qx] = s;
           }
         }
       }
@@ -257,7 +297,7 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
     // ---- B2: y stage, thread per (plane, qx) line
     {
       constexpr int FL = NF * D1 * Q;
-      constexpr int TASKS = FL + (MODE == 0 ? DT * Q : 0);
+      constexpr int TASKS = FL;  // (e's y stage runs inline in C1)
 #pragma unroll
       for (int rep = 0; rep < (EPC * TASKS + NT - 1) / NT; ++rep) {
         const int it = t + rep * NT;
@@ -265,13 +305,13 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
         const int el = it / TASKS, k = it - el * TASKS;
         const double* X = work + el * PER;
         double* T = work + el * PER + XR;
-        if (k < FL) {
+        {
           const int pl = k / Q, qx = k - pl * Q;
           double vb[D1], vg[D1];
 #pragma unroll
           for (int dy = 0; dy < D1; ++dy) {
-            vb[dy] = X[(pl * D1 + dy) * XP + qx];
-            vg[dy] = X[(pl * D1 + dy) * XP + Q + qx];
+            vb[dy] = X[pl * XPP + dy * XP + qx];
+            vg[dy] = X[pl * XPP + dy * XP + Q + qx];
           }
           double* o = T + pl * PP + qx;
 #pragma unroll
@@ -286,18 +326,6 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
             o[qy * Q] = bb;
             o[QQ + qy * Q] = gb;
             o[2 * QQ + qy * Q] = bg;
-          }
-        } else {
-          const int r = k - FL, dz = r / Q, qx = r - dz * Q;
-          double vb[DT];
-#pragma unroll
-          for (int dy = 0; dy < DT; ++dy) vb[dy] = X[XFS + (dz * DT + dy) * Q + qx];
-#pragma unroll
-          for (int qy = 0; qy < Q; ++qy) {
-            double s = 0.0;
-#pragma unroll
-            for (int dy = 0; dy < DT; ++dy) s = fma(cBt[qy * DT + dy], vb[dy], s);
-            T[TFS + dz * QQ + qy * Q + qx] = s;
           }
         }
       }
@@ -352,9 +380,16 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
           key = kk < key ? kk : key;
         }
       } else {
+        // e at q: y stage (ascending dy from 0.0) then z stage, from the thermo x-rows
+        const int qy = col / Q, qx = col - qy * Q;
         double eq = 0.0;
 #pragma unroll
-        for (int dz = 0; dz < DT; ++dz) eq = fma(cBt[qz * DT + dz], T[TFS + dz * QQ + col], eq);
+        for (int dz = 0; dz < DT; ++dz) {
+          double sy = 0.0;
+#pragma unroll
+          for (int dy = 0; dy < DT; ++dy) sy = fma(cBt[qy * DT + dy], T[TFS + (dz * DT + dy) * Q + qx], sy);
+          eq = fma(cBt[qz * DT + dz], sy, eq);
+        }
         PointOut<3> po;
         point_physics_fast(J, dv, vq, eq, gcur[R::FQ + el * NQ + q], a.gam ? __ldg(a.gam + e) : a.gamma, a.q1,
                            a.q2, po);
@@ -374,9 +409,9 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
 #pragma unroll
           for (int l = 0; l < 3; ++l) {
             s += DF[c][l] * dv[c][l];
-            W[(c * 3 + l) * NQ + q] = DF[c][l] * p1;
+            W[(c * 3 + l) * NQ + kq] = DF[c][l] * p1;  // (col, qz) order: conflict-free stores
           }
-        W[9 * NQ + q] = s;
+        W[9 * NQ + kq] = s;
       }
     }
     if constexpr (MODE == 1) continue;
@@ -402,9 +437,9 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
           }
 #pragma unroll
           for (int qz = 0; qz < Q; ++qz) {
-            const double s0 = W[(c * 3 + 0) * NQ + qz * QQ + col];
-            const double s1 = W[(c * 3 + 1) * NQ + qz * QQ + col];
-            const double s2 = W[(c * 3 + 2) * NQ + qz * QQ + col];
+            const double s0 = W[(c * 3 + 0) * NQ + col * Q + qz];
+            const double s1 = W[(c * 3 + 1) * NQ + col * Q + qz];
+            const double s2 = W[(c * 3 + 2) * NQ + col * Q + qz];
 #pragma unroll
             for (int dz = 0; dz < D1; ++dz) {
               z0[dz] = fma(cB[qz * D1 + dz], s0, z0[dz]);
@@ -424,7 +459,7 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
           for (int dz = 0; dz < DT; ++dz) zt[dz] = 0.0;
 #pragma unroll
           for (int qz = 0; qz < Q; ++qz) {
-            const double s = W[9 * NQ + qz * QQ + col];
+            const double s = W[9 * NQ + col * Q + qz];
 #pragma unroll
             for (int dz = 0; dz < DT; ++dz) zt[dz] = fma(cBt[qz * DT + dz], s, zt[dz]);
           }
@@ -468,8 +503,8 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
           }
 #pragma unroll
           for (int dy = 0; dy < D1; ++dy) {
-            Y[(pl * D1 + dy) * XP + qx] = yg[dy];
-            Y[(pl * D1 + dy) * XP + Q + qx] = yb[dy];
+            Y[pl * XPP + dy * XP + qx] = yg[dy];
+            Y[pl * XPP + dy * XP + Q + qx] = yb[dy];
           }
         } else {
           const int r = k - FL, dz = r / Q, qx = r - dz * Q;
@@ -502,11 +537,12 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
         double* O = work + el * PER + XR;  // aliases Z (dead): [c][l] F.1, then fv
         if (k < FR) {
           const int c = k / DD, r = k - c * DD;  // r = dz*D1 + dy
+          const int dz = r / D1, dy = r - dz * D1;
           double yg[Q], yb[Q];
 #pragma unroll
           for (int qx = 0; qx < Q; ++qx) {
-            yg[qx] = Y[k * XP + qx];
-            yb[qx] = Y[k * XP + Q + qx];
+            yg[qx] = Y[(c * D1 + dz) * XPP + dy * XP + qx];
+            yb[qx] = Y[(c * D1 + dz) * XPP + dy * XP + Q + qx];
           }
 #pragma unroll
           for (int dx = 0; dx < D1; ++dx) {
@@ -516,7 +552,7 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
               s = fma(cG[qx * D1 + dx], yg[qx], s);
               s = fma(cB[qx * D1 + dx], yb[qx], s);
             }
-            O[c * NL + r * D1 + dx] = s;
+            O[c * OPL + r * OR + dx] = s;
           }
         } else {
           const int r = k - FR;  // dz_t*DT + dy_t
@@ -528,7 +564,7 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
             double s = 0.0;
 #pragma unroll
             for (int qx = 0; qx < Q; ++qx) s = fma(cBt[qx * DT + dx], y[qx], s);
-            O[3 * NL + r * DT + dx] = s;
+            O[3 * OPL + r * DT + dx] = s;
           }
         }
       }
@@ -538,7 +574,7 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
     for (int it = t; it < nel * NL * 3; it += NT) {
       const int el = it / (NL * 3), rem = it - el * (NL * 3);
       const int l = rem / 3, c = rem - l * 3;
-      const double val = work[el * PER + XR + c * NL + l];
+      const double val = work[el * PER + XR + c * OPL + (l / D1) * OR + (l % D1)];
       const long long e = e0 + el;
       const long long pos = a.slot ? (long long)__ldg(a.slot + e * NL + l) * 3 + c : e * (NL * 3) + rem;
       a.evec[pos] = val;
@@ -546,11 +582,18 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
     for (int it = t; it < nel * NTH; it += NT) {
       const int el = it / NTH, i = it - el * NTH;
       const long long e = e0 + el;
-      const double* fv = work + el * PER + XR + 3 * NL;
-      const double* mi = gcur + R::FM + (el * NTH + i) * NTH;
+      const double* fv = work + el * PER + XR + 3 * OPL;
       double s = 0.0;
+      if constexpr (PK) {  // row i of the symmetric inverse: L[i][0..i], then L[j][i] for j > i
+        const double* mi = gcur + R::FM + el * MN;
+        const int ri = tri(i);
 #pragma unroll
-      for (int j = 0; j < NTH; ++j) s = fma(mi[j], fv[j], s);
+        for (int j = 0; j < NTH; ++j) s = fma(mi[j <= i ? ri + j : tri(j) + i], fv[j], s);
+      } else {
+        const double* mi = gcur + R::FM + (el * NTH + i) * NTH;
+#pragma unroll
+        for (int j = 0; j < NTH; ++j) s = fma(mi[j], fv[j], s);
+      }
       a.de[e * NTH + i] = s;
     }
   }
