@@ -201,6 +201,11 @@ int hx_phase_begin(hx_ctx* ctx, const double* x, const double* qdata0, const uin
 int hx_stress(hx_ctx* ctx, const hx_params* prm, const double* x, const double* v,
               const double* e, const double* qdata0, double* sigma, double* min_ratio,
               int64_t* clamped, hx_inverted* inv);
+/* timestep_estimate's ratio (hydro.py:364-367 -> compute_geometric_factors fespace.py:305-346
+ * + stress_qdata hydro.py:254-315): min h/(c_s+|v|), clamp count and the first inverted
+ * point, fused (no geometry or sigma written); after hx_phase_begin; 3D, p >= 2. */
+int hx_timestep_ratio(hx_ctx* ctx, const hx_params* prm, const double* x, const double* v,
+                      const double* e, double* min_ratio, int64_t* clamped, hx_inverted* inv);
 /* solve_energy (hydro.py:339-344): out = M_e^{-1} rhs per element (after hx_phase_begin). */
 int hx_energy_solve(hx_ctx* ctx, const double* rhs, double* out);
 /* rates (hydro.py:346-360): fused quadrature-point setup + F.1 + F^T v + M_e^{-1},

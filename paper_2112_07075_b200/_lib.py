@@ -87,6 +87,8 @@ _SIGS = {
     "hx_phase_begin": (C.c_int, [P, P, P, P, P, P, P]),
     "hx_stress": (C.c_int, [P, C.POINTER(Params), P, P, P, P, P, C.POINTER(C.c_double),
                             C.POINTER(C.c_int64), C.POINTER(Inverted)]),
+    "hx_timestep_ratio": (C.c_int, [P, C.POINTER(Params), P, P, P, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                    C.POINTER(Inverted)]),
     "hx_energy_solve": (C.c_int, [P, P, P]),
     "hx_rates": (C.c_int, [P, C.POINTER(Params), P, P, P, P, P, C.POINTER(StepInfo)]),
     "hx_step": (C.c_int, [P, C.POINTER(Params), C.c_double, P, P, P, P, P, P, C.POINTER(StepInfo)]),

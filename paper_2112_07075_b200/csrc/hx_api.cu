@@ -312,7 +312,7 @@ static int launch_rates_pc(hx_ctx* ctx, const RatesPCArgs& a) {
   }
   static unsigned grid = 0;
   if (!grid) grid = persistent_grid(k, R::THREADS, R::bytes, 1ll << 40);
-  prof_begin(ctx, MODE == 0 ? K_RATES : K_VALID);
+  prof_begin(ctx, MODE == 0 ? K_RATES : (MODE == 2 ? K_OTHER : K_VALID));
   k<<<std::min(grid, gblocks(ctx->ne, R::EPC)), R::THREADS, R::bytes, ctx->stream>>>(a);
   prof_end(ctx);
   CKL();
@@ -353,6 +353,7 @@ struct LaunchRates {
         // p = 3: 35 vs 40); at p = 4 its images cap it at 2 CTAs/SM and the rates kernel's
         // geometry-only mode wins (54 vs 89 us)
         if (mode == 0) return launch_rates_pc<P, 0>(ctx, a);
+        if (mode == 2) return launch_rates_pc<P, 2>(ctx, a);
         return P <= 3 ? launch_valid<P>(ctx, a) : launch_rates_pc<P, 1>(ctx, a);
       }
     }
@@ -776,8 +777,8 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   ctx->preg = 2 * std::max<long long>(gblocks(3 * nn, 256), gblocks(ne, 1)) + 64;
   ok &= dalloc(&ctx->partials, 2 * (size_t)ctx->preg) == cudaSuccess;
   ok &= dalloc(&ctx->cg, 2) == cudaSuccess;
-  ok &= dalloc(&ctx->t_dev, 1) == cudaSuccess;
-  ok &= cudaMallocHost((void**)&ctx->h_t, sizeof(double)) == cudaSuccess;
+  ok &= dalloc(&ctx->t_dev, 2) == cudaSuccess;  // {t, caller-given dt} for the step graphs
+  ok &= cudaMallocHost((void**)&ctx->h_t, 2 * sizeof(double)) == cudaSuccess;
   ok &= cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking) == cudaSuccess;
   ok &= cudaStreamCreateWithFlags(&ctx->gstream2, cudaStreamNonBlocking) == cudaSuccess;
   ok &= dalloc(&ctx->st, 4) == cudaSuccess;
@@ -1818,6 +1819,31 @@ extern "C" int hx_stress(hx_ctx* ctx, const hx_params* prm, const double* x, con
   return h.inv_key != ~0ull ? HX_EINVERTED : HX_OK;
 }
 
+// timestep_estimate's CFL ratio (hydro.py:364-367): compute_geometric_factors' inversion
+// check + stress_qdata's min h/(c_s+|v|) and clamp count, without materialising the
+// geometry or sigma -- one fused point-physics launch (k_rates_pc MODE 2) on the phase's
+// qdata0.  3D, p >= 2 (the fused kernels' range); other discretisations keep the
+// reference's geometry + stress calls (hx_geometry, hx_stress).
+extern "C" int hx_timestep_ratio(hx_ctx* ctx, const hx_params* prm, const double* x, const double* v,
+                                 const double* e, double* min_ratio, int64_t* clamped, hx_inverted* inv) {
+  if (!ctx || !prm || !x || !v || !e || !ctx->phase) return HX_EINVAL;
+  if (ctx->dim != 3 || ctx->p < 2) return fail(ctx, HX_EINVAL, "hx_timestep_ratio: 3D, p >= 2 only");
+  CK(cudaSetDevice(ctx->device));
+  StatusDev* st = ctx->st + 3;
+  int rc = status_reset(ctx, st);
+  if (rc) return rc;
+  rc = dispatch<LaunchRates>(ctx, x, v, e, (double*)nullptr, (double*)nullptr, st, 2, prm->gamma, prm->q1, prm->q2);
+  if (!rc && ctx->peer) rc = peer_status(ctx, st, 1);
+  if (rc) return rc;
+  rc = read_status(ctx, st, ctx->h_st + 3);
+  if (rc) return rc;
+  const StatusDev& h = ctx->h_st[3];
+  if (min_ratio) *min_ratio = h.min_ratio;
+  if (clamped) *clamped = (int64_t)h.clamps;
+  decode_inv(ctx, h.inv_key, inv);
+  return h.inv_key != ~0ull ? HX_EINVERTED : HX_OK;
+}
+
 extern "C" int hx_energy_solve(hx_ctx* ctx, const double* rhs, double* out) {
   if (!ctx || !rhs || !out || !ctx->phase) return HX_EINVAL;
   CK(cudaSetDevice(ctx->device));
@@ -2120,7 +2146,9 @@ static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_
   hx_ctx::StepGraph* sg = nullptr;
   const int dup = ctx->dup_class;
   for (auto& g : ctx->graphs)
-    if (!memcmp(g.key, key, sizeof key) && g.dt_fixed == dt_fixed && same_params(g.prm, *prm) && g.dup == dup)
+    // a caller-given dt (rk2_step) is a graph input like t, not part of the graph
+    if (!memcmp(g.key, key, sizeof key) && (g.dt_fixed >= 0.0) == (dt_fixed >= 0.0) && same_params(g.prm, *prm) &&
+        g.dup == dup)
       sg = &g;
   if (!sg) {
     if (ctx->graphs.size() >= 16) {
@@ -2148,8 +2176,9 @@ static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_
     int rc = capture_step(ctx, prm, dt_fixed, x, v, e, x_out, v_out, e_out, &sg->exec, sg->gprof.get());
     if (rc) return rc;
   }
-  *ctx->h_t = t;
-  CK(cudaMemcpyAsync(ctx->t_dev, ctx->h_t, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h_t[0] = t;
+  ctx->h_t[1] = dt_fixed;
+  CK(cudaMemcpyAsync(ctx->t_dev, ctx->h_t, 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaGraphLaunch(sg->exec, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   {

@@ -1552,12 +1552,12 @@ struct DtArgs {
   double cfl, dt_max, t_final, t;
   double dt_fixed;   // >= 0: rk2_step(state, dt) with a caller-given dt
   int retry;
-  const double* tptr;  // state time on the device (graph mode) or null (use t)
+  const double* tptr;  // graph mode: {state time, caller-given dt} on the device, or null (use t, dt_fixed)
 };
 __global__ void k_dt(DtArgs a) {
   double dt;
   if (a.dt_fixed >= 0.0) {
-    dt = a.dt_fixed;
+    dt = a.tptr ? a.tptr[1] : a.dt_fixed;
   } else {
     const double t = a.tptr ? *a.tptr : a.t;
     dt = a.cfl * a.st->min_ratio;

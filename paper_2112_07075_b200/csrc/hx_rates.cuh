@@ -20,6 +20,8 @@
 //   D2  transposed x stage, thread per (comp, z, y) row                -> staging
 //   E   F.1 E-vector out (element-major or node-sorted) and de = M_e^{-1} F^T v
 // MODE 1 (validity of the new geometry, hydro.py:400-401) runs A-C1 on x only.
+// MODE 2 (timestep_estimate's CFL ratio, hydro.py:364-367) runs A-C1 with the point
+// physics (ratio, clamp count, first inverted point) and writes nothing else.
 // Shared images alias once dead: W over G+X, Z over T, Y over X, staging over G.
 #pragma once
 
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
   constexpr int OR = R::OR, OPL = R::OPL;
   constexpr int FS = R::FS, XR = R::XR;
   constexpr int NT = R::THREADS;
-  constexpr int NF = MODE == 0 ? 6 : 3;  // fields gathered / contracted
+  constexpr int NF = MODE == 1 ? 3 : 6;  // fields gathered / contracted
   const double* cB = c_B[P - 1];
   const double* cG = c_G[P - 1];
   const double* cBt = c_Bt[P - 1];
@@ -178,7 +180,7 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
     sw[i] = a.wnd[i];
     sp[i] = a.psi1[i];
   }
-  if constexpr (MODE == 0) {
+  if constexpr (MODE != 1) {
     if (t == 0) {
       mbar_init(bar, 1);
       mbar_init(bar + 1, 1);
@@ -214,9 +216,9 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
         }
         double* g = fb + el * R::GS + row * RP + sidx;
         cp_async8(g, a.x + n * 3 + c);
-        if constexpr (MODE == 0) cp_async8(g + GRP, a.v + n * 3 + c);
+        if constexpr (MODE != 1) cp_async8(g + GRP, a.v + n * 3 + c);
       }
-      if constexpr (MODE == 0) {
+      if constexpr (MODE != 1) {
         // e, qd0, M_e^{-1} of the pass are contiguous: bulk copies on buffer b's mbarrier
         const double* se = a.e + f0 * NTH;
         const double* sq = a.qd0 + f0 * NQ;
@@ -224,11 +226,11 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
         if (t == 0) {
           fence_proxy_async_smem();  // the generic reads of this buffer's last use are done
           mbar_expect_tx(bar + b, span_bulk_bytes(se, fel * NTH) + span_bulk_bytes(sq, fel * NQ) +
-                                      span_bulk_bytes(sm, fel * MN));
+                                      (MODE == 0 ? span_bulk_bytes(sm, fel * MN) : 0u));
         }
         span_bulk<NT>(fb + R::FE, se, fel * NTH, t, bar + b);
         span_bulk<NT>(fb + R::FQ, sq, fel * NQ, t, bar + b);
-        span_bulk<NT>(fb + R::FM, sm, fel * MN, t, bar + b);
+        if constexpr (MODE == 0) span_bulk<NT>(fb + R::FM, sm, fel * MN, t, bar + b);
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -241,7 +243,7 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
     const int nel = (int)((a.ne - e0) < EPC ? (a.ne - e0) : EPC);
     const double* gcur = smem + buf * FS;
     asm volatile("cp.async.wait_group 0;" ::: "memory");
-    if constexpr (MODE == 0) {
+    if constexpr (MODE != 1) {
       mbar_wait(bar + buf, buf ? ph1 : ph0);  // this pass's bulk copies landed
       if (buf) ph1 ^= 1; else ph0 ^= 1;
     }
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
     // ---- B1: x stage, thread per row
     {
       constexpr int FR = NF * D1 * D1;                 // field rows
-      constexpr int TASKS = FR + (MODE == 0 ? DTT : 0);
+      constexpr int TASKS = FR + (MODE != 1 ? DTT : 0);
 #pragma unroll
       for (int rep = 0; rep < (EPC * TASKS + NT - 1) / NT; ++rep) {
         const int it = t + rep * NT;
@@ -399,6 +401,7 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
         }
         clamps += po.clamped;
         rmin = fmin(rmin, po.ratio);
+        if constexpr (MODE == 0) {
         double DF[3][3];
         force_point<3>(po.sigma, po.jinv, sw[q] * po.det, DF);
         const double p1 = sp[q];
@@ -412,9 +415,10 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
             W[(c * 3 + l) * NQ + kq] = DF[c][l] * p1;  // (col, qz) order: conflict-free stores
           }
         W[9 * NQ + kq] = s;
+        }
       }
     }
-    if constexpr (MODE == 1) continue;
+    if constexpr (MODE != 0) continue;
     __syncthreads();
     // ---- C2: transposed z stage, thread per (comp, column) (+ F^T v per column)
     {

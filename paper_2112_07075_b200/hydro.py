@@ -364,8 +364,26 @@ class LagrangeHydro:
     # -- stepping (hydro.py:364-405) ---------------------------------------------------
 
     def timestep_estimate(self, state: HydroState, controls: StepControls) -> float:
-        geom = compute_geometric_factors(self.mesh, self.quad, x=state.x)
-        _, min_ratio = self.stress_qdata(state, geom)
+        """dt = min(cfl * min h/(c_s+|v|), dt_max, t_final - t) (hydro.py:364-373).
+
+        3D p >= 2: one fused device launch (hx_timestep_ratio) with the semantics of the
+        reference's compute_geometric_factors + stress_qdata pair (same first inverted
+        point, same clamp count, same ratio); otherwise those two calls."""
+        if self.mesh.dim == 3 and self.mesh.order >= 2 and self._phase_ready:
+            X, V, E = to_dev(state.x), to_dev(state.v), to_dev(state.e)
+            ratio = C.c_double()
+            clamps = C.c_int64()
+            inv = _lib.Inverted()
+            rc = self._call(self._ctx.lib.hx_timestep_ratio, C.byref(self._params()), _lib.ptr(X), _lib.ptr(V),
+                            _lib.ptr(E), C.byref(ratio), C.byref(clamps), C.byref(inv))
+            if rc == _lib.HX_EINVERTED:
+                raise InvertedElementError(int(inv.element), int(inv.point), float("nan"))
+            self._ctx.check(rc, "timestep_estimate")
+            self.clamp_warnings += int(clamps.value)
+            min_ratio = float(ratio.value)
+        else:
+            geom = compute_geometric_factors(self.mesh, self.quad, x=state.x)
+            _, min_ratio = self.stress_qdata(state, geom)
         dt = controls.cfl * min_ratio
         dt = min(dt, controls.dt_max, controls.t_final - state.t)
         if dt < controls.dt_min:
