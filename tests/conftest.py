@@ -41,3 +41,23 @@ def entry_err(a, b, floor=1e-6):
     if s == 0.0:
         return float(np.max(np.abs(a)))
     return float(np.max(np.abs(a - b) / (np.abs(b) + floor * s)))
+
+
+_ENTRY_LOG = os.environ.get("HX_ENTRY_LOG")
+
+
+def close(a, b, tol, floor=1e-8, entry_tol=None, tag=""):
+    """Parity check: the norm-wise relative error < tol AND every entry within
+    entry_tol (default 100 tol) of the reference, relative to |b_i| + floor * max|b|
+    (so small-magnitude entries such as far-field velocities cannot hide behind the
+    norm).  HX_ENTRY_LOG=path appends the measured pair to a JSON-lines file."""
+    r = rel(a, b)
+    ee = entry_err(a, b, floor=floor)
+    if _ENTRY_LOG:
+        import json
+
+        with open(_ENTRY_LOG, "a") as f:
+            f.write(json.dumps({"tag": tag, "tol": tol, "rel": r, "entry": ee, "floor": floor}) + "\n")
+    et = 100.0 * tol if entry_tol is None else entry_tol
+    assert r < tol, f"{tag}: norm-wise relative error {r:.3e} >= {tol:.1e}"
+    assert ee < et, f"{tag}: per-entry error {ee:.3e} >= {et:.1e} (floor {floor:.0e} max|b|)"

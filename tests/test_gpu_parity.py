@@ -6,12 +6,21 @@ single operator applies 1e-13 relative (fp64, different summation order than
 numpy/OpenBLAS); CG solutions 1e-10 with the same iteration count; N-step
 states and energies 1e-10 relative (BASELINE.json north star), on configs whose
 reference noise floor (1e-15 input perturbation) is below 1.2e-11.
+
+Every norm-wise check is paired with a per-entry one (conftest.close): each entry within
+100 tol of the reference relative to |b_i| + 1e-8 max|b| for single operator applies
+(1e-6 max|b| for the D tables), and within 100 tol relative to |b_i| + 1e-2 max|b| for the
+N-step states (every entry within 1e-10 max|b| absolute, entries above 1% of the maximum
+within 1e-8 relative).  There the far-field velocities are many decades below the maximum;
+measured on B200 (HX_ENTRY_LOG): up to 8e-12 max|v| absolute in the 3D Sedov runs, the
+level of their reference noise floor (1.1e-11), which a norm-wise check alone would not
+show.
 """
 
 import numpy as np
 import pytest
 
-from conftest import golden, rel
+from conftest import close, golden, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -47,12 +56,10 @@ def test_geometry(d, p):
 
     g = golden(f"ops_{d}d_p{p}")
     geom = compute_geometric_factors(_mesh_from(g, d, p), gauss_legendre(p + 2))
-    assert rel(geom.jac, g["jac"]) < 1e-14
-    assert rel(geom.detj, g["detj"]) < 1e-14
-    assert rel(geom.jinv, g["jinv"]) < 1e-14
-    assert rel(geom.wdetj, g["wdetj"]) < 1e-14
-
-
+    close(geom.jac, g["jac"], 1e-14, tag="geom.jac")
+    close(geom.detj, g["detj"], 1e-14, tag="geom.detj")
+    close(geom.jinv, g["jinv"], 1e-14, tag="geom.jinv")
+    close(geom.wdetj, g["wdetj"], 1e-14, tag="geom.wdetj")
 @pytest.mark.parametrize("brick", [True, False], ids=["brick", "csr"])
 @pytest.mark.parametrize("d,p", CASES)
 def test_mass_pa(d, p, brick, monkeypatch):
@@ -68,15 +75,13 @@ def test_mass_pa(d, p, brick, monkeypatch):
     mesh = _mesh_from(g, d, p)
     geom = compute_geometric_factors(mesh, gauss_legendre(p + 2))
     m = MassPA(FiniteElementSpace(mesh, "H1"), geom, coeff=g["mass_coeff"])
-    assert rel(m.D, g["mass_D"]) < 1e-15
-    assert rel(m.apply(g["mass_u1"]), g["mass_y1"]) < 1e-13
-    assert rel(m.apply(g["mass_u3"]), g["mass_y3"]) < 1e-13
-    assert rel(m.diagonal(), g["mass_diag"]) < 1e-13
+    close(m.D, g["mass_D"], 1e-15, tag="m.D")
+    close(m.apply(g["mass_u1"]), g["mass_y1"], 1e-13, tag="m.apply(g['mass_u1'])")
+    close(m.apply(g["mass_u3"]), g["mass_y3"], 1e-13, tag="m.apply(g['mass_u3'])")
+    close(m.diagonal(), g["mass_diag"], 1e-13, tag="m.diagonal()")
     x, it = cg_solve(m.apply, g["cg_b"], precond_diag=m.diagonal(), rel_tol=1e-8, max_iter=500)
     assert it == int(g["cg_iters"])
-    assert rel(x, g["cg_x"]) < 1e-10
-
-
+    close(x, g["cg_x"], 1e-10, tag="x")
 @pytest.mark.parametrize("d,p", CASES)
 def test_force_pa(d, p):
     from paper_2112_07075_b200.fespace import FiniteElementSpace, compute_geometric_factors
@@ -89,10 +94,10 @@ def test_force_pa(d, p):
     kin = FiniteElementSpace(mesh, "H1", vdim=d)
     thermo = FiniteElementSpace(mesh, "L2", order=max(p - 1, 0))
     f = ForcePA(kin, thermo, geom, g["force_sigma"])
-    assert rel(f.D, g["force_D"]) < 1e-14
-    assert rel(f.apply(g["force_e"]), g["force_Fe"]) < 1e-13
-    assert rel(f.apply(np.ones(thermo.ndof)), g["force_F1"]) < 1e-13
-    assert rel(f.apply_transpose(g["force_v"]), g["force_Ftv"]) < 1e-13
+    close(f.D, g["force_D"], 1e-14, floor=1e-6, tag="f.D")
+    close(f.apply(g["force_e"]), g["force_Fe"], 1e-13, tag="f.apply(g['force_e'])")
+    close(f.apply(np.ones(thermo.ndof)), g["force_F1"], 1e-13, tag="f.apply(np.ones(thermo.ndof))")
+    close(f.apply_transpose(g["force_v"]), g["force_Ftv"], 1e-13, tag="f.apply_transpose(g['force_v'])")
     # adjointness (test_operators.py:195-203)
     e, v = g["force_e"], g["force_v"]
     assert np.vdot(f.apply(e), v) == pytest.approx(np.vdot(e, f.apply_transpose(v)), rel=1e-12)
@@ -116,30 +121,28 @@ def test_hydro_point_data_and_rates(d, p):
     hy = _hydro_from(g, d, p)
     st = HydroState(g["st_x"], g["st_v"], g["st_e"], g["st_qdata0"], 0.0)
     hy.begin_phase(st)
-    assert rel(hy.mass_pa.D, g["mass_D_phase"]) < 1e-15
-    assert rel(hy._mass_diag, g["mdiag"]) < 1e-13
-    assert rel(hy._m_e_inv, g["minv"]) < 1e-11
+    close(hy.mass_pa.D, g["mass_D_phase"], 1e-15, tag="hy.mass_pa.D")
+    close(hy._mass_diag, g["mdiag"], 1e-13, tag="hy._mass_diag")
+    close(hy._m_e_inv, g["minv"], 1e-11, tag="hy._m_e_inv")
     geom = compute_geometric_factors(hy.mesh, hy.quad, x=st.x)
     sig, ratio = hy.stress_qdata(st, geom)
-    assert rel(sig, g["stress_sigma"]) < 1e-13
+    close(sig, g["stress_sigma"], 1e-13, tag="sig")
     assert ratio == pytest.approx(float(g["stress_ratio"]), rel=1e-13)
     assert hy.clamp_warnings == int(g["stress_clamps"])
     r = hy.rates(st)
-    assert rel(r.dv, g["rates_dv"]) < 1e-10
-    assert rel(r.de, g["rates_de"]) < 1e-11
+    close(r.dv, g["rates_dv"], 1e-10, tag="r.dv")
+    close(r.de, g["rates_de"], 1e-11, tag="r.de")
     assert r.min_h_over_speed == pytest.approx(float(g["rates_ratio"]), rel=1e-13)
     assert r.clamped == int(g["rates_clamped"])
-    assert rel(hy.solve_energy(g["esolve_rhs"]), g["esolve_out"]) < 1e-11
+    close(hy.solve_energy(g["esolve_rhs"]), g["esolve_out"], 1e-11, tag="hy.solve_energy(g['esolve_rhs'])")
     assert hy.kinetic_energy(st) == pytest.approx(float(g["ke"]), rel=1e-12)
     assert hy.internal_energy(st) == pytest.approx(float(g["ie"]), rel=1e-13)
     assert hy.total_mass(st) == pytest.approx(float(g["mass_total"]), rel=1e-15)
     new, info = hy.rk2_step(st, 1e-3)
     assert info["dt"] == 1e-3
-    assert rel(new.x, g["step_x"]) < 1e-12
-    assert rel(new.v, g["step_v"]) < 1e-10
-    assert rel(new.e, g["step_e"]) < 1e-11
-
-
+    close(new.x, g["step_x"], 1e-12, tag="new.x")
+    close(new.v, g["step_v"], 1e-10, tag="new.v")
+    close(new.e, g["step_e"], 1e-11, tag="new.e")
 RUNS = ["sedov2d_q2", "sedov3d_q3", "sedov3d_q2", "triple3d_q3", "tgv3d_q4"]
 
 
@@ -191,10 +194,10 @@ def test_nstep_run_matches_reference(name, fused, brick, monkeypatch):
         energies.append(hy.total_energy(st))
     st = hy.to_host(st)
     tol = 1e-10
-    assert rel(st.x, z["x"]) < tol
-    assert rel(st.v, z["v"]) < tol
-    assert rel(st.e, z["e"]) < tol
-    assert rel(dts, z["dts"]) < tol
+    close(st.x, z["x"], tol, floor=1e-2, entry_tol=100 * tol, tag="st.x")
+    close(st.v, z["v"], tol, floor=1e-2, entry_tol=100 * tol, tag="st.v")
+    close(st.e, z["e"], tol, floor=1e-2, entry_tol=100 * tol, tag="st.e")
+    close(dts, z["dts"], tol, floor=1e-2, entry_tol=100 * tol, tag="dts")
     assert abs(energies[-1] - float(z["energies"][-1])) <= tol * abs(float(z["energies"][-1]))
     assert st.t == pytest.approx(float(z["t"]), rel=1e-12)
     assert hy.clamp_warnings == int(z["clamps"])
@@ -212,15 +215,15 @@ def test_remap_operators(d, p):
     geom = compute_geometric_factors(mesh, gauss_legendre(p + 2))
     h1 = FiniteElementSpace(mesh, "H1")
     dif = DiffusionPA(h1, geom, nu=g["nu"])
-    assert rel(dif.D, g["diff_D"]) < 1e-14
+    close(dif.D, g["diff_D"], 1e-14, floor=1e-6, tag="dif.D")
     assert dif.stored_values == g["diff_D"].size
-    assert rel(dif.apply(g["diff_x"]), g["diff_y"]) < 1e-13
+    close(dif.apply(g["diff_x"]), g["diff_y"], 1e-13, tag="dif.apply(g['diff_x'])")
     dif1 = DiffusionPA(h1, geom)
-    assert rel(dif1.D, g["diff1_D"]) < 1e-14
-    assert rel(dif1.apply(g["diff_x"]), g["diff1_y"]) < 1e-13
+    close(dif1.D, g["diff1_D"], 1e-14, floor=1e-6, tag="dif1.D")
+    close(dif1.apply(g["diff_x"]), g["diff1_y"], 1e-13, tag="dif1.apply(g['diff_x'])")
     con = ConvectionPA(h1, geom, g["conv_u"])
-    assert rel(con.D, g["conv_D"]) < 1e-14
-    assert rel(con.apply(g["diff_x"]), g["conv_y"]) < 1e-13
+    close(con.D, g["conv_D"], 1e-14, floor=1e-6, tag="con.D")
+    close(con.apply(g["diff_x"]), g["conv_y"], 1e-13, tag="con.apply(g['diff_x'])")
     with pytest.raises(ValueError):
         dif.apply(np.zeros(h1.ndof + 1))
 
@@ -248,7 +251,7 @@ def test_multimaterial_triple_point_matches_oracle(fused):
     ctl = StepControls(cfl=0.02, dt_max=1.0, t_final=10.0)
     oh = O.Hydro(d, p, mesh.node_dofmap, mesh.coords, ge, 0.5, 2.0, bc_mask=O.box_mask(mesh.coords))
     ost = oh.initial_state(r0, v0, e0)
-    assert rel(st.e, ost["e"]) < 1e-15
+    close(st.e, ost["e"], 1e-15, tag="st.e")
     if fused:
         st = hy.to_device(st)
     for _ in range(6):
@@ -262,7 +265,7 @@ def test_multimaterial_triple_point_matches_oracle(fused):
         assert abs(info["dt"] - odt) <= 1e-12 * odt
     st = hy.to_host(st)
     for k in ("x", "v", "e"):
-        assert rel(getattr(st, k), ost[k]) < 1e-10
+        close(getattr(st, k), ost[k], 1e-10, floor=1e-3, entry_tol=1e-9, tag=k)
     # the single-gamma run differs: the per-element gamma is really used
     hy1 = LagrangeHydro(mesh, gauss_legendre(p + 2), MaterialModel(1.5), ViscosityModel(0.5, 2.0),
                         bc_mask=box_velocity_bc(mesh))
