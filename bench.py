@@ -447,6 +447,7 @@ def run_distributed(args, world, rank, local):
     stream = torch.cuda.current_stream()
     dist.barrier()
     torch.cuda.synchronize()
+    launches0 = hy._ctx.launches() if not args.host_cg else 0
     tot = 0.0
     timed_idx = []
     with ClockSampler(local) as clk:
@@ -463,21 +464,59 @@ def run_distributed(args, world, rank, local):
     tt = torch.tensor([tot], dtype=torch.float64, device="cpu" if dist.get_backend() == "gloo" else "cuda")
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     tot = float(tt.item())
-    if args.ktime == "dup":
-        kpass = {"method": "dup",
-                 "note": "per-launch kernel cost in the step graph by duplication: the same timed steps replayed "
-                         "from the post-warm-up snapshot with every launch of one class doubled (CG node pass: "
-                         "dry twin writing to scratch); avg_us = (T_dup - T_plain) / working duplicates, CUDA "
-                         "events around whole steps",
-                 "ms_per_step_plain_replay": prof_ms / args.steps}
-    else:
-        kpass = {"method": "events",
-                 "note": "the same timed steps replayed from the post-warm-up snapshot as plain stream launches; "
-                         "the library records a CUDA event pair on the launching stream around every launch; "
-                         "share = class time / replay step time",
-                 "ms_per_step_replay": prof_ms / args.steps}
-        if ktimes_dup:
-            kpass["graph_dup_avg_us"] = {k: 1e3 * t / c for k, (t, c) in ktimes_dup.items()}
+    launches = None
+    if not args.host_cg:
+        ll = torch.tensor([float(hy._ctx.launches() - launches0)], dtype=torch.float64,
+                          device="cpu" if dist.get_backend() == "gloo" else "cuda")
+        dist.all_reduce(ll)
+        launches = int(ll.item())
+
+    # ---- e2e: every rank steps its brick through the C-ABI host entry (hx_step_host:
+    # pinned host x, v, e -> H2D, the step graph with its peer exchanges, D2H), the same
+    # window; time = max over ranks of the host wall clock around the call
+    e2e = None
+    if not args.no_e2e and not args.host_cg:
+        from paper_2112_07075_b200 import _lib
+
+        nx, nvv, ne_ = x.numel(), v.numel(), e.numel()
+        arena = torch.empty(nx + nvv + ne_, dtype=torch.float64).pin_memory()
+        hx_, hv_, he_ = arena[:nx], arena[nx:nx + nvv], arena[nx + nvv:]
+        init = torch.cat([a.reshape(-1).cpu() for a in (x, v, e)])
+        prm = hy._params(ctl)
+        t_state = [0.0]
+        info_c = _lib.StepInfo()
+        hwin = Window()
+        lib, h = hy._ctx.lib, hy._ctx.h
+
+        def host_step():
+            if hwin.due():
+                arena.copy_(init)
+                t_state[0] = 0.0
+            hy._ctx.sync_stream()
+            rc = lib.hx_step_host(h, _lib.C.byref(prm), float(t_state[0]), hx_.data_ptr(), hv_.data_ptr(),
+                                  he_.data_ptr(), _lib.C.byref(info_c))
+            if rc != 0:
+                raise RuntimeError(f"hx_step_host failed: rc {rc}, info.code {info_c.code}")
+            t_state[0] = info_c.t_new
+            hwin.advance()
+
+        for _ in range(args.warmup):
+            host_step()
+        e2e_s = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            host_step()
+            e2e_s += time.perf_counter() - t0
+        te = torch.tensor([e2e_s], dtype=torch.float64, device="cpu" if dist.get_backend() == "gloo" else "cuda")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_s = float(te.item())
+        nb = 8 * (nx + nvv + ne_) * world
+        e2e = {"value": V_global * args.steps / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": nb,
+               "d2h_bytes_per_step": nb, "ms_per_step": 1e3 * e2e_s / args.steps,
+               "path": "hx_step_host (C-ABI) from pinned host x, v, e on every rank; max over ranks"}
 
     if rank == 0:
         line = {
@@ -490,7 +529,7 @@ def run_distributed(args, world, rank, local):
                        "l2": "flushed before every timed step",
                        "window": {"horizon_steps": HORIZON, "timed_cycle_indices": timed_idx},
                        "setup_s_rank0": setup_s},
-            "e2e": None, "gpu_launches": None, "roofline": None, "cpu_baseline": None, "clocks": clk.summary(),
+            "e2e": e2e, "gpu_launches": launches, "roofline": None, "cpu_baseline": None, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

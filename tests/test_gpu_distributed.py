@@ -125,24 +125,26 @@ def _graph_worker(rank, world, port, case, out):
     dist.destroy_process_group()
 
 
-def test_graph_step_ranks_match_single_domain_oracle(tmp_path):
-    """Device-resident distributed step (two processes sharing one B200): every
-    exchange -- mass-diagonal and F.1 interface sums, CG halo and world scalars, CFL /
-    clamp / inversion status -- runs inside each rank's step graph."""
+@pytest.mark.parametrize("world", [2, 4])
+def test_graph_step_ranks_match_single_domain_oracle(tmp_path, world):
+    """Device-resident distributed step (two or four processes sharing one B200, 2x1x1 /
+    2x2x1 bricks: four ranks put interior edge nodes on four sharers): every exchange --
+    mass-diagonal and F.1 interface sums, CG halo and world scalars, CFL / clamp /
+    inversion status -- runs inside each rank's step graph."""
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
     out = str(tmp_path / "res")
-    world = 2
-    mp.spawn(_graph_worker, args=(world, port, CASE, out), nprocs=world, join=True)
-    hy, st, _ = _initial(CASE)
+    case = CASE if world == 2 else dict(CASE, counts=(4, 4, 2))
+    mp.spawn(_graph_worker, args=(world, port, case, out), nprocs=world, join=True)
+    hy, st, _ = _initial(case)
     dts = []
-    for _ in range(CASE["steps"]):
-        dt = hy.timestep_estimate(st, CASE["cfl"], dt_max=1.0, t_final=10.0)
+    for _ in range(case["steps"]):
+        dt = hy.timestep_estimate(st, case["cfl"], dt_max=1.0, t_final=10.0)
         st, info = hy.rk2_step(st, dt)
         dts.append(info["dt"])
-    nt = max(CASE["p"], 1) ** CASE["dim"]
+    nt = max(case["p"], 1) ** case["dim"]
     X, V = np.full_like(st["x"], np.nan), np.full_like(st["v"], np.nan)
     E = np.full(st["e"].reshape(-1, nt).shape, np.nan)
     for r in range(world):
