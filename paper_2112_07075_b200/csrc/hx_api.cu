@@ -1125,10 +1125,41 @@ static bool launch_node_row(hx_ctx* ctx, const NodeArgs& na, int* rc) {
   return true;
 }
 
+// HX_NODE_ASYNC=1: the cp.async-staged brick node pass (k_cg_node_async)
+static int g_node_async = -1;
+
+template <int P, int NC>
+static bool launch_node_async(hx_ctx* ctx, const NodeArgs& na, int* rc) {
+  if (g_node_async < 0) {
+    const char* v = getenv("HX_NODE_ASYNC");
+    g_node_async = v ? atoi(v) : 0;
+  }
+  if (!g_node_async || ctx->peer || !na.invdn) return false;
+  using C = NodeAsyncCfg<NC>;
+  auto k = k_cg_node_async<P, NC>;
+  static bool attr = false;
+  if (!attr) {
+    *rc = smem_attr(k, C::bytes) == cudaSuccess ? HX_OK : HX_ECUDA;
+    if (*rc) return true;
+    attr = true;
+  }
+  static unsigned cap = 0;
+  if (!cap) cap = persistent_grid(k, C::NT, C::bytes, 1ll << 40);
+  const long long ntiles = (ctx->nn * NC + C::TN - 1) / C::TN;
+  prof_begin(ctx, K_CGNODE);
+  k<<<(unsigned)std::min<long long>(cap, ntiles), C::NT, C::bytes, ctx->stream>>>(na, ctx->bk);
+  prof_end(ctx);
+  const cudaError_t e = cudaGetLastError();
+  *rc = e == cudaSuccess ? HX_OK : fail(ctx, HX_ECUDA, "k_cg_node_async launch: %s", cudaGetErrorString(e));
+  ++ctx->launches;
+  return true;
+}
+
 template <int NC, class SUM>
 static int launch_cg_nodes(hx_ctx* ctx, const NodeArgs& na, SUM sum, bool init) {
   if constexpr (BrickOrder<SUM>::value > 0) {
     int rc = HX_OK;
+    if (!init && launch_node_async<BrickOrder<SUM>::value, NC>(ctx, na, &rc)) return rc;
     if (!init && launch_node_row<BrickOrder<SUM>::value, NC>(ctx, na, &rc)) return rc;
   }
 #ifndef NODE_PF
