@@ -50,6 +50,7 @@ typedef struct hx_ctx hx_ctx;
 typedef struct hx_mass hx_mass;
 typedef struct hx_force hx_force;
 typedef struct hx_op hx_op;
+typedef struct hx_tmop hx_tmop;
 
 /* Mesh + discretisation description (HighOrderMesh fespace.py:63-80,
  * FiniteElementSpace fespace.py:177-208, QuadratureRule1D tensor_basis.py:41-50,
@@ -189,6 +190,31 @@ int hx_convection_create(hx_ctx* ctx, const double* jinv, const double* u_points
                          double* D_out, hx_op** out);
 int hx_op_apply(hx_op* op, const double* x, double* y);
 int hx_op_destroy(hx_op* op);
+
+/* ---- TMOP mesh optimisation (meshopt.py:248-486) ------------------------- */
+
+/* TMOPObjective.__init__ (meshopt.py:257-287): the per-point target inverses winv
+ * (d,d,nq,NE), wdetW = w_q det W (nq,NE), the anchor positions x0 (NN,d) and the limiting
+ * radii d(x0) (NN), device pointers in the reference layouts (copied).  composite = 0: the
+ * shape metric of metric_for(d) (2D |T|^2/(2 det T) - 1, 3D |T|^2|T^-1|^2/9 - 1); 1:
+ * w_shape * shape + w_size * SizeMetric (metric_for(d, with_size=True): 1, 1). */
+int hx_tmop_create(hx_ctx* ctx, const double* winv, const double* wdetw, const double* x0,
+                   const double* dlim, int composite, double w_shape, double w_size, double gamma,
+                   hx_tmop** out);
+/* gamma (the "auto" value is computed by the caller from hx_tmop_terms, meshopt.py:300-312). */
+int hx_tmop_set_gamma(hx_tmop* op, double gamma);
+/* _mu_term / _limit_term (meshopt.py:335-356): mu_sum = sum w detW mu(T(x)); lim_sum (if
+ * want_limit) = sum_a sum_q w detW ((x - x0)/d)_a^2 without gamma; valid = 0 when det A <= 0
+ * at some point (the objective's +inf sentinel, meshopt.py:357-362). */
+int hx_tmop_terms(hx_tmop* op, const double* x, int want_limit, double* mu_sum, double* lim_sum,
+                  int* valid);
+/* gradient (meshopt.py:376-389, 391-405): dF/dx (NN,d), HX_EINVERTED on an invalid mesh. */
+int hx_tmop_gradient(hx_tmop* op, const double* x, double* grad);
+/* hessian_action (meshopt.py:407-440): H(x) dx (NN,d). */
+int hx_tmop_hessian_action(hx_tmop* op, const double* x, const double* dx, double* out);
+/* hessian_diagonal (meshopt.py:442-486): diag H(x) (NN,d), matrix-free. */
+int hx_tmop_hessian_diagonal(hx_tmop* op, const double* x, double* diag);
+int hx_tmop_destroy(hx_tmop* op);
 
 /* ---- Lagrange phase (hydro.py:220-405) ------------------------------- */
 

@@ -87,6 +87,13 @@ _SIGS = {
     "hx_phase_begin": (C.c_int, [P, P, P, P, P, P, P]),
     "hx_stress": (C.c_int, [P, C.POINTER(Params), P, P, P, P, P, C.POINTER(C.c_double),
                             C.POINTER(C.c_int64), C.POINTER(Inverted)]),
+    "hx_tmop_create": (C.c_int, [P, P, P, P, P, C.c_int, C.c_double, C.c_double, C.c_double, C.POINTER(P)]),
+    "hx_tmop_set_gamma": (C.c_int, [P, C.c_double]),
+    "hx_tmop_terms": (C.c_int, [P, P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int)]),
+    "hx_tmop_gradient": (C.c_int, [P, P, P]),
+    "hx_tmop_hessian_action": (C.c_int, [P, P, P, P]),
+    "hx_tmop_hessian_diagonal": (C.c_int, [P, P, P]),
+    "hx_tmop_destroy": (C.c_int, [P]),
     "hx_timestep_ratio": (C.c_int, [P, C.POINTER(Params), P, P, P, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                     C.POINTER(Inverted)]),
     "hx_energy_solve": (C.c_int, [P, P, P]),

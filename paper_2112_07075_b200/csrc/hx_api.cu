@@ -25,6 +25,7 @@
 #include "hx_brick.cuh"
 #include "hx_rates.cuh"
 #include "hx_remap.cuh"
+#include "hx_tmop.cuh"
 #include "hx_peer.cuh"
 #include "hx_tma.cuh"
 #include "hx_node.cuh"
@@ -151,6 +152,21 @@ struct hx_op {
 struct hx_force {
   hx_ctx* ctx;
   double* DF;  // (NE, d*d, nq)
+};
+
+struct hx_tmop {
+  hx_ctx* ctx;
+  double* winv = nullptr;   // (NE, nq, d, d)
+  double* wdetw = nullptr;  // (NE, nq)
+  double* x0 = nullptr;     // (NN, d)
+  double* dlim = nullptr;   // (NN)
+  double* nb0 = nullptr;    // (NN, d) node scratch: the mu part
+  double* nb1 = nullptr;    // (NN, d) node scratch: limiting field / its assembled part
+  double* epart = nullptr;  // (NE) per-element sums
+  double* sums = nullptr;   // (2) device scalars
+  int* bad = nullptr;       // det A <= 0 seen
+  TmopMetric mt{1.0, 0.0, 0};
+  double gamma = 0.0;
 };
 
 // ---------------------------------------------------------------------------
@@ -1773,6 +1789,214 @@ extern "C" int hx_op_apply(hx_op* op, const double* x, double* y) {
 extern "C" int hx_op_destroy(hx_op* op) {
   if (!op) return HX_OK;
   cudaFree(op->D);
+  delete op;
+  return HX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// TMOP mesh-optimisation operator (meshopt.py:248-486)
+
+template <int DIM, int P>
+struct LaunchTmop {
+  static int run(hx_ctx* ctx, const hx_tmop* op, int mode, const double* x, const double* dx) {
+    using SM = TmopSmem<DIM, P>;
+    TmopArgs a{x, dx, op->winv, op->wdetw, ctx->emap, ctx->slot, ctx->B, ctx->G, op->mt, ctx->ne, ctx->evec2,
+               op->epart, op->bad};
+    constexpr int NT = 128;
+    switch (mode) {
+#define HX_TMOP_MODE(M)                                         \
+  case M: {                                                     \
+    auto k = k_tmop<DIM, P, NT, M>;                             \
+    CK(smem_attr(k, SM::bytes));                                \
+    k<<<(unsigned)ctx->ne, NT, SM::bytes, ctx->stream>>>(a);    \
+    break;                                                      \
+  }
+      HX_TMOP_MODE(0)
+      HX_TMOP_MODE(1)
+      HX_TMOP_MODE(2)
+      HX_TMOP_MODE(3)
+      HX_TMOP_MODE(4)
+      HX_TMOP_MODE(5)
+#undef HX_TMOP_MODE
+      default:
+        return HX_EINVAL;
+    }
+    CKL();
+    return HX_OK;
+  }
+};
+
+__global__ void k_tmop_winv(const double* winv_ref /*(d,d,nq,NE)*/, int d, int nq, long long ne, double* winv) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)d * d * nq * ne) return;
+  const long long e = t % ne, r = t / ne;
+  const int q = (int)(r % nq), bl = (int)(r / nq);
+  winv[(e * nq + q) * d * d + bl] = winv_ref[t];
+}
+
+extern "C" int hx_tmop_create(hx_ctx* ctx, const double* winv, const double* wdetw, const double* x0,
+                              const double* dlim, int composite, double w_shape, double w_size, double gamma,
+                              hx_tmop** out) {
+  if (!ctx || !winv || !wdetw || !x0 || !dlim || !out) return HX_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  const int d = ctx->dim;
+  hx_tmop* op = new hx_tmop();
+  op->ctx = ctx;
+  op->mt = TmopMetric{w_shape, w_size, composite ? 1 : 0};
+  op->gamma = gamma;
+  const size_t nv = (size_t)ctx->nn * d, npq = (size_t)ctx->ne * ctx->nq;
+  bool ok = dalloc(&op->winv, npq * d * d) == cudaSuccess;
+  ok &= dalloc(&op->wdetw, npq) == cudaSuccess;
+  ok &= dalloc(&op->x0, nv) == cudaSuccess;
+  ok &= dalloc(&op->dlim, ctx->nn) == cudaSuccess;
+  ok &= dalloc(&op->nb0, nv) == cudaSuccess;
+  ok &= dalloc(&op->nb1, nv) == cudaSuccess;
+  ok &= dalloc(&op->epart, ctx->ne) == cudaSuccess;
+  ok &= dalloc(&op->sums, 2) == cudaSuccess;
+  ok &= cudaMalloc(&op->bad, sizeof(int)) == cudaSuccess;
+  if (!ok) {
+    hx_tmop_destroy(op);
+    return fail(ctx, HX_ECUDA, "hx_tmop_create: alloc");
+  }
+  const long long nw = (long long)npq * d * d;
+  k_tmop_winv<<<gblocks(nw, 256), 256, 0, ctx->stream>>>(winv, d, ctx->nq, ctx->ne, op->winv);
+  CKL();
+  k_transpose<<<gblocks((long long)npq, 256), 256, 0, ctx->stream>>>(wdetw, ctx->nq, ctx->ne, op->wdetw);
+  CKL();
+  CK(cudaMemcpyAsync(op->x0, x0, sizeof(double) * nv, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(op->dlim, dlim, sizeof(double) * ctx->nn, cudaMemcpyDeviceToDevice, ctx->stream));
+  *out = op;
+  return HX_OK;
+}
+
+extern "C" int hx_tmop_set_gamma(hx_tmop* op, double gamma) {
+  if (!op) return HX_EINVAL;
+  op->gamma = gamma;
+  return HX_OK;
+}
+
+static int tmop_bad_reset(hx_tmop* op) {
+  hx_ctx* ctx = op->ctx;
+  CK(cudaMemsetAsync(op->bad, 0, sizeof(int), ctx->stream));
+  return HX_OK;
+}
+
+static int tmop_bad_read(hx_tmop* op, int* bad) {
+  hx_ctx* ctx = op->ctx;
+  CK(cudaMemcpyAsync(ctx->h_t, op->bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *bad = *reinterpret_cast<int*>(ctx->h_t);
+  return HX_OK;
+}
+
+static int tmop_sum(hx_tmop* op, int slot, double* host) {
+  hx_ctx* ctx = op->ctx;
+  k_sum<<<1, 256, 0, ctx->stream>>>(op->epart, ctx->ne, op->sums + slot);
+  CKL();
+  CK(cudaMemcpyAsync(host, op->sums + slot, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  return HX_OK;
+}
+
+// the two integrals of the objective (meshopt.py:335-356): mu_sum = sum w detW mu(T) at x
+// (valid = 0 when det A <= 0 anywhere: the caller's +inf sentinel, meshopt.py:322-326,
+// 357-362) and, when want_limit, lim_sum = sum_a sum_q w detW ((x - x0)/d)_a^2 (without gamma)
+extern "C" int hx_tmop_terms(hx_tmop* op, const double* x, int want_limit, double* mu_sum, double* lim_sum,
+                             int* valid) {
+  if (!op || !x || !mu_sum || !valid) return HX_EINVAL;
+  hx_ctx* ctx = op->ctx;
+  CK(cudaSetDevice(ctx->device));
+  int rc = tmop_bad_reset(op);
+  if (rc) return rc;
+  rc = dispatch<LaunchTmop>(ctx, (const hx_tmop*)op, 0, x, (const double*)nullptr);
+  if (rc) return rc;
+  double h[2] = {0.0, 0.0};
+  rc = tmop_sum(op, 0, &h[0]);
+  if (rc) return rc;
+  if (want_limit) {
+    const long long nv = ctx->nn * ctx->dim;
+    k_tmop_nodes<<<gblocks(nv, 256), 256, 0, ctx->stream>>>(0, x, op->x0, op->dlim, nullptr, nullptr, 0.0,
+                                                            ctx->dim, ctx->nn, op->nb1);
+    CKL();
+    rc = dispatch<LaunchTmop>(ctx, (const hx_tmop*)op, 4, (const double*)op->nb1, (const double*)nullptr);
+    if (rc) return rc;
+    rc = tmop_sum(op, 1, &h[1]);
+    if (rc) return rc;
+  }
+  int bad = 0;
+  rc = tmop_bad_read(op, &bad);  // synchronises the stream (the sums landed too)
+  if (rc) return rc;
+  *valid = bad ? 0 : 1;
+  *mu_sum = h[0];
+  if (lim_sum) *lim_sum = h[1];
+  return HX_OK;
+}
+
+// kind 1 gradient (x), 2 Hessian action (x, dx), 3 Hessian diagonal (x): the mu part
+// assembled, plus gamma's limiting part (meshopt.py:376-486).  HX_EINVERTED when det A <= 0
+// anywhere (the reference raises ValueError).
+static int tmop_derivative(hx_tmop* op, int kind, const double* x, const double* dx, double* out) {
+  hx_ctx* ctx = op->ctx;
+  CK(cudaSetDevice(ctx->device));
+  const int d = ctx->dim;
+  const long long nv = ctx->nn * d;
+  int rc = tmop_bad_reset(op);
+  if (rc) return rc;
+  rc = dispatch<LaunchTmop>(ctx, (const hx_tmop*)op, kind, x, dx);
+  if (rc) return rc;
+  const bool lim = op->gamma != 0.0;
+  rc = launch_scatter(ctx, ctx->evec2, d, lim ? op->nb0 : out);
+  if (rc) return rc;
+  int bad = 0;
+  rc = tmop_bad_read(op, &bad);
+  if (rc) return rc;
+  if (bad) return fail(ctx, HX_EINVERTED, "TMOP: mesh has non-positive Jacobians");
+  if (!lim) return HX_OK;
+  if (kind == 3) {
+    rc = dispatch<LaunchTmop>(ctx, (const hx_tmop*)op, 5, x, (const double*)nullptr);
+    if (rc) return rc;
+    rc = launch_scatter(ctx, ctx->evec2, 1, op->nb1);
+    if (rc) return rc;
+  } else {
+    k_tmop_nodes<<<gblocks(nv, 256), 256, 0, ctx->stream>>>(kind == 1 ? 0 : 1, kind == 1 ? x : dx, op->x0, op->dlim,
+                                                            nullptr, nullptr, 0.0, d, ctx->nn, op->nb1);
+    CKL();
+    rc = dispatch<LaunchTmop>(ctx, (const hx_tmop*)op, 4, (const double*)op->nb1, (const double*)nullptr);
+    if (rc) return rc;
+    rc = launch_scatter(ctx, ctx->evec2, d, op->nb1);
+    if (rc) return rc;
+  }
+  k_tmop_nodes<<<gblocks(nv, 256), 256, 0, ctx->stream>>>(kind == 3 ? 3 : 2, nullptr, nullptr, op->dlim, op->nb0,
+                                                          op->nb1, op->gamma, d, ctx->nn, out);
+  CKL();
+  return HX_OK;
+}
+
+extern "C" int hx_tmop_gradient(hx_tmop* op, const double* x, double* grad) {
+  if (!op || !x || !grad) return HX_EINVAL;
+  return tmop_derivative(op, 1, x, nullptr, grad);
+}
+
+extern "C" int hx_tmop_hessian_action(hx_tmop* op, const double* x, const double* dx, double* out) {
+  if (!op || !x || !dx || !out) return HX_EINVAL;
+  return tmop_derivative(op, 2, x, dx, out);
+}
+
+extern "C" int hx_tmop_hessian_diagonal(hx_tmop* op, const double* x, double* diag) {
+  if (!op || !x || !diag) return HX_EINVAL;
+  return tmop_derivative(op, 3, x, nullptr, diag);
+}
+
+extern "C" int hx_tmop_destroy(hx_tmop* op) {
+  if (!op) return HX_OK;
+  cudaFree(op->winv);
+  cudaFree(op->wdetw);
+  cudaFree(op->x0);
+  cudaFree(op->dlim);
+  cudaFree(op->nb0);
+  cudaFree(op->nb1);
+  cudaFree(op->epart);
+  cudaFree(op->sums);
+  cudaFree(op->bad);
   delete op;
   return HX_OK;
 }
