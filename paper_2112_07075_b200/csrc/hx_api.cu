@@ -1798,25 +1798,27 @@ extern "C" int hx_op_destroy(hx_op* op) {
 
 template <int DIM, int P>
 struct LaunchTmop {
-  static int run(hx_ctx* ctx, const hx_tmop* op, int mode, const double* x, const double* dx) {
+  static int run(hx_ctx* ctx, const hx_tmop* op, int mode, bool lim, const double* x, const double* dx) {
     using SM = TmopSmem<DIM, P>;
     TmopArgs a{x, dx, op->winv, op->wdetw, ctx->emap, ctx->slot, ctx->B, ctx->G, op->mt, ctx->ne, ctx->evec2,
-               op->epart, op->bad};
+               op->epart, op->bad, op->x0, op->dlim, ctx->evec, op->epart + ctx->ne};
     constexpr int NT = 128;
-    switch (mode) {
-#define HX_TMOP_MODE(M)                                         \
-  case M: {                                                     \
-    auto k = k_tmop<DIM, P, NT, M>;                             \
-    CK(smem_attr(k, SM::bytes));                                \
-    k<<<(unsigned)ctx->ne, NT, SM::bytes, ctx->stream>>>(a);    \
-    break;                                                      \
+    switch (mode * 2 + (lim ? 1 : 0)) {
+#define HX_TMOP_MODE(M, L)                                       \
+  case M * 2 + L: {                                              \
+    auto k = k_tmop<DIM, P, NT, M, L>;                           \
+    CK(smem_attr(k, SM::bytes));                                 \
+    k<<<(unsigned)ctx->ne, NT, SM::bytes, ctx->stream>>>(a);     \
+    break;                                                       \
   }
-      HX_TMOP_MODE(0)
-      HX_TMOP_MODE(1)
-      HX_TMOP_MODE(2)
-      HX_TMOP_MODE(3)
-      HX_TMOP_MODE(4)
-      HX_TMOP_MODE(5)
+      HX_TMOP_MODE(0, false)
+      HX_TMOP_MODE(0, true)
+      HX_TMOP_MODE(1, false)
+      HX_TMOP_MODE(1, true)
+      HX_TMOP_MODE(2, false)
+      HX_TMOP_MODE(2, true)
+      HX_TMOP_MODE(3, false)
+      HX_TMOP_MODE(3, true)
 #undef HX_TMOP_MODE
       default:
         return HX_EINVAL;
@@ -1851,7 +1853,7 @@ extern "C" int hx_tmop_create(hx_ctx* ctx, const double* winv, const double* wde
   ok &= dalloc(&op->dlim, ctx->nn) == cudaSuccess;
   ok &= dalloc(&op->nb0, nv) == cudaSuccess;
   ok &= dalloc(&op->nb1, nv) == cudaSuccess;
-  ok &= dalloc(&op->epart, ctx->ne) == cudaSuccess;
+  ok &= dalloc(&op->epart, 2 * (size_t)ctx->ne) == cudaSuccess;  // mu, limiting
   ok &= dalloc(&op->sums, 2) == cudaSuccess;
   ok &= cudaMalloc(&op->bad, sizeof(int)) == cudaSuccess;
   if (!ok) {
@@ -1891,7 +1893,7 @@ static int tmop_bad_read(hx_tmop* op, int* bad) {
 
 static int tmop_sum(hx_tmop* op, int slot, double* host) {
   hx_ctx* ctx = op->ctx;
-  k_sum<<<1, 256, 0, ctx->stream>>>(op->epart, ctx->ne, op->sums + slot);
+  k_sum<<<1, 256, 0, ctx->stream>>>(op->epart + slot * ctx->ne, ctx->ne, op->sums + slot);
   CKL();
   CK(cudaMemcpyAsync(host, op->sums + slot, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   return HX_OK;
@@ -1907,18 +1909,12 @@ extern "C" int hx_tmop_terms(hx_tmop* op, const double* x, int want_limit, doubl
   CK(cudaSetDevice(ctx->device));
   int rc = tmop_bad_reset(op);
   if (rc) return rc;
-  rc = dispatch<LaunchTmop>(ctx, (const hx_tmop*)op, 0, x, (const double*)nullptr);
+  rc = dispatch<LaunchTmop>(ctx, (const hx_tmop*)op, 0, want_limit != 0, x, (const double*)nullptr);
   if (rc) return rc;
   double h[2] = {0.0, 0.0};
   rc = tmop_sum(op, 0, &h[0]);
   if (rc) return rc;
   if (want_limit) {
-    const long long nv = ctx->nn * ctx->dim;
-    k_tmop_nodes<<<gblocks(nv, 256), 256, 0, ctx->stream>>>(0, x, op->x0, op->dlim, nullptr, nullptr, 0.0,
-                                                            ctx->dim, ctx->nn, op->nb1);
-    CKL();
-    rc = dispatch<LaunchTmop>(ctx, (const hx_tmop*)op, 4, (const double*)op->nb1, (const double*)nullptr);
-    if (rc) return rc;
     rc = tmop_sum(op, 1, &h[1]);
     if (rc) return rc;
   }
@@ -1941,33 +1937,22 @@ static int tmop_derivative(hx_tmop* op, int kind, const double* x, const double*
   const long long nv = ctx->nn * d;
   int rc = tmop_bad_reset(op);
   if (rc) return rc;
-  rc = dispatch<LaunchTmop>(ctx, (const hx_tmop*)op, kind, x, dx);
-  if (rc) return rc;
   const bool lim = op->gamma != 0.0;
+  rc = dispatch<LaunchTmop>(ctx, (const hx_tmop*)op, kind, lim, x, dx);
+  if (rc) return rc;
   rc = launch_scatter(ctx, ctx->evec2, d, lim ? op->nb0 : out);
   if (rc) return rc;
+  if (lim) {  // the limiting element vectors (same launch) -> nodes, then the reference's combine
+    rc = launch_scatter(ctx, ctx->evec, kind == 3 ? 1 : d, op->nb1);
+    if (rc) return rc;
+    k_tmop_nodes<<<gblocks(nv, 256), 256, 0, ctx->stream>>>(kind == 3 ? 3 : 2, nullptr, nullptr, op->dlim, op->nb0,
+                                                            op->nb1, op->gamma, d, ctx->nn, out);
+    CKL();
+  }
   int bad = 0;
   rc = tmop_bad_read(op, &bad);
   if (rc) return rc;
   if (bad) return fail(ctx, HX_EINVERTED, "TMOP: mesh has non-positive Jacobians");
-  if (!lim) return HX_OK;
-  if (kind == 3) {
-    rc = dispatch<LaunchTmop>(ctx, (const hx_tmop*)op, 5, x, (const double*)nullptr);
-    if (rc) return rc;
-    rc = launch_scatter(ctx, ctx->evec2, 1, op->nb1);
-    if (rc) return rc;
-  } else {
-    k_tmop_nodes<<<gblocks(nv, 256), 256, 0, ctx->stream>>>(kind == 1 ? 0 : 1, kind == 1 ? x : dx, op->x0, op->dlim,
-                                                            nullptr, nullptr, 0.0, d, ctx->nn, op->nb1);
-    CKL();
-    rc = dispatch<LaunchTmop>(ctx, (const hx_tmop*)op, 4, (const double*)op->nb1, (const double*)nullptr);
-    if (rc) return rc;
-    rc = launch_scatter(ctx, ctx->evec2, d, op->nb1);
-    if (rc) return rc;
-  }
-  k_tmop_nodes<<<gblocks(nv, 256), 256, 0, ctx->stream>>>(kind == 3 ? 3 : 2, nullptr, nullptr, op->dlim, op->nb0,
-                                                          op->nb1, op->gamma, d, ctx->nn, out);
-  CKL();
   return HX_OK;
 }
 

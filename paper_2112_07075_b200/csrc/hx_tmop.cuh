@@ -11,10 +11,11 @@
 //           P = dS W^{-T} w detW, grad_t                                (meshopt.py:407-424)
 //   MODE 3  Hessian diagonal: K_a[l1,l2] = W^{-1} h4[a,:,a,:] W^{-T} w detW contracted
 //           with the per-axis basis products (B B, B G, G G)            (meshopt.py:442-486)
-// and the limiting term's pieces (meshopt.py:342-356, 391-405, 426-440, 480-484):
-//   MODE 4  r at the points (interp of the nodal r = (x - x0)/d or dx/d): per-element
-//           sum_a sum_q w detW r_a^2 and the element vectors B^T (w detW r_a)
-//   MODE 5  limiting diagonal: (B o B)^T w detW per element (component independent)
+// and, with LIM (gamma != 0), the limiting term's pieces in the same element pass
+// (meshopt.py:342-356, 391-405, 426-440, 480-484): r = (x - x0)/d (objective, gradient) or
+// dx/d (Hessian action) formed at the gather with the reference's rounding, interpolated to
+// the points: the per-element sum_a sum_q w detW r_a^2 (MODE 0) or the element vectors
+// B^T (w detW r_a) (MODE 1, 2) into a second E-vector; MODE 3 adds (B o B)^T w detW.
 // E-vectors are node-sorted and summed by the deterministic CSR node pass (scatter_add
 // order).  The metric derivatives are analytic (shape: 2D |T|^2/(2 det T) - 1, 3D
 // |T|^2 |T^{-1}|^2 / 9 - 1; size (det T + 1/det T)/2 - 1; composite = w_shape * shape +
@@ -253,12 +254,16 @@ struct TmopArgs {
   const double* G;
   TmopMetric mt;
   long long ne;
-  double* evec;         // (NE*nl, NC) node-sorted element vectors
-  double* epart;        // (NE) per-element sums (MODE 0, MODE 4)
-  int* bad;             // set when det A <= 0 at any point (MODE 0-3)
+  double* evec;         // (NE*nl, NC) node-sorted element vectors (mu part)
+  double* epart;        // (NE) per-element sums (MODE 0)
+  int* bad;             // set when det A <= 0 at any point
+  const double* x0;     // (NN, d) limiting anchor (LIM)
+  const double* dlim;   // (NN) limiting radii (LIM)
+  double* evec2;        // (NE*nl, NC) limiting element vectors (LIM, MODE 1-3)
+  double* epart2;       // (NE) limiting per-element sums (LIM, MODE 0)
 };
 
-template <int DIM, int P, int NT, int MODE>
+template <int DIM, int P, int NT, int MODE, bool LIM>
 __global__ void __launch_bounds__(NT) k_tmop(TmopArgs a) {
   using D = Disc<DIM, P>;
   using SM = TmopSmem<DIM, P>;
@@ -289,43 +294,54 @@ __global__ void __launch_bounds__(NT) k_tmop(TmopArgs a) {
   const int* em = a.emap + e * NL;
   const double* We = a.winv + e * NQ * DIM * DIM;
   const double* wd = a.wdetw + e * NQ;
-  if constexpr (MODE == 5) {  // limiting diagonal: (B o B)^T-interpolated w detW
-    for (int q = tid; q < NQ; q += NT) rA[q] = wd[q];
-    __syncthreads();
-    const double* res = interp_t<DIM, D1, Q, 1, NT>(sBB, rA, rS, tid);
-    __syncthreads();
-    for (int i = tid; i < NL; i += NT) a.evec[a.slot[e * NL + i]] = res[i];
-    return;
-  }
-  // gather the nodal field(s): x (or r) -> rA (component-major)
+  // the limiting term of this element (LIM): r = (x - x0)/d or dx/d at the nodes ->
+  // the points -> sum w detW r^2 (MODE 0) or B^T (w detW r) into evec2 (MODE 1, 2); the
+  // diagonal's (B o B)^T w detW (MODE 3).  Uses rA, rS, rO only.
+  auto limiting = [&]() {
+    if constexpr (MODE == 3) {
+      for (int q = tid; q < NQ; q += NT) rA[q] = wd[q];
+      __syncthreads();
+      const double* res = interp_t<DIM, D1, Q, 1, NT>(sBB, rA, rS, tid);
+      __syncthreads();
+      for (int i = tid; i < NL; i += NT) a.evec2[a.slot[e * NL + i]] = res[i];
+    } else {
+      const double* src = MODE == 2 ? a.dx : a.x;
+      for (int i = tid; i < NL * DIM; i += NT) {
+        const int l = i / DIM, c = i - l * DIM;
+        const long long n = em[l];
+        const double d = a.dlim[n];
+        rA[c * NL + l] = MODE == 2 ? src[n * DIM + c] / d : (src[n * DIM + c] - a.x0[n * DIM + c]) / d;
+      }
+      __syncthreads();
+      double* rq = interp<DIM, D1, Q, DIM, NT>(sB, rA, rS, tid);
+      __syncthreads();
+      if constexpr (MODE == 0) {
+        double acc = 0.0;
+        for (int i = tid; i < DIM * NQ; i += NT) {
+          const double v = rq[i];
+          acc = fma(wd[i % NQ] * v, v, acc);
+        }
+        const double tot = block_sum<NT>(acc, red);
+        if (tid == 0) a.epart2[e] = tot;
+      } else {
+        for (int i = tid; i < DIM * NQ; i += NT) rO[i] = wd[i % NQ] * rq[i];
+        __syncthreads();
+        const double* res = interp_t<DIM, D1, Q, DIM, NT>(sB, rO, rS, tid);
+        __syncthreads();
+        for (int i = tid; i < NL * DIM; i += NT) {
+          const int l = i / DIM, c = i - l * DIM;
+          a.evec2[(long long)a.slot[e * NL + l] * DIM + c] = res[c * NL + l];
+        }
+      }
+    }
+  };
+  // gather the positions -> rA (component-major)
   for (int i = tid; i < NL * DIM; i += NT) {
     const int l = i / DIM, c = i - l * DIM;
     rA[c * NL + l] = a.x[(long long)em[l] * DIM + c];
   }
   __syncthreads();
-  if constexpr (MODE == 4) {
-    // r at the points (tensor interp per component), its w detW-weighted square sum, and
-    // B^T (w detW r) per component
-    double* rq = interp<DIM, D1, Q, DIM, NT>(sB, rA, rS, tid);
-    __syncthreads();
-    double acc = 0.0;
-    for (int i = tid; i < DIM * NQ; i += NT) {
-      const int q = i % NQ;
-      const double v = rq[i];
-      acc = fma(wd[q] * v, v, acc);
-      rO[i] = wd[q] * v;
-    }
-    const double tot = block_sum<NT>(acc, red);
-    if (tid == 0) a.epart[e] = tot;
-    __syncthreads();
-    const double* res = interp_t<DIM, D1, Q, DIM, NT>(sB, rO, rS, tid);
-    __syncthreads();
-    for (int i = tid; i < NL * DIM; i += NT) {
-      const int l = i / DIM, c = i - l * DIM;
-      a.evec[(long long)a.slot[e * NL + l] * DIM + c] = res[c * NL + l];
-    }
-    return;
-  } else {
+  {
     grad<DIM, D1, Q, DIM, DIM + 1, NT>(sB, sG, rA, rS, rA, rO, tid);  // A[a][l] at the points
     __syncthreads();
     if constexpr (MODE == 2) {
@@ -423,6 +439,10 @@ __global__ void __launch_bounds__(NT) k_tmop(TmopArgs a) {
     if constexpr (MODE == 0) {
       const double tot = block_sum<NT>(acc, red);
       if (tid == 0) a.epart[e] = tot;
+      if constexpr (LIM) {
+        __syncthreads();
+        limiting();
+      }
       return;
     }
     __syncthreads();
@@ -466,13 +486,12 @@ __global__ void __launch_bounds__(NT) k_tmop(TmopArgs a) {
       const int l = i / DIM, c = i - l * DIM;
       a.evec[(long long)a.slot[e * NL + l] * DIM + c] = rR[c * NL + l];
     }
+    if constexpr (LIM) limiting();  // rA / rS / rO are free (grad_t / the diagonal are done)
   }
 }
 
-// node-level finishing steps (elementwise, reference rounding):
-//   mode 0  r = (x - x0) / d           (meshopt.py:342-343)
-//   mode 1  r = dx / d                 (meshopt.py:429)
-//   mode 2  out = mu + (2 gamma s) / d (gradient / Hessian action, meshopt.py:387-389, 422-424)
+// node-level combine of the two assembled parts (elementwise, reference rounding):
+//   mode 2  out = mu + (2 gamma s) / d   (gradient / Hessian action, meshopt.py:387-389, 422-424)
 //   mode 3  out = mu + (2 gamma s) / d^2, s per node broadcast over components (meshopt.py:480-484)
 __global__ void k_tmop_nodes(int mode, const double* x, const double* x0, const double* dlim, const double* mu,
                              const double* s, double gamma, int dim, long long nn, double* out) {
@@ -480,10 +499,10 @@ __global__ void k_tmop_nodes(int mode, const double* x, const double* x0, const 
   if (j >= nn * dim) return;
   const long long n = j / dim;
   const double d = dlim[n];
-  if (mode == 0) out[j] = (x[j] - x0[j]) / d;
-  else if (mode == 1) out[j] = x[j] / d;
-  else if (mode == 2) out[j] = mu[j] + (2.0 * gamma * s[j]) / d;
+  if (mode == 2) out[j] = mu[j] + (2.0 * gamma * s[j]) / d;
   else out[j] = mu[j] + (2.0 * gamma * s[n]) / (d * d);
+  (void)x;
+  (void)x0;
 }
 
 }  // namespace hx
