@@ -330,8 +330,11 @@ def run_reference(args, rank):
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"3D Sedov blast Q{args.p}-Q{args.p - 1} (CPU sample {n}^3 elements per step)",
-                   "global_batch": V, "seq_len": None, "parallelism": "cpu", "window_steps": HORIZON},
+        # the GPU arm's workload name; the CPU times a stated sample of it per step
+        "config": {"workload": f"{problem_setup(args)[3]}, {3 * (args.p * args.n + 1) ** 3} velocity dofs per GPU, "
+                               f"CFL {args.cfl}",
+                   "sample": f"{n}^3 elements per CPU step ({V} velocity dofs), same window", "global_batch": V,
+                   "seq_len": None, "parallelism": "cpu", "window_steps": HORIZON},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
                          "one_core": {"value": one_core, "unit": UNIT, "cores": 1,
                                       "sample": f"{len(t1)} steps after 1 warm-up, BLAS threads = 1"}},
