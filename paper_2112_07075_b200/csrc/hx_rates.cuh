@@ -3,7 +3,7 @@
 // stress_qdata (hydro.py:254-315), ForcePA F.1 and F^T v (operators.py:247-300) and
 // M_e^{-1} (hydro.py:339-344).  D_F never leaves shared memory.
 //
-// A CTA of 256 threads runs EPC elements per pass.  Every sum-factorisation stage is
+// A CTA of RATES_PC_NT (128) threads runs EPC elements per pass (one at p = 3, two at p = 2).  Every sum-factorisation stage is
 // its own phase with one thread per 1D line, so no thread carries more than one
 // line of one stage (short dependency chains, modest registers, all lanes busy):
 //   A   prefetch one pass ahead: x, v node rows (6 fields) by cp.async -> G image;
@@ -30,11 +30,17 @@
 
 namespace hx {
 
+#ifndef RATES_PC_NT
+#define RATES_PC_NT 128  // one element per CTA at p = 3 (measured: 123 vs 137 us with 2 per 256-thread CTA)
+#endif
+#ifndef RATES_PC_MINB
+#define RATES_PC_MINB (512 / RATES_PC_NT)
+#endif
 template <int P>
 struct RatesPC {
   static constexpr int D1 = P + 1, Q = P + 2, DT = P, DD = D1 * D1, QQ = Q * Q, NL = D1 * DD, NQ = Q * QQ;
   static constexpr int NT = DT * DT * DT, DTT = DT * DT;
-  static constexpr int THREADS = 256;
+  static constexpr int THREADS = RATES_PC_NT;
   static constexpr int EPC = THREADS / NQ > 0 ? THREADS / NQ : 1;
   static constexpr int XPL = 6 * D1;                   // field planes
   // G image: the node rows of x and of v as they lie in memory (D1 nodes x 3 comps per
@@ -156,7 +162,7 @@ __device__ __forceinline__ void point_physics_fast(const double (&J)[3][3], cons
 }
 
 template <int P, int MODE>
-__global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
+__global__ void __launch_bounds__(RATES_PC_NT, RATES_PC_MINB) k_rates_pc(RatesPCArgs a) {
   using R = RatesPC<P>;
   constexpr int D1 = R::D1, Q = R::Q, DT = R::DT, DD = R::DD, QQ = R::QQ, NL = R::NL, NQ = R::NQ;
   constexpr int NTH = R::NT, DTT = R::DTT, EPC = R::EPC, RP = R::RP, GRP = R::GRP;
@@ -601,7 +607,7 @@ __global__ void __launch_bounds__(256, 2) k_rates_pc(RatesPCArgs a) {
       a.de[e * NTH + i] = s;
     }
   }
-  publish_status<256>(a.st, rmin, clamps, key, nullptr);
+  publish_status<NT>(a.st, rmin, clamps, key, nullptr);
 }
 
 
