@@ -1808,7 +1808,9 @@ struct LaunchTmop {
   case M * 2 + L: {                                              \
     auto k = k_tmop<DIM, P, NT, M, L>;                           \
     CK(smem_attr(k, SM::bytes));                                 \
-    k<<<(unsigned)ctx->ne, NT, SM::bytes, ctx->stream>>>(a);     \
+    static unsigned grid = 0;                                    \
+    if (!grid) grid = persistent_grid(k, NT, SM::bytes, 1ll << 40); \
+    k<<<std::min<unsigned>(grid, gblocks(ctx->ne, 1)), NT, SM::bytes, ctx->stream>>>(a); \
     break;                                                       \
   }
       HX_TMOP_MODE(0, false)

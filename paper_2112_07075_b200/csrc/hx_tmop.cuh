@@ -264,7 +264,7 @@ struct TmopArgs {
 };
 
 template <int DIM, int P, int NT, int MODE, bool LIM>
-__global__ void __launch_bounds__(NT) k_tmop(TmopArgs a) {
+__global__ void __launch_bounds__(NT) k_tmop(TmopArgs a) {  // persistent grid
   using D = Disc<DIM, P>;
   using SM = TmopSmem<DIM, P>;
   constexpr int D1 = D::D1, Q = D::Q, NL = D::NL, NQ = D::NQ, QD = Q * D1;
@@ -282,7 +282,6 @@ __global__ void __launch_bounds__(NT) k_tmop(TmopArgs a) {
   double* rO2 = rO + SM::OUT;
   double* rR = rO2 + SM::OUT2;
   const int tid = threadIdx.x;
-  const long long e = blockIdx.x;
   for (int i = tid; i < QD; i += NT) {
     const double b = a.B[i], g = a.G[i];
     sB[i] = b;
@@ -291,6 +290,9 @@ __global__ void __launch_bounds__(NT) k_tmop(TmopArgs a) {
     sBG[i] = b * g;
     sGG[i] = g * g;
   }
+  __syncthreads();
+  // persistent CTAs: the tables once, then one element at a time (grid-stride)
+  auto element = [&](const long long e) {
   const int* em = a.emap + e * NL;
   const double* We = a.winv + e * NQ * DIM * DIM;
   const double* wd = a.wdetw + e * NQ;
@@ -487,6 +489,11 @@ __global__ void __launch_bounds__(NT) k_tmop(TmopArgs a) {
       a.evec[(long long)a.slot[e * NL + l] * DIM + c] = rR[c * NL + l];
     }
     if constexpr (LIM) limiting();  // rA / rS / rO are free (grad_t / the diagonal are done)
+  }
+  };
+  for (long long e = blockIdx.x; e < a.ne; e += gridDim.x) {
+    element(e);
+    __syncthreads();  // the element's images are dead before the next gather
   }
 }
 

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--n", type=int, default=23)
     ap.add_argument("--p", type=int, default=3)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--cpu-n", type=int, default=8, help="CPU reference sample: elements per direction (0: skip)")
     args = ap.parse_args()
     from paper_2112_07075_b200 import _lib, meshopt
     from paper_2112_07075_b200._device import to_dev
@@ -74,12 +75,43 @@ def main():
             e1.synchronize()
             tot += e0.elapsed_time(e1)
         res[name] = {"ms": tot / args.reps, "Mdof_per_s": V / (tot / args.reps / 1e3) / 1e6}
+    # the reference's own CPU path (baseline/_ref, unmodified) beside it, on an n^3 sample
+    cpu = None
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if args.cpu_n > 0 and os.path.isdir(os.path.join(ref_dir, "ale_minihydro")):
+        import time
+
+        sys.path.insert(0, ref_dir)
+        from ale_minihydro import fespace as rf
+        from ale_minihydro import meshopt as rm
+        from ale_minihydro import tensor_basis as rt
+
+        cn = args.cpu_n
+        rmesh = rf.cartesian_mesh(d, (1.0,) * d, (cn,) * d, p)
+        rquad = rt.gauss_legendre(p + 2)
+        robj = rm.TMOPObjective(rmesh, rquad, rm.build_targets(rmesh, rquad), gamma=1.0)
+        rfree = robj.free_interior_mask()
+        rh = 1.0 / (cn * p)
+        rx = rmesh.coords + np.where(rfree, 0.1 * rh * rng.uniform(-1, 1, rmesh.coords.shape), 0.0)
+        rdx = np.where(rfree, rng.standard_normal(rx.shape), 0.0)
+        cpu = {"sample": f"3D Q{p} {cn}^3 elements ({d * rmesh.num_nodes} position dofs), baseline/_ref "
+                         f"ale_minihydro.meshopt (unmodified), {os.cpu_count()} host cores available"}
+        Vc = d * rmesh.num_nodes
+        for name, fn in (("gradient", lambda: robj.gradient(rx)),
+                         ("hessian_action", lambda: robj.hessian_action(rx, rdx))):
+            fn()
+            t0 = time.perf_counter()
+            for _ in range(2):
+                fn()
+            ms = 1e3 * (time.perf_counter() - t0) / 2
+            cpu[name] = {"ms": ms, "Mdof_per_s": Vc / (ms / 1e3) / 1e6}
     pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     ha_gbs = alg_ha / (res["hessian_action"]["ms"] / 1e3) / 1e9
     print(json.dumps({"workload": f"TMOP 3D Q{p} {n}^3 elements ({V} position dofs), 0.1h perturbation, ideal-uniform "
                                   f"targets, gamma {obj.gamma:.4g}", "calls": res,
                       "hessian_action_roofline": {"alg_bytes": alg_ha, "achieved_gbs": ha_gbs, "peak_gbs": pk,
                                                   "frac": ha_gbs / pk},
+                      "cpu_reference": cpu,
                       "note": "CUDA events around each C-ABI call (kernel + scatter + limiting pieces; "
                               "objective includes its host read-back), L2 flushed before each call"}))
 
