@@ -40,7 +40,9 @@ template <int P>
 struct RatesPC {
   static constexpr int D1 = P + 1, Q = P + 2, DT = P, DD = D1 * D1, QQ = Q * Q, NL = D1 * DD, NQ = Q * QQ;
   static constexpr int NT = DT * DT * DT, DTT = DT * DT;
-  static constexpr int THREADS = RATES_PC_NT;
+  // p = 4 (216 points) keeps 256 threads: one point per thread in the z / physics stage
+  // (128 threads measured 255 vs 189 us there)
+  static constexpr int THREADS = P >= 4 ? 256 : RATES_PC_NT;
   static constexpr int EPC = THREADS / NQ > 0 ? THREADS / NQ : 1;
   static constexpr int XPL = 6 * D1;                   // field planes
   // G image: the node rows of x and of v as they lie in memory (D1 nodes x 3 comps per
@@ -162,7 +164,7 @@ __device__ __forceinline__ void point_physics_fast(const double (&J)[3][3], cons
 }
 
 template <int P, int MODE>
-__global__ void __launch_bounds__(RATES_PC_NT, RATES_PC_MINB) k_rates_pc(RatesPCArgs a) {
+__global__ void __launch_bounds__(RatesPC<P>::THREADS, P >= 4 ? 2 : RATES_PC_MINB) k_rates_pc(RatesPCArgs a) {
   using R = RatesPC<P>;
   constexpr int D1 = R::D1, Q = R::Q, DT = R::DT, DD = R::DD, QQ = R::QQ, NL = R::NL, NQ = R::NQ;
   constexpr int NTH = R::NT, DTT = R::DTT, EPC = R::EPC, RP = R::RP, GRP = R::GRP;

@@ -2,7 +2,7 @@
 # bench every BASELINE.json config on one GPU (usage: tools/gpu_configs.sh TAG)
 TAG=${1:-cfg}; export TAG
 mkdir -p gpurun_out/cfg_$TAG
-run() { NAME=$1; shift; timeout 400 python bench.py --steps 10 --warmup 3 --no-cpu "$@" > gpurun_out/cfg_$TAG/$NAME.json 2> gpurun_out/cfg_$TAG/$NAME.err; tail -1 gpurun_out/cfg_$TAG/$NAME.err | cut -c1-200; }
+run() { NAME=$1; shift; timeout 400 python bench.py --steps 20 --warmup 5 --no-cpu "$@" > gpurun_out/cfg_$TAG/$NAME.json 2> gpurun_out/cfg_$TAG/$NAME.err; tail -1 gpurun_out/cfg_$TAG/$NAME.err | cut -c1-200; }
 run sedov_q3_n23 --p 3 --n 23
 run sedov_q2_n34 --p 2 --n 34
 run tgv_q4_n17 --p 4 --n 17 --problem tgv
