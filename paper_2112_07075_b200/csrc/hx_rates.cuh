@@ -207,6 +207,17 @@ __global__ void __launch_bounds__(RatesPC<P>::THREADS, P >= 4 ? 2 : RATES_PC_MIN
       const int fel = (int)((a.ne - f0) < EPC ? (a.ne - f0) : EPC);
       double* fb = smem + b * FS;
       constexpr int ROW = 3 * D1;  // doubles per node row (D1 nodes x 3 comps, contiguous)
+      long long nb[EPC];  // brick: the pass's element base nodes, once per pass (not per item)
+      if (a.brick) {
+#pragma unroll
+        for (int el = 0; el < EPC; ++el) {
+          const unsigned ue = (unsigned)(f0 + el);
+          const unsigned ez = a.b.fnxy.div(ue);
+          const unsigned r2 = ue - ez * (unsigned)(a.b.nx * a.b.ny);
+          const unsigned ey = a.b.fnx.div(r2), ex = r2 - ey * (unsigned)a.b.nx;
+          nb[el] = (long long)(ex * P) + (long long)(ey * P) * a.b.Nx + (long long)(ez * P) * a.b.NxNy;
+        }
+      }
       for (int it = t; it < fel * DD * ROW; it += NT) {
         const int el = it / (DD * ROW), rem = it - el * (DD * ROW);
         const int row = rem / ROW, sidx = rem - row * ROW;  // row = dz*D1 + dy
@@ -214,11 +225,11 @@ __global__ void __launch_bounds__(RatesPC<P>::THREADS, P >= 4 ? 2 : RATES_PC_MIN
         const long long e = f0 + el;
         long long n;
         if (a.brick) {
-          const unsigned ue = (unsigned)e;
-          const unsigned ez = a.b.fnxy.div(ue);
-          const unsigned r2 = ue - ez * (unsigned)(a.b.nx * a.b.ny);
-          const unsigned ey = a.b.fnx.div(r2), ex = r2 - ey * (unsigned)a.b.nx;
-          n = (long long)(ex * P + dx) + (long long)(ey * P + dy) * a.b.Nx + (long long)(ez * P + dz) * a.b.NxNy;
+          long long b0 = nb[0];
+#pragma unroll
+          for (int u = 1; u < EPC; ++u)
+            if (el == u) b0 = nb[u];
+          n = b0 + dx + (long long)dy * a.b.Nx + (long long)dz * a.b.NxNy;
         } else {
           n = __ldg(a.emap + e * NL + row * D1 + dx);
         }
@@ -653,6 +664,17 @@ __global__ void __launch_bounds__(128, VALID_MINB) k_valid(RatesPCArgs a) {
     // gather x node rows -> G image (aliases the T image of the previous pass); every
     // load of the thread is issued before the first shared store
     constexpr int ROW = 3 * D1, GI = EPC * DD * ROW, GU = (GI + NT - 1) / NT;
+    long long nb[EPC];  // brick: the pass's element base nodes, once per pass
+    if (a.brick) {
+#pragma unroll
+      for (int el = 0; el < EPC; ++el) {
+        const unsigned ue = (unsigned)(e0 + el);
+        const unsigned ez = a.b.fnxy.div(ue);
+        const unsigned r2 = ue - ez * (unsigned)(a.b.nx * a.b.ny);
+        const unsigned ey = a.b.fnx.div(r2), ex = r2 - ey * (unsigned)a.b.nx;
+        nb[el] = (long long)(ex * P) + (long long)(ey * P) * a.b.Nx + (long long)(ez * P) * a.b.NxNy;
+      }
+    }
     {
       double xv[GU];
       int so[GU];
@@ -667,11 +689,11 @@ __global__ void __launch_bounds__(128, VALID_MINB) k_valid(RatesPCArgs a) {
           const long long e = e0 + el;
           long long n;
           if (a.brick) {
-            const unsigned ue = (unsigned)e;
-            const unsigned ez = a.b.fnxy.div(ue);
-            const unsigned r2 = ue - ez * (unsigned)(a.b.nx * a.b.ny);
-            const unsigned ey = a.b.fnx.div(r2), ex = r2 - ey * (unsigned)a.b.nx;
-            n = (long long)(ex * P + dx) + (long long)(ey * P + dy) * a.b.Nx + (long long)(ez * P + dz) * a.b.NxNy;
+            long long b0 = nb[0];
+#pragma unroll
+            for (int u = 1; u < EPC; ++u)
+              if (el == u) b0 = nb[u];
+            n = b0 + dx + (long long)dy * a.b.Nx + (long long)dz * a.b.NxNy;
           } else {
             n = __ldg(a.emap + e * NL + row * D1 + dx);
           }
