@@ -403,7 +403,24 @@ def run_distributed(args, world, rank, local):
     ctl = StepControls(cfl=args.cfl, dt_max=1.0, t_final=1e9)
     V_global = d * int(np.prod([c * p + 1 for c in counts]))
     win = Window()
-    if args.host_cg:
+    # device-resident exchanges need every pair of ranks to map each other's mailbox (CUDA
+    # IPC + peer access); if any rank cannot, every rank falls back to the host-driven step
+    use_peer = not args.host_cg
+    if use_peer:
+        ok, pex = 1, None
+        try:
+            pex = PeerExchange(lhy, sub, maxh)
+            pex.connect_ipc()
+        except Exception as exc:  # noqa: BLE001
+            ok = 0
+            print(f"[rank {rank}] peer-memory exchange unavailable ({exc}); host-driven fallback", file=sys.stderr)
+        flag = torch.tensor([ok], dtype=torch.int32, device="cpu" if dist.get_backend() == "gloo" else "cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            if ok and pex is not None:
+                pex.close()
+            use_peer = False
+    if not use_peer:
         ops = DeviceOps(sub, 1.4, 0.5, 2.0)
         dl = DistributedLagrange(sub, ops, 1.4, device="cuda")
         dl.begin_phase(x, q0)
@@ -426,7 +443,6 @@ def run_distributed(args, world, rank, local):
         # every exchange inside (F.1 / diagonal interface sums, CG halo + world scalars,
         # CFL / clamp / inversion status) over CUDA-IPC-mapped peer mailboxes
         hy = lhy
-        PeerExchange(hy, sub, maxh).connect_ipc()
         hy.begin_phase(HydroState(x, v, e, q0, 0.0))  # again: the mass diagonal's interface sums
         bufs = [(torch.empty_like(x), torch.empty_like(v), torch.empty_like(e)) for _ in range(2)]
         cg_mode = "device-resident step graph per rank (peer-memory exchanges, one host sync per step)"
@@ -450,7 +466,7 @@ def run_distributed(args, world, rank, local):
     stream = torch.cuda.current_stream()
     dist.barrier()
     torch.cuda.synchronize()
-    launches0 = hy._ctx.launches() if not args.host_cg else 0
+    launches0 = hy._ctx.launches() if use_peer else 0
     tot = 0.0
     timed_idx = []
     with ClockSampler(local) as clk:
@@ -468,7 +484,7 @@ def run_distributed(args, world, rank, local):
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     tot = float(tt.item())
     launches = None
-    if not args.host_cg:
+    if use_peer:
         ll = torch.tensor([float(hy._ctx.launches() - launches0)], dtype=torch.float64,
                           device="cpu" if dist.get_backend() == "gloo" else "cuda")
         dist.all_reduce(ll)
@@ -478,7 +494,7 @@ def run_distributed(args, world, rank, local):
     # pinned host x, v, e -> H2D, the step graph with its peer exchanges, D2H), the same
     # window; time = max over ranks of the host wall clock around the call
     e2e = None
-    if not args.no_e2e and not args.host_cg:
+    if not args.no_e2e and use_peer:
         from paper_2112_07075_b200 import _lib
 
         nx, nvv, ne_ = x.numel(), v.numel(), e.numel()
