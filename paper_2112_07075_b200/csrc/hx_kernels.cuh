@@ -380,6 +380,9 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+#ifndef PEER_WORLD_PURE
+#define PEER_WORLD_PURE 0
+#endif
 #ifndef PEER_SPIN_PURE
 #define PEER_SPIN_PURE 0
 #endif
@@ -468,7 +471,7 @@ __device__ __forceinline__ bool peer_world(const PeerLite& pl, unsigned long lon
       unsigned long long spins = 0;
       const unsigned long long* f = mb_flag(pl.me, q);
       while (ld_relaxed_sys(f) < seq) {
-        __nanosleep(32);
+        if (spins >= PEER_WORLD_PURE) __nanosleep(32);  // pure polls first, then back off
         if (++spins > PEER_SPIN_LIMIT) {
           ok = 0;
           break;
