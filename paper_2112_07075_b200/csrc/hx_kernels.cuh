@@ -1239,6 +1239,9 @@ __device__ __forceinline__ void node_sum(const int* off, const int* idx, const d
 #ifndef NODE_MINB
 #define NODE_MINB 4
 #endif
+#ifndef NODE_PEER_MINB
+#define NODE_PEER_MINB NODE_MINB
+#endif
 struct NodeArgs {
   const int* off;
   const int* idx;
@@ -1416,7 +1419,7 @@ __global__ void __launch_bounds__(256, NODE_MINB) k_cg_node(NodeArgs a, SUM sum)
 // world p.Ap handshake; interface nodes add the neighbours' partials afterwards
 // (PEER = false: the same prologue overlap on one GPU, NODE_PF)
 template <int NC, class SUM, bool PEER = true>
-__global__ void __launch_bounds__(256, NODE_MINB) k_cg_node_peer(NodeArgs a, SUM sum) {
+__global__ void __launch_bounds__(256, PEER ? NODE_PEER_MINB : NODE_MINB) k_cg_node_peer(NodeArgs a, SUM sum) {
   __shared__ double red[32];
   CGDev* g = a.cg;
   if (!g->active) return;
