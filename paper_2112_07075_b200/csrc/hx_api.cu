@@ -121,6 +121,13 @@ struct hx_ctx {
   std::vector<StepGraph> graphs;
   bool step_warm = false;
   cudaStream_t gstream = nullptr, gstream2 = nullptr;
+  // single-GPU step graphs: external events marking x' and e' complete inside the graph, so
+  // hx_step_host reads them back on its copy stream (created on first use) while stage 2 runs
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_x = nullptr, ev_e = nullptr;
+  double* early_xh = nullptr;  // hx_step_host: host x', e' read back early (null: off)
+  double* early_eh = nullptr;
+  bool early_done = false;     // the last graph launch queued those reads
   double* t_dev = nullptr;
   double* h_t = nullptr;
   // host-buffer entry scratch (device state)
@@ -797,6 +804,8 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   ok &= cudaMallocHost((void**)&ctx->h_t, 2 * sizeof(double)) == cudaSuccess;
   ok &= cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking) == cudaSuccess;
   ok &= cudaStreamCreateWithFlags(&ctx->gstream2, cudaStreamNonBlocking) == cudaSuccess;
+  for (cudaEvent_t* ev : {&ctx->ev_x, &ctx->ev_e})
+    ok &= cudaEventCreateWithFlags(ev, cudaEventDisableTiming) == cudaSuccess;
   ok &= dalloc(&ctx->st, 4) == cudaSuccess;
   ok &= dalloc(&ctx->dt, 2) == cudaSuccess;
   ok &= dalloc(&ctx->scal, 16) == cudaSuccess;
@@ -880,6 +889,9 @@ extern "C" int hx_destroy(hx_ctx* ctx) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
   if (ctx->gstream2) cudaStreamDestroy(ctx->gstream2);
+  if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
+  for (cudaEvent_t ev : {ctx->ev_x, ctx->ev_e})
+    if (ev) cudaEventDestroy(ev);
   for (auto& e : ctx->prof_ev) cudaEventDestroy(e);
   if (ctx->mailbox) cudaFree(ctx->mailbox);
   if (ctx->peer_plan) cudaFree(ctx->peer_plan);
@@ -2277,11 +2289,17 @@ static void l2_window(hx_ctx* ctx, cudaStream_t s) {
 
 static bool same_params(const hx_params& a, const hx_params& b) { return memcmp(&a, &b, sizeof a) == 0; }
 
+static int g_early = -1;  // HX_EARLY=0: the serial step graph (x', e', validity at the end)
+
 static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, const double* x, const double* v,
                         const double* e, double* x_out, double* v_out, double* e_out, cudaGraphExec_t* exec,
                         hx_ctx::GProf* gprof = nullptr) {
   const long long nv = ctx->nn * ctx->dim, nte = ctx->ne * ctx->nt;
   const unsigned ga = gblocks((std::max(nv, nte) + 1) / 2, 256);  // 2 entries per thread
+  if (g_early < 0) {
+    const char* ge = getenv("HX_EARLY");
+    g_early = (ge && ge[0] == '0') ? 0 : 1;
+  }
   cudaStream_t user = ctx->stream;
   const bool prof = ctx->prof_on;
   const long long launches = ctx->launches;
@@ -2317,14 +2335,29 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
     DtArgs da{ctx->st + 0, ctx->dt, prm->cfl, prm->dt_max, prm->t_final, 0.0, dt_fixed, 0, ctx->t_dev};
     k_dt<<<1, 1, 0, ctx->stream>>>(da);
     CKL();
+    // single GPU: x' = x + dt v_half is known as soon as v_half is, and e' = e + dt de1 after
+    // stage 2's rates, so both are written early; external events mark them for the host
+    // read-back of hx_step_host, which then overlaps stage 2.  (A side branch running the
+    // validity check of x' concurrently with stage 2 measured neutral and costs two more
+    // streams per context, so the check stays at the end.)
+    const bool early = !ctx->peer && g_early != 0;
     AxpyArgs m{x, v, e, v, ctx->dv0, ctx->de0, ctx->xm, ctx->vm, ctx->em, ctx->dt + 1, 0.5, nv, nte};
+    if (early) m.xf = x_out;
     prof_begin(ctx, K_AXPY);
     k_axpy_state<<<ga, 256, 0, ctx->stream>>>(m);
     prof_end(ctx);
     CKL();
+    cudaStream_t main_s = ctx->stream;
+    if (early) CK(cudaEventRecordWithFlags(ctx->ev_x, main_s, cudaEventRecordExternal));
     // stage 2: rates(mid)
     r = rates_launch(ctx, prm, ctx->xm, ctx->vm, ctx->em, ctx->de1, ctx->st + 1);
     if (r) return r;
+    if (early) {
+      AxpyArgs ee{x, v, e, nullptr, nullptr, ctx->de1, nullptr, nullptr, e_out, ctx->dt + 1, 1.0, 0, nte};
+      k_axpy_state<<<gblocks((nte + 1) / 2, 256), 256, 0, ctx->stream>>>(ee);
+      CKL();
+      CK(cudaEventRecordWithFlags(ctx->ev_e, main_s, cudaEventRecordExternal));
+    }
     ctx->prof_tag_stage = 1;
     CGLaunch L1;
     r = cg_prepare(ctx, ctx->cg + 1, ctx->Dm, nullptr, ctx->evec, 1, mask, ctx->invd, prm->rel_tol,
@@ -2333,7 +2366,8 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
     r = cg_capture(ctx, L1, ctx->last_iters[1]);
     if (r) return r;
     ctx->prof_tag_stage = -1;
-    AxpyArgs n{x, v, e, ctx->vm, ctx->dv1, ctx->de1, x_out, v_out, e_out, ctx->dt + 1, 1.0, nv, nte};
+    AxpyArgs n{x, v, e, ctx->vm, ctx->dv1, ctx->de1, early ? nullptr : x_out, v_out, early ? nullptr : e_out,
+               ctx->dt + 1, 1.0, nv, early ? 0 : nte};
     prof_begin(ctx, K_AXPY);
     k_axpy_state<<<ga, 256, 0, ctx->stream>>>(n);
     prof_end(ctx);
@@ -2376,6 +2410,7 @@ static int g_use_graph = -1;  // HX_GRAPH=0 disables the graph path
 
 // the context's own state buffers (host-buffer entry hx_step_host, staged steps)
 static int ensure_stage(hx_ctx* ctx) {
+  if (!ctx->cstream) CK(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
   if (ctx->hx_x) return HX_OK;
   const size_t nvb = sizeof(double) * ctx->nn * ctx->dim, neb = sizeof(double) * ctx->ne * ctx->nt;
   CK(cudaMalloc(&ctx->hx_x, nvb));
@@ -2458,6 +2493,17 @@ static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_
   ctx->h_t[1] = dt_fixed;
   CK(cudaMemcpyAsync(ctx->t_dev, ctx->h_t, 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaGraphLaunch(sg->exec, ctx->stream));
+  ctx->early_done = false;
+  if (ctx->early_xh && !ctx->peer && g_early == 1) {
+    // hx_step_host: read x' and e' back while stage 2 still runs (the graph's external
+    // events mark them written); a retried step rewrites them and is read again after
+    const size_t nvb = sizeof(double) * ctx->nn * ctx->dim, neb = sizeof(double) * ctx->ne * ctx->nt;
+    CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_x, 0));
+    CK(cudaMemcpyAsync(ctx->early_xh, x_out, nvb, cudaMemcpyDeviceToHost, ctx->cstream));
+    CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_e, 0));
+    CK(cudaMemcpyAsync(ctx->early_eh, e_out, neb, cudaMemcpyDeviceToHost, ctx->cstream));
+    ctx->early_done = true;
+  }
   CK(cudaStreamSynchronize(ctx->stream));
   {
     const int prc = peer_check(ctx);  // before the status: a timed-out status exchange reads as an inversion
@@ -2562,11 +2608,32 @@ extern "C" int hx_step_host(hx_ctx* ctx, const hx_params* prm, double t, double*
   CK(cudaMemcpyAsync(ctx->hx_x, x_host, nvb, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->hx_v, v_host, nvb, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->hx_e, e_host, neb, cudaMemcpyHostToDevice, ctx->stream));
-  int rc = hx_step(ctx, prm, t, ctx->hx_x, ctx->hx_v, ctx->hx_e, ctx->hx_xo, ctx->hx_vo, ctx->hx_eo, info);
-  if (rc) return rc;
-  CK(cudaMemcpyAsync(x_host, ctx->hx_xo, nvb, cudaMemcpyDeviceToHost, ctx->stream));
+  // x' and e' may be read back by the step itself while its stage 2 runs (step_dispatch)
+  ctx->early_xh = x_host;
+  ctx->early_eh = e_host;
+  ctx->early_done = false;
+  hx_step_info local{};
+  hx_step_info* inf = info ? info : &local;
+  int rc = hx_step(ctx, prm, t, ctx->hx_x, ctx->hx_v, ctx->hx_e, ctx->hx_xo, ctx->hx_vo, ctx->hx_eo, inf);
+  ctx->early_xh = ctx->early_eh = nullptr;
+  const bool early = ctx->early_done && inf->retries == 0;
+  CK(cudaStreamSynchronize(ctx->cstream));
+  if (rc) {
+#ifdef HX_DEBUG_EARLY
+    fprintf(stderr, "hx_step_host rc=%d early_done=%d\n", rc, (int)ctx->early_done);
+#endif
+    if (ctx->early_done) {  // a failed step leaves the caller's state as it was
+      CK(cudaMemcpyAsync(x_host, ctx->hx_x, nvb, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaMemcpyAsync(e_host, ctx->hx_e, neb, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return rc;
+  }
+  if (!early) {
+    CK(cudaMemcpyAsync(x_host, ctx->hx_xo, nvb, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(e_host, ctx->hx_eo, neb, cudaMemcpyDeviceToHost, ctx->stream));
+  }
   CK(cudaMemcpyAsync(v_host, ctx->hx_vo, nvb, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(e_host, ctx->hx_eo, neb, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return HX_OK;
 }

@@ -1521,6 +1521,9 @@ struct AxpyArgs {
   double scale;        // 0.5 (midpoint) or 1.0
   long long nv;        // NN*d
   long long nte;       // NE*nt
+  double* xf;          // midpoint launch only, or null: the step's final x = x + dt v_half (the
+                       // reference's S + dt r1 position, hydro.py:392-396), computed as soon as
+                       // v_half exists so the rest of the step can overlap its use
 };
 
 // y = a + h*b on pairs of entries (16-byte accesses when every array is 16-byte aligned)
@@ -1545,10 +1548,14 @@ __global__ void __launch_bounds__(256) k_axpy_state(AxpyArgs a) {
                      reinterpret_cast<unsigned long long>(a.xo) | reinterpret_cast<unsigned long long>(a.vo) |
                      reinterpret_cast<unsigned long long>(a.eo)) & 15ull) == 0;
   if (i < a.nv) {
-    axpy2(a.x, a.dxs, a.xo, h, i, a.nv, vec);
-    axpy2(a.v, a.dv, a.vo, h, i, a.nv, vec);
+    if (a.xo) axpy2(a.x, a.dxs, a.xo, h, i, a.nv, vec);
+    if (a.vo) axpy2(a.v, a.dv, a.vo, h, i, a.nv, vec);
+    if (a.xf) {  // x + dt * v_half from the just-rounded v_half
+      const double dt = *a.dtp;
+      for (long long j = i; j < a.nv && j < i + 2; ++j) a.xf[j] = __dadd_rn(a.x[j], __dmul_rn(dt, a.vo[j]));
+    }
   }
-  if (i < a.nte) axpy2(a.e, a.de, a.eo, h, i, a.nte, vec);
+  if (i < a.nte && a.eo) axpy2(a.e, a.de, a.eo, h, i, a.nte, vec);
 }
 
 // dt = min(cfl*ratio, dt_max, t_final - t) / 2^retry  (timestep_estimate hydro.py:364-373)

@@ -5,6 +5,7 @@ the loop.  The distributed solution must match the single-domain device solve of
 same system (same iteration count; 1e-8 and the true residual on a random right-hand side), and interface nodes must be bit-identical
 on both ranks."""
 
+import gc
 import threading
 
 import numpy as np
@@ -64,6 +65,12 @@ def _solve_all(ranks):
     buffers, and all threads start the CG together."""
     out, errs = [None] * len(ranks), []
     bar = threading.Barrier(len(ranks))
+    # no device frees while the ranks spin on each other either: a garbage-collected context of
+    # an earlier test would run cudaFree (a device-wide synchronisation) in the middle of the
+    # exchange, so collect first and keep the collector off during the solve
+    gc.collect()
+    torch.cuda.synchronize()
+    gc.disable()
 
     def work(i):
         try:
@@ -84,10 +91,13 @@ def _solve_all(ranks):
             bar.abort()
 
     th = [threading.Thread(target=work, args=(i,)) for i in range(len(ranks))]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join()
+    try:
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+    finally:
+        gc.enable()
     if errs:
         raise errs[0]
     return [(H(x), it) for x, it in out]
