@@ -124,9 +124,10 @@ struct hx_ctx {
   // single-GPU step graphs: external events marking x' and e' complete inside the graph, so
   // hx_step_host reads them back on its copy stream (created on first use) while stage 2 runs
   cudaStream_t cstream = nullptr;
-  cudaEvent_t ev_x = nullptr, ev_e = nullptr;
+  cudaEvent_t ev_x = nullptr, ev_e = nullptr, ev_v = nullptr;
   double* early_xh = nullptr;  // hx_step_host: host x', e' read back early (null: off)
   double* early_eh = nullptr;
+  double* early_vh = nullptr;
   bool early_done = false;     // the last graph launch queued those reads
   double* t_dev = nullptr;
   double* h_t = nullptr;
@@ -804,7 +805,7 @@ extern "C" int hx_create(const hx_mesh_desc* d, hx_ctx** out) {
   ok &= cudaMallocHost((void**)&ctx->h_t, 2 * sizeof(double)) == cudaSuccess;
   ok &= cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking) == cudaSuccess;
   ok &= cudaStreamCreateWithFlags(&ctx->gstream2, cudaStreamNonBlocking) == cudaSuccess;
-  for (cudaEvent_t* ev : {&ctx->ev_x, &ctx->ev_e})
+  for (cudaEvent_t* ev : {&ctx->ev_x, &ctx->ev_e, &ctx->ev_v})
     ok &= cudaEventCreateWithFlags(ev, cudaEventDisableTiming) == cudaSuccess;
   ok &= dalloc(&ctx->st, 4) == cudaSuccess;
   ok &= dalloc(&ctx->dt, 2) == cudaSuccess;
@@ -890,7 +891,7 @@ extern "C" int hx_destroy(hx_ctx* ctx) {
   if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
   if (ctx->gstream2) cudaStreamDestroy(ctx->gstream2);
   if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
-  for (cudaEvent_t ev : {ctx->ev_x, ctx->ev_e})
+  for (cudaEvent_t ev : {ctx->ev_x, ctx->ev_e, ctx->ev_v})
     if (ev) cudaEventDestroy(ev);
   for (auto& e : ctx->prof_ev) cudaEventDestroy(e);
   if (ctx->mailbox) cudaFree(ctx->mailbox);
@@ -2372,6 +2373,7 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
     k_axpy_state<<<ga, 256, 0, ctx->stream>>>(n);
     prof_end(ctx);
     CKL();
+    if (early) CK(cudaEventRecordWithFlags(ctx->ev_v, main_s, cudaEventRecordExternal));  // v' read back during the check
     // validity of the new geometry
     r = validity_launch(ctx, x_out, ctx->st + 2);
     if (r) return r;
@@ -2502,6 +2504,8 @@ static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_
     CK(cudaMemcpyAsync(ctx->early_xh, x_out, nvb, cudaMemcpyDeviceToHost, ctx->cstream));
     CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_e, 0));
     CK(cudaMemcpyAsync(ctx->early_eh, e_out, neb, cudaMemcpyDeviceToHost, ctx->cstream));
+    CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_v, 0));
+    CK(cudaMemcpyAsync(ctx->early_vh, v_out, nvb, cudaMemcpyDeviceToHost, ctx->cstream));
     ctx->early_done = true;
   }
   CK(cudaStreamSynchronize(ctx->stream));
@@ -2611,11 +2615,12 @@ extern "C" int hx_step_host(hx_ctx* ctx, const hx_params* prm, double t, double*
   // x' and e' may be read back by the step itself while its stage 2 runs (step_dispatch)
   ctx->early_xh = x_host;
   ctx->early_eh = e_host;
+  ctx->early_vh = v_host;
   ctx->early_done = false;
   hx_step_info local{};
   hx_step_info* inf = info ? info : &local;
   int rc = hx_step(ctx, prm, t, ctx->hx_x, ctx->hx_v, ctx->hx_e, ctx->hx_xo, ctx->hx_vo, ctx->hx_eo, inf);
-  ctx->early_xh = ctx->early_eh = nullptr;
+  ctx->early_xh = ctx->early_eh = ctx->early_vh = nullptr;
   const bool early = ctx->early_done && inf->retries == 0;
   CK(cudaStreamSynchronize(ctx->cstream));
   if (rc) {
@@ -2624,6 +2629,7 @@ extern "C" int hx_step_host(hx_ctx* ctx, const hx_params* prm, double t, double*
 #endif
     if (ctx->early_done) {  // a failed step leaves the caller's state as it was
       CK(cudaMemcpyAsync(x_host, ctx->hx_x, nvb, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaMemcpyAsync(v_host, ctx->hx_v, nvb, cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaMemcpyAsync(e_host, ctx->hx_e, neb, cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
     }
@@ -2631,10 +2637,10 @@ extern "C" int hx_step_host(hx_ctx* ctx, const hx_params* prm, double t, double*
   }
   if (!early) {
     CK(cudaMemcpyAsync(x_host, ctx->hx_xo, nvb, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(v_host, ctx->hx_vo, nvb, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(e_host, ctx->hx_eo, neb, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
   }
-  CK(cudaMemcpyAsync(v_host, ctx->hx_vo, nvb, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
   return HX_OK;
 }
 
