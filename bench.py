@@ -756,7 +756,14 @@ def main():
         lib.hx_prof_enable(h, 0)
         return tot, out
 
+    # two replays, per kernel class the lower average (a replay occasionally runs all the
+    # memory-bound launches ~1.5x slower; the timed region above is not affected)
     ev_ms, ev_times = replay_events()
+    ev_ms2, ev_times2 = replay_events()
+    for name, (t2, c2) in ev_times2.items():
+        if name not in ev_times or (c2 and t2 / c2 < ev_times[name][0] / max(ev_times[name][1], 1)):
+            ev_times[name] = (t2, c2)
+    ev_ms = min(ev_ms, ev_ms2)
     ktimes_dup = {}
     prof_base = None
     if args.ktime in ("dup", "both"):
@@ -905,9 +912,9 @@ def main():
                  "ms_per_step_plain_replay": prof_ms / args.steps}
     else:
         kpass = {"method": "events",
-                 "note": "the same timed steps replayed from the post-warm-up snapshot as plain stream launches; "
-                         "the library records a CUDA event pair on the launching stream around every launch; "
-                         "share = class time / replay step time",
+                 "note": "the same timed steps replayed (twice) from the post-warm-up snapshot as plain stream "
+                         "launches; the library records a CUDA event pair on the launching stream around every "
+                         "launch; per class the replay with the lower average; share = class time / replay step time",
                  "ms_per_step_replay": prof_ms / args.steps}
         if ktimes_dup:
             kpass["graph_dup_avg_us"] = {k: 1e3 * t / c for k, (t, c) in ktimes_dup.items()}
