@@ -163,6 +163,9 @@ struct CsrSum {
 #ifndef MASS_ALIAS
 #define MASS_ALIAS 1
 #endif
+#ifndef MASS_ALIAS_PMIN
+#define MASS_ALIAS_PMIN 3
+#endif
 #ifndef MASS_LD
 #define MASS_LD __ldcg
 #endif
@@ -190,7 +193,7 @@ struct MassBrickCfg {
   // MASS_ALIAS (p >= 3, measured faster; p = 2 keeps separate images): the gather /
   // staging planes live inside the T planes -- each plane thread reads its own plane into
   // registers before it overwrites it (phases 1 and 3), so one image suffices
-  static constexpr bool ALIAS = MASS_ALIAS && P >= 3;
+  static constexpr bool ALIAS = MASS_ALIAS && P >= MASS_ALIAS_PMIN;
   static constexpr int GP = ALIAS ? QQ : DD + 1;  // plane pitch of the gather / staging image
   static constexpr int GS = PLN * GP;             // gather doubles per element
   static constexpr int TS = PLN * QQ;             // T image doubles per element
