@@ -346,3 +346,32 @@ def test_inverted_element_reported(dim):
         compute_geometric_factors(mesh, gauss_legendre(3), x=x)
     assert err.value.element == mesh.num_elements - 1
     assert "<= 0" in str(err.value)
+
+
+@pytest.mark.parametrize("order", [2, 3])
+def test_timestep_estimate_reports_first_inverted_point(order):
+    """timestep_estimate on an inverted mesh raises InvertedElementError naming the same first
+    (q-major) point as compute_geometric_factors (hydro.py:364-367 -> fespace.py:340-344), and
+    otherwise returns the ratio the reference pair (geometry + stress_qdata) gives -- the fused
+    3D ratio launch (hx_timestep_ratio) against the device geometry + stress kernels."""
+    from paper_2112_07075_b200.fespace import InvertedElementError, compute_geometric_factors
+    from paper_2112_07075_b200.hydro import StepControls
+
+    hy = _hydro(3, (3, 3, 2), order=order)
+    st = _uniform(hy, e=1.0, vfn=_vortex(3))
+    hy.begin_phase(st)
+    ctl = StepControls(cfl=0.3, dt_max=1.0, t_final=10.0)
+    dt = hy.timestep_estimate(st, ctl)
+    _, ratio = hy.stress_qdata(st, compute_geometric_factors(hy.mesh, hy.quad, x=st.x))
+    ref_dt = min(ctl.cfl * ratio, ctl.dt_max, ctl.t_final - st.t)
+    assert abs(dt - ref_dt) <= 1e-14 * ref_dt  # (cbrt vs the stress kernel's h: an ulp at most)
+    bad = st.x.copy()
+    dm = hy.mesh.node_dofmap
+    e0 = 7
+    bad[dm[-1, e0]] = bad[dm[0, e0]] - 0.01  # fold the element's last corner past its first
+    with pytest.raises(InvertedElementError) as ref:
+        compute_geometric_factors(hy.mesh, hy.quad, x=bad)
+    st.x = bad
+    with pytest.raises(InvertedElementError) as got:
+        hy.timestep_estimate(st, ctl)
+    assert (got.value.element, got.value.point) == (ref.value.element, ref.value.point)
