@@ -172,6 +172,9 @@ struct CsrSum {
 #ifndef MASS_CMAJOR
 #define MASS_CMAJOR 0
 #endif
+#ifndef MASS_P3COL
+#define MASS_P3COL 0
+#endif
 #ifndef MASS_EBREG
 #define MASS_EBREG 1  // measured 603 vs 592 Mdof*steps/s (mass 24.3 vs 25.6 us)
 #endif
@@ -421,6 +424,39 @@ __global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : MASS_BRICK_MINB) 
     }
     __syncthreads();
     // ---- phase 3 (planes): y^T, x^T -> staging image (same layout as the gather image)
+#if MASS_P3COL
+    // column by column (qx): y^T of the column, then its x^T contribution accumulated into the
+    // 16 outputs -- the same ascending sums as below (so bit-identical), with 25 instead of 45
+    // doubles live
+    if (pact) {
+      const double* T = sT + pe * M::TS + pr * QQ;
+      double o3[D1][D1];
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < D1; ++dx) o3[dy][dx] = 0.0;
+#pragma unroll
+      for (int qx = 0; qx < Q; ++qx) {
+        double tq[Q];
+#pragma unroll
+        for (int qy = 0; qy < Q; ++qy) tq[qy] = T[qy * Q + qx];
+#pragma unroll
+        for (int dy = 0; dy < D1; ++dy) {
+          double v = 0.0;
+#pragma unroll
+          for (int qy = 0; qy < Q; ++qy) v = fma(cB[qy * D1 + dy], tq[qy], v);
+#pragma unroll
+          for (int dx = 0; dx < D1; ++dx) o3[dy][dx] = fma(cB[qx * D1 + dx], v, o3[dy][dx]);
+        }
+      }
+      double* o = sG + pe * GS + pr * GP;
+#pragma unroll
+      for (int dy = 0; dy < D1; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < D1; ++dx) o[dy * D1 + dx] = o3[dy][dx];
+    }
+    if (false)
+#endif
     if (pact) {
       const double* T = sT + pe * M::TS + pr * QQ;
       double Tq[QQ];
