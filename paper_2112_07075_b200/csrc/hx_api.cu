@@ -1469,7 +1469,7 @@ static int peer_halo(hx_ctx* ctx, CGLaunch& L) {
   if (ctx->pd.nsh == 0) return HX_OK;  // no neighbours: nothing to send
   const unsigned gp = capg(std::max(1u, std::min<unsigned>(gblocks((long long)ctx->pd.nsh * L.nc, 256), 592)));
   int rc = with_node_sum(ctx, L.nc, ctx->evec, [&](auto sum, auto ncc) {
-    k_halo_pack<decltype(ncc)::value><<<gp, 256, 0, ctx->stream>>>(ctx->pd, L.na.cg, sum);
+    k_halo_pack<decltype(ncc)::value><<<gp, 256, 0, ctx->stream>>>(ctx->pd, L.na.cg, sum, ctx->pl);
     return HX_OK;
   });
   if (rc) return rc;
@@ -1482,7 +1482,7 @@ static int peer_evec_halo(hx_ctx* ctx, double* evec, int nc) {
   const unsigned gp = capg(std::max(1u, std::min<unsigned>(gblocks((long long)ctx->pd.nsh * nc, 256), 592)));
   const unsigned gc = capg(std::max(1u, std::min<unsigned>(gblocks((long long)ctx->pd.nh * nc, 256), 592)));
   int rc = with_node_sum(ctx, nc, evec, [&](auto sum, auto ncc) {
-    k_halo_pack<decltype(ncc)::value><<<gp, 256, 0, ctx->stream>>>(ctx->pd, nullptr, sum);
+    k_halo_pack<decltype(ncc)::value><<<gp, 256, 0, ctx->stream>>>(ctx->pd, nullptr, sum, ctx->pl);
     return HX_OK;
   });
   if (rc) return rc;
@@ -2024,7 +2024,7 @@ extern "C" int hx_phase_begin(hx_ctx* ctx, const double* x, const double* qdata0
   if (ctx->peer) {  // multi-GPU: interface sums of the assembled diagonal
     const unsigned gp = capg(std::max(1u, std::min<unsigned>(gblocks(ctx->pd.nsh, 256), 592)));
     const unsigned gc = capg(std::max(1u, std::min<unsigned>(gblocks(ctx->pd.nh, 256), 592)));
-    k_halo_pack<1><<<gp, 256, 0, ctx->stream>>>(ctx->pd, nullptr, NodeVec<1>{ctx->mdiag});
+    k_halo_pack<1><<<gp, 256, 0, ctx->stream>>>(ctx->pd, nullptr, NodeVec<1>{ctx->mdiag}, ctx->pl);
     CKL();
     rc = peer_sync<0>(ctx, nullptr, nullptr, nullptr);
     if (rc) return rc;
@@ -2791,9 +2791,21 @@ extern "C" int hx_peer_connect(hx_ctx* ctx, void* const* mailboxes) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
   ctx->graphs.clear();
   ctx->step_warm = false;
+  // HX_PEER_POST=1: the CG's world scalars posted by their producer launches (PeerLite::post).
+  // Opt-in: on the one-rank proxy the producers' last-CTA tail (740 arrivals on one counter,
+  // then the reduction) costs more than the consumer-side handshake it replaces (2.23 vs 2.11
+  // ms/step, profiles/r2/r2g_variants.md); the opt-in mass-kernel variants never post
+  auto envon = [](const char* n) {
+    const char* v = getenv(n);
+    return v && v[0] && v[0] != '0';
+  };
+  int post = 0;
+  if (envon("HX_PEER_POST") && !envon("HX_MASS_TMA") && !envon("HX_MASS_W2") && !MASS_PIPE && ctx->brick &&
+      ctx->elem_major)
+    post = PEER_POST_ON | (ctx->pd.nsh == 0 ? PEER_POST_MASS : 0);
   ctx->pl = PeerLite{ctx->mailbox, reinterpret_cast<double* const*>(reinterpret_cast<char*>(ctx->pd_dev) +
                                                                      offsetof(PeerDev, mb)),
-                     ctx->peer_ctr, ctx->pd.rank, ctx->pd.nranks};
+                     ctx->peer_ctr, ctx->pd.rank, ctx->pd.nranks, post};
   ctx->peer = true;
   return HX_OK;
 }

@@ -512,6 +512,10 @@ __global__ void __launch_bounds__(MASS_BRICK_NT, (P >= 4 ? 4 : MASS_BRICK_MINB) 
     __syncthreads();
   }
   cg_partial(a.partials, &a.cg->nparts_m, block_sum<M::NT>(acc, red));
+  if constexpr (PEER) {  // a rank without neighbours posts p.Ap_k here (else the halo pack does)
+    if ((a.pl.post & (PEER_POST_ON | PEER_POST_MASS)) == (PEER_POST_ON | PEER_POST_MASS))
+      cg_post_last<M::NT>(a.pl, a.partials, gridDim.x, &a.cg->cnt[3], a.cg->seq0 + 2ull * k, red);
+  }
 }
 
 

@@ -365,7 +365,14 @@ struct PeerLite {
   double* const* mbs;       // every rank's mailbox (device array)
   unsigned long long* seq;  // exchange counter
   int rank, nranks;
+  int post;                 // PEER_POST_*: the CG's world scalars posted by their producer launch
 };
+// producer-side posting of the CG's per-iteration world scalars (r.z_k by the node launch,
+// p.Ap_k by the halo pack launch, or by the mass launch on a rank without neighbours): the
+// last CTA of the producer to finish reduces the per-CTA partials and posts this rank's value
+// to every rank, so the consumer launch's CTAs only poll flags that are usually already set
+// (the post overlaps the launch gap instead of the consumer's prologue)
+constexpr int PEER_POST_ON = 1, PEER_POST_MASS = 2;
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -536,7 +543,82 @@ __device__ __forceinline__ bool peer_world(const PeerLite& pl, unsigned long lon
   return wok != 0;
 }
 __device__ __forceinline__ PeerLite peer_lite(const PeerDev* pd) {
-  return PeerLite{pd->mb[pd->rank], pd->mb, pd->seq, pd->rank, pd->nranks};
+  return PeerLite{pd->mb[pd->rank], pd->mb, pd->seq, pd->rank, pd->nranks, 0};
+}
+
+// fixed-order sum of n grid partials, broadcast to every thread of the CTA
+template <int NT>
+__device__ __forceinline__ double reduce_bcast(const double* parts, int n, double* red) {
+  __shared__ double bc;
+  const double v = reduce_partials<NT>(parts, n, red);
+  if (threadIdx.x == 0) bc = v;
+  __syncthreads();
+  return bc;
+}
+
+// world sum of NV values posted by the ranks' producer launches (cg_post_last): every CTA
+// polls the ranks' flags (relaxed, then one acquire per flag) and sums the slots in ascending
+// rank order, this rank's own included.  False on a peer timeout.
+template <int NV>
+__device__ __forceinline__ bool peer_recv(const PeerLite& pl, unsigned long long seq, double (&v)[NV]) {
+  __shared__ double wv[NV];
+  __shared__ int wok;
+  if (threadIdx.x == 0) {
+    const int par = (int)(seq & 1);
+    int ok = 1;
+    for (int q = 0; q < pl.nranks && ok; ++q) {
+      unsigned long long spins = 0;
+      const unsigned long long* f = mb_flag(pl.me, q);
+      while (ld_relaxed_sys(f) < seq) {
+        if (spins >= PEER_WORLD_PURE) __nanosleep(32);
+        if (++spins > PEER_SPIN_LIMIT) {
+          ok = 0;
+          break;
+        }
+      }
+      if (ok) (void)ld_acquire_sys(f);
+    }
+    if (ok) {
+      const double* s = pl.me + MB_SLOT + par * HX_MAXR * SLOTW;
+#pragma unroll
+      for (int t = 0; t < NV; ++t) {
+        double tot = 0.0;
+        for (int q = 0; q < pl.nranks; ++q) tot += __ldcg(s + q * SLOTW + t);
+        wv[t] = tot;
+      }
+    }
+    wok = ok;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < NV; ++t) v[t] = wv[t];
+  return wok != 0;
+}
+
+// end of a producer launch: every CTA has written its partial (and, for the halo pack, its
+// system-fenced halo entries); the last CTA to arrive reduces the partials in the same fixed
+// order the consumers used to (reduce_bcast) and posts the rank's value with seq to every
+// rank's slot, then resets the arrival counter for the next launch.
+template <int NT>
+__device__ __forceinline__ void cg_post_last(const PeerLite& pl, const double* parts, int nparts, unsigned* counter,
+                                             unsigned long long seq, double* red) {
+  __shared__ int is_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  const double v = reduce_bcast<NT>(parts, nparts, red);
+  if (threadIdx.x == 0) {
+    *counter = 0u;
+    const int par = (int)(seq & 1);
+    for (int q = 0; q < pl.nranks; ++q) pl.mbs[q][MB_SLOT + (par * HX_MAXR + pl.rank) * SLOTW] = v;
+    for (int q = 0; q < pl.nranks; ++q) st_release_sys(mb_flag(pl.mbs[q], pl.rank), seq);
+    *pl.seq = seq;
+  }
 }
 
 // interface node sum (multi-GPU): the sharers' partials in ascending rank order from 0.0,
@@ -593,15 +675,6 @@ __device__ __forceinline__ void cg_publish(const CGDev* g) {
   if (g->use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)g->cond, g->active ? 1u : 0u);
 }
 
-// fixed-order sum of n grid partials, broadcast to every thread of the CTA
-template <int NT>
-__device__ __forceinline__ double reduce_bcast(const double* parts, int n, double* red) {
-  __shared__ double bc;
-  const double v = reduce_partials<NT>(parts, n, red);
-  if (threadIdx.x == 0) bc = v;
-  __syncthreads();
-  return bc;
-}
 
 // mass-launch prologue of iteration k = it_m: for k >= 2 finish N(k-1)'s r.z
 // reduction, stop test (operators.py:361-362) and beta_k = rz_{k-1}/rz_{k-2}.
@@ -659,10 +732,14 @@ __device__ __forceinline__ bool cg_mass_begin(CGDev* g, double* red, double& bet
     beta = 0.0;
     return !(none || maxed);
   }
-  double rzk = reduce_bcast<NT>(g->parts_n, g->nparts_n, red);
+  double rzk = 0.0;
+  const bool posted = PEER && g->peer && pl && (pl->post & PEER_POST_ON);
+  if (!posted) rzk = reduce_bcast<NT>(g->parts_n, g->nparts_n, red);
   if (PEER && g->peer) {  // world r.z_{k-1}
     double w[1] = {rzk};
-    if (!peer_world<1>(pl ? *pl : peer_lite(g->peer), g->seq0 + 2ull * k - 1, w)) {
+    const bool okw = posted ? peer_recv<1>(*pl, g->seq0 + 2ull * k - 1, w)
+                            : peer_world<1>(pl ? *pl : peer_lite(g->peer), g->seq0 + 2ull * k - 1, w);
+    if (!okw) {
       if (threadIdx.x == 0) {  // any block that timed out stops the CG (same values from every block)
         g->code = 6;
         g->active = 0;
@@ -703,10 +780,14 @@ __device__ __forceinline__ bool cg_node_begin(CGDev* g, double* red, double& alp
                                               const PeerLite* pl = nullptr) {
   if (!g->active) return false;
   k = g->it_n;
-  double pAp = reduce_bcast<NT>(g->parts_m, g->nparts_m, red);
+  double pAp = 0.0;
+  const bool posted = PEER && g->peer && pl && (pl->post & PEER_POST_ON);
+  if (!posted) pAp = reduce_bcast<NT>(g->parts_m, g->nparts_m, red);
   if (PEER && g->peer) {  // world p.Ap_k; the flag also publishes this rank's halo (k_halo_pack)
     double w[1] = {pAp};
-    if (!peer_world<1>(pl ? *pl : peer_lite(g->peer), g->seq0 + 2ull * k, w)) {
+    const bool okw = posted ? peer_recv<1>(*pl, g->seq0 + 2ull * k, w)
+                            : peer_world<1>(pl ? *pl : peer_lite(g->peer), g->seq0 + 2ull * k, w);
+    if (!okw) {
       if (threadIdx.x == 0) {  // any block that timed out stops the CG (same values from every block)
         g->code = 6;
         g->active = 0;
@@ -1351,6 +1432,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_init(NodeArgs a, SUM sum) {
       g->use_cond = a.use_cond;
       g->peer = a.peer;
       g->seq0 = a.peer ? *a.peer->seq : 0ull;
+      g->cnt[2] = g->cnt[3] = 0u;  // producer-post arrival counters
       g->active = 1;
     }
   }
@@ -1490,6 +1572,9 @@ __global__ void __launch_bounds__(256, PEER ? NODE_PEER_MINB : NODE_MINB) k_cg_n
     }
   }
   cg_partial(a.partials, &g->nparts_n, block_sum<256>(rz, red));
+  if constexpr (PEER) {  // post this rank's r.z_k (consumed by M(k+1)'s prologue)
+    if (a.pl.post & PEER_POST_ON) cg_post_last<256>(a.pl, a.partials, gridDim.x, &g->cnt[2], g->seq0 + 2ull * kk + 1, red);
+  }
 }
 
 // CG epilogue: apply the x update of a final odd iteration (x_k = x_{k-1} + a_k p_k;

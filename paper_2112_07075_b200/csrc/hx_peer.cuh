@@ -129,7 +129,8 @@ struct NodeVec {
 // halo, part 1: this rank's node sums at the nodes it shares, stored into each
 // neighbour's recv block (published by the following k_peer_sync)
 template <int NC, class SUM>
-__global__ void __launch_bounds__(256) k_halo_pack(PeerDev pd, const CGDev* g, SUM sum) {
+__global__ void __launch_bounds__(256) k_halo_pack(PeerDev pd, CGDev* g, SUM sum, PeerLite pl) {
+  __shared__ double red[32];
   if (g && !g->active) return;
   const long long N = (long long)pd.nsh * NC;
   bool wrote = false;
@@ -140,6 +141,8 @@ __global__ void __launch_bounds__(256) k_halo_pack(PeerDev pd, const CGDev* g, S
     wrote = true;
   }
   if (wrote) __threadfence_system();
+  // in the CG: post this rank's p.Ap_k behind the halo (the flag publishes both)
+  if (g && (pl.post & PEER_POST_ON)) cg_post_last<256>(pl, g->parts_m, g->nparts_m, &g->cnt[3], g->seq0 + 2ull * g->it_n, red);
 }
 
 // halo, part 2 (after the flags): total = sum over the sharers in ascending rank order
