@@ -2624,9 +2624,6 @@ extern "C" int hx_step_host(hx_ctx* ctx, const hx_params* prm, double t, double*
   const bool early = ctx->early_done && inf->retries == 0;
   CK(cudaStreamSynchronize(ctx->cstream));
   if (rc) {
-#ifdef HX_DEBUG_EARLY
-    fprintf(stderr, "hx_step_host rc=%d early_done=%d\n", rc, (int)ctx->early_done);
-#endif
     if (ctx->early_done) {  // a failed step leaves the caller's state as it was
       CK(cudaMemcpyAsync(x_host, ctx->hx_x, nvb, cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaMemcpyAsync(v_host, ctx->hx_v, nvb, cudaMemcpyDeviceToHost, ctx->stream));
