@@ -133,6 +133,18 @@ struct hx_ctx {
   double* h_t = nullptr;
   // host-buffer entry scratch (device state)
   double *hx_x = nullptr, *hx_v = nullptr, *hx_e = nullptr, *hx_xo = nullptr, *hx_vo = nullptr, *hx_eo = nullptr;
+  // hx_step_host streamed inputs (brick, single GPU): x, v, e are copied in z-slabs on the
+  // copy stream, each slab followed by a flag copy (= the call's epoch); the stage-1 rates
+  // kernel waits per pass for the slab its elements need, so the H2D overlaps it
+  unsigned long long* in_flag = nullptr;  // device: [in_ns] slab epochs, [in_ns] required epoch
+  unsigned long long* h_in = nullptr;     // pinned: the epoch values copied
+  unsigned long long* in_err_dev = nullptr;  // device view of h_in[HX_MAX_SLABS] (mapped): wait timed out
+  unsigned long long in_epoch = 0;
+  int in_ns = 0, in_ez = 0;               // slabs, element layers per slab
+  std::vector<long long> in_node_end, in_elem_end;
+  cudaStream_t istream = nullptr;        // the slab copies (own stream: independent of cstream's
+                                        // read-backs, which wait on the step's events)
+  const double *in_xh = nullptr, *in_vh = nullptr, *in_eh = nullptr;  // slabs still to enqueue
   // multi-GPU exchange (hx_peer_*): plan arrays + own mailbox; active once connected
   bool peer = false;
   PeerDev pd{};
@@ -145,6 +157,8 @@ struct hx_ctx {
   PeerLite pl{};                 // prologue essentials passed by value
   int last_iters[2] = {0, 0};    // CG iterations of the last plain step's two solves (graph unroll)
 };
+
+static int issue_inputs(hx_ctx* ctx);
 
 struct hx_mass {
   hx_ctx* ctx;
@@ -373,6 +387,12 @@ struct LaunchRates {
       if (g_rates_kernel == 1) {
         RatesPCArgs a{x, v, e, ctx->qd0, ctx->emap, ctx->elem_major ? nullptr : ctx->slot, ctx->minv, ctx->wnd,
                       ctx->psi1, gamma, q1, q2, ctx->gamma_e, ctx->ne, evec, de, st, ctx->bk, ctx->brick ? 1 : 0};
+        if (mode == 0 && ctx->in_ns > 0 && x == ctx->hx_x && ctx->brick && !ctx->peer) {
+          a.inflag = ctx->in_flag;  // hx_step_host's streamed inputs (a no-op wait otherwise)
+          a.inerr = ctx->in_err_dev;
+          a.in_ez = ctx->in_ez;
+          a.in_ns = ctx->in_ns;
+        }
         // the lean validity kernel is measured faster for p <= 3 (p = 2: 44 vs 51 us,
         // p = 3: 35 vs 40); at p = 4 its images cap it at 2 CTAs/SM and the rates kernel's
         // geometry-only mode wins (54 vs 89 us)
@@ -876,7 +896,8 @@ extern "C" int hx_destroy(hx_ctx* ctx) {
                  ctx->own, ctx->slot, ctx->emapf, ctx->emapf_api, ctx->arena, ctx->evec2, ctx->z, ctx->partials,
                  ctx->hist, ctx->cg,  ctx->st,   ctx->dt,   ctx->scal, ctx->qd0,   ctx->minv, ctx->invdn,
                  ctx->mdiag, ctx->xm, ctx->vm,   ctx->em, ctx->gamma_e,
-                 ctx->de0, ctx->de1, ctx->hx_x, ctx->hx_v, ctx->hx_e, ctx->hx_xo, ctx->hx_vo, ctx->hx_eo};
+                 ctx->de0, ctx->de1, ctx->hx_x, ctx->hx_v, ctx->hx_e, ctx->hx_xo, ctx->hx_vo, ctx->hx_eo,
+                 ctx->in_flag};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_cg) cudaFreeHost(ctx->h_cg);
@@ -885,12 +906,14 @@ extern "C" int hx_destroy(hx_ctx* ctx) {
   if (ctx->dup_scratch) cudaFree(ctx->dup_scratch);
   if (ctx->h_dt) cudaFreeHost(ctx->h_dt);
   if (ctx->h_t) cudaFreeHost(ctx->h_t);
+  if (ctx->h_in) cudaFreeHost(ctx->h_in);
   if (ctx->t_dev) cudaFree(ctx->t_dev);
   for (auto& g : ctx->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
   if (ctx->gstream2) cudaStreamDestroy(ctx->gstream2);
   if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
+  if (ctx->istream) cudaStreamDestroy(ctx->istream);
   for (cudaEvent_t ev : {ctx->ev_x, ctx->ev_e, ctx->ev_v})
     if (ev) cudaEventDestroy(ev);
   for (auto& e : ctx->prof_ev) cudaEventDestroy(e);
@@ -2147,6 +2170,10 @@ static int step_impl(hx_ctx* ctx, const hx_params* prm, double t, double dt_fixe
                      const double* v, const double* e, double* x_out, double* v_out, double* e_out,
                      hx_step_info* info, int attempt0 = 0, const hx_step_info* carry = nullptr) {
   if (!ctx || !prm || !x || !v || !e || !x_out || !v_out || !e_out || !ctx->phase) return HX_EINVAL;
+  {
+    const int irc = issue_inputs(ctx);  // plain launches may sync mid-step: copies first
+    if (irc) return irc;
+  }
   CK(cudaSetDevice(ctx->device));
   const bool estimate = dt_fixed < 0.0;
   hx_step_info out{};
@@ -2495,6 +2522,10 @@ static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_
   ctx->h_t[1] = dt_fixed;
   CK(cudaMemcpyAsync(ctx->t_dev, ctx->h_t, 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaGraphLaunch(sg->exec, ctx->stream));
+  {
+    const int irc = issue_inputs(ctx);  // hx_step_host's slab copies, behind the launch
+    if (irc) return irc;
+  }
   ctx->early_done = false;
   if (ctx->early_xh && !ctx->peer && g_early == 1) {
     // hx_step_host: read x' and e' back while stage 2 still runs (the graph's external
@@ -2602,6 +2633,102 @@ extern "C" int hx_rk2_step(hx_ctx* ctx, const hx_params* prm, double t, double d
   return step_dispatch(ctx, prm, t, dt, x, v, e, x_out, v_out, e_out, info);
 }
 
+// hx_step_host's slab copies + flags on istream (once per call; a no-op when none are pending).
+// Called right after the step graph's launch, before a plain-launch step (which may sync the
+// stream mid-step), and on hx_step_host's way out (error paths), so every waiting rates launch
+// is always followed by its copies.
+typedef int (*StreamWrite64Fn)(cudaStream_t, unsigned long long, unsigned long long, unsigned);
+static StreamWrite64Fn g_write64 = nullptr;  // cuStreamWriteValue64 (driver entry point), or null
+
+static int issue_inputs(hx_ctx* ctx) {
+  if (!ctx->in_xh) return HX_OK;
+  const double *x_host = ctx->in_xh, *v_host = ctx->in_vh, *e_host = ctx->in_eh;
+  ctx->in_xh = ctx->in_vh = ctx->in_eh = nullptr;
+  long long n0 = 0, e0 = 0;
+  const int d = ctx->dim, nt = ctx->nt;
+  for (int s = 0; s < ctx->in_ns; ++s) {
+    const long long n1 = ctx->in_node_end[s], e1 = ctx->in_elem_end[s];
+    if (n1 > n0) {
+      CK(cudaMemcpyAsync(ctx->hx_x + n0 * d, x_host + n0 * d, sizeof(double) * (n1 - n0) * d,
+                         cudaMemcpyHostToDevice, ctx->istream));
+      CK(cudaMemcpyAsync(ctx->hx_v + n0 * d, v_host + n0 * d, sizeof(double) * (n1 - n0) * d,
+                         cudaMemcpyHostToDevice, ctx->istream));
+    }
+    if (e1 > e0)
+      CK(cudaMemcpyAsync(ctx->hx_e + e0 * nt, e_host + e0 * nt, sizeof(double) * (e1 - e0) * nt,
+                         cudaMemcpyHostToDevice, ctx->istream));
+    // the flag: a stream memory operation (front end, no DMA: a small H2D copy costs ~13 us)
+    if (g_write64) {
+      if (g_write64(ctx->istream, (unsigned long long)(uintptr_t)(ctx->in_flag + s), ctx->h_in[s], 0) != 0)
+        return fail(ctx, HX_ECUDA, "cuStreamWriteValue64 failed");
+    } else {
+      CK(cudaMemcpyAsync(ctx->in_flag + s, ctx->h_in + s, sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                         ctx->istream));
+    }
+    n0 = n1;
+    e0 = e1;
+  }
+  return HX_OK;
+}
+
+static int g_stream_in = -1;
+static constexpr int HX_MAX_SLABS = 64;
+
+// slab boundaries of the streamed inputs: slab s holds the elements of layers
+// [s*in_ez, (s+1)*in_ez) (e) and every node they touch (x, v: node layers up to P*(s+1)*in_ez),
+// each end rounded up to 16 nodes / 16 elements so that no 128-byte line of x, v or e spans two
+// slabs (16 * 24 B = 3 lines, 16 * nt * 8 B = nt lines)
+static int stream_in_setup(hx_ctx* ctx, int slabs) {
+  const int nz = ctx->bk.nz;
+  const int ez = std::max(1, (nz + std::min(slabs, nz) - 1) / std::min(slabs, nz));
+  const int ns = (nz + ez - 1) / ez;
+  if (!ctx->istream) CK(cudaStreamCreateWithFlags(&ctx->istream, cudaStreamNonBlocking));
+  static bool looked = false;
+  if (!looked) {
+    looked = true;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && !getenv("HX_STREAM_IN_MEMCPY"))
+      g_write64 = (StreamWrite64Fn)fn;
+    cudaGetLastError();
+  }
+  if (ctx->in_flag && ctx->in_ns == ns && ctx->in_ez == ez) return HX_OK;
+  if (ctx->in_flag) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(ctx->in_flag);
+    ctx->in_flag = nullptr;
+  }
+  if (!ctx->h_in) {
+    CK(cudaHostAlloc(&ctx->h_in, sizeof(unsigned long long) * (HX_MAX_SLABS + 1), cudaHostAllocMapped));
+    void* dp = nullptr;
+    CK(cudaHostGetDevicePointer(&dp, ctx->h_in, 0));
+    ctx->in_err_dev = (unsigned long long*)dp + HX_MAX_SLABS;
+  }
+  if (ns > HX_MAX_SLABS) return fail(ctx, HX_EINVAL, "streamed inputs: %d slabs > %d", ns, HX_MAX_SLABS);
+  CK(cudaMalloc(&ctx->in_flag, sizeof(unsigned long long) * (ns + 1)));
+  CK(cudaMemset(ctx->in_flag, 0, sizeof(unsigned long long) * (ns + 1)));
+  ctx->in_epoch = 0;
+  ctx->in_node_end.assign(ns, 0);
+  ctx->in_elem_end.assign(ns, 0);
+  const long long lay = (long long)ctx->bk.nx * ctx->bk.ny;
+  for (int s = 0; s < ns; ++s) {
+    const long long zend = std::min<long long>((long long)(s + 1) * ez, nz);
+    long long n1 = (zend * ctx->p + 1) * ctx->bk.NxNy, e1 = zend * lay;
+    n1 = (n1 + 15) / 16 * 16;
+    e1 = (e1 + 15) / 16 * 16;
+    ctx->in_node_end[s] = s == ns - 1 ? ctx->nn : std::min(n1, ctx->nn);
+    ctx->in_elem_end[s] = s == ns - 1 ? ctx->ne : std::min(e1, ctx->ne);
+  }
+  ctx->in_ez = ez;
+  ctx->in_ns = ns;
+  // graphs captured before the slabs existed launch the rates kernel without the wait
+  for (auto& g : ctx->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  ctx->graphs.clear();
+  return HX_OK;
+}
+
 extern "C" int hx_step_host(hx_ctx* ctx, const hx_params* prm, double t, double* x_host, double* v_host,
                             double* e_host, hx_step_info* info) {
   if (!ctx || !prm || !x_host || !v_host || !e_host) return HX_EINVAL;
@@ -2609,9 +2736,35 @@ extern "C" int hx_step_host(hx_ctx* ctx, const hx_params* prm, double t, double*
   const size_t nvb = sizeof(double) * ctx->nn * ctx->dim, neb = sizeof(double) * ctx->ne * ctx->nt;
   int src = ensure_stage(ctx);
   if (src) return src;
-  CK(cudaMemcpyAsync(ctx->hx_x, x_host, nvb, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->hx_v, v_host, nvb, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->hx_e, e_host, neb, cudaMemcpyHostToDevice, ctx->stream));
+  {
+    const char* se = getenv("HX_STREAM_IN");  // slabs of the streamed H2D (0: one up-front copy)
+    g_stream_in = se ? atoi(se) : 3;  // measured: 2-4 slabs best (per-slab DMA setup ~10 us)
+  }
+  if (g_rates_kernel < 0) {
+    const char* sr = getenv("HX_RATES");
+    g_rates_kernel = (sr && strcmp(sr, "cta") == 0) ? 0 : 1;
+  }
+  const bool streamed = g_stream_in > 0 && ctx->dim == 3 && ctx->p >= 2 && ctx->brick && !ctx->peer &&
+                        g_rates_kernel != 0 && ctx->bk.nz >= 2;
+  if (streamed) {
+    src = stream_in_setup(ctx, g_stream_in);
+    if (src) return src;
+    // required epoch first (stream-ordered before the step's first rates launch), then the
+    // slabs on the copy stream, each followed by its flag; the copies depend on nothing the
+    // step does, so the waiting rates kernel cannot block them
+    const unsigned long long ep = ++ctx->in_epoch;
+    for (int s = 0; s <= ctx->in_ns; ++s) ctx->h_in[s] = ep;
+    ctx->h_in[HX_MAX_SLABS] = 0;
+    CK(cudaMemcpyAsync(ctx->in_flag + ctx->in_ns, ctx->h_in + ctx->in_ns, sizeof(unsigned long long),
+                       cudaMemcpyHostToDevice, ctx->stream));
+    ctx->in_xh = x_host;  // enqueued right after the step's launch (issue_inputs): the host's
+    ctx->in_vh = v_host;  // enqueue time then overlaps the GPU instead of delaying the launch
+    ctx->in_eh = e_host;
+  } else {
+    CK(cudaMemcpyAsync(ctx->hx_x, x_host, nvb, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->hx_v, v_host, nvb, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->hx_e, e_host, neb, cudaMemcpyHostToDevice, ctx->stream));
+  }
   // x' and e' may be read back by the step itself while its stage 2 runs (step_dispatch)
   ctx->early_xh = x_host;
   ctx->early_eh = e_host;
@@ -2620,6 +2773,13 @@ extern "C" int hx_step_host(hx_ctx* ctx, const hx_params* prm, double t, double*
   hx_step_info local{};
   hx_step_info* inf = info ? info : &local;
   int rc = hx_step(ctx, prm, t, ctx->hx_x, ctx->hx_v, ctx->hx_e, ctx->hx_xo, ctx->hx_vo, ctx->hx_eo, inf);
+  {
+    const int irc = issue_inputs(ctx);  // (error paths that launched nothing: keep the flags whole)
+    if (streamed) CK(cudaStreamSynchronize(ctx->istream));
+    if (irc && !rc) rc = irc;
+    if (streamed && !rc && *(volatile unsigned long long*)(ctx->h_in + HX_MAX_SLABS))
+      rc = fail(ctx, HX_ECUDA, "hx_step_host: streamed input slab did not land within the wait bound");
+  }
   ctx->early_xh = ctx->early_eh = ctx->early_vh = nullptr;
   const bool early = ctx->early_done && inf->retries == 0;
   CK(cudaStreamSynchronize(ctx->cstream));

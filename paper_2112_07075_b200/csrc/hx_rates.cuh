@@ -98,7 +98,33 @@ struct RatesPCArgs {
   StatusDev* st;
   Brick b;
   int brick;
+  // hx_step_host streamed inputs (brick, MODE 0): inflag[0..in_ns) = epoch of each z-slab of
+  // x, v, e that has landed, inflag[in_ns] = the epoch this launch needs (stream-ordered);
+  // null when the inputs are resident
+  const unsigned long long* inflag;
+  unsigned long long* inerr;  // mapped host word: set on a wait that timed out (hx_step_host fails)
+  int in_ez, in_ns;
 };
+
+// streamed inputs: wait (thread 0, then the CTA) until the slab holding elements up to
+// `last` has landed.  Every 128-byte line of x, v, e lies in one slab (host-side rounding),
+// so no line read here can be cached from before its slab's copy.
+__device__ __forceinline__ void rates_wait_inputs(const RatesPCArgs& a, long long last) {
+  if (threadIdx.x == 0) {
+    const int ez = (int)a.b.fnxy.div((unsigned)last);
+    const int s = min(ez / a.in_ez, a.in_ns - 1);
+    const unsigned long long need = *(volatile const unsigned long long*)(a.inflag + a.in_ns);
+    unsigned long long spins = 0;
+    while (ld_acquire_sys(a.inflag + s) < need)
+      if (++spins > (1ull << 24)) {  // >= 1 s: the copy stream is stuck; report, do not hang
+        st_release_sys(a.inerr, 1ull);
+        break;
+      } else {
+        __nanosleep(64);
+      }
+  }
+  __syncthreads();
+}
 
 // reference "inverse" (cof/det = J^{-T} in 3D, fespace.py:280-302,338) with one reciprocal
 __device__ __forceinline__ double det_inv_fast(const double (&J)[3][3], double (&inv)[3][3]) {
@@ -206,6 +232,7 @@ __global__ void __launch_bounds__(RatesPC<P>::THREADS, P >= 4 ? 2 : RATES_PC_MIN
     if (f0 < a.ne) {
       const int fel = (int)((a.ne - f0) < EPC ? (a.ne - f0) : EPC);
       double* fb = smem + b * FS;
+      if (MODE == 0 && a.inflag) rates_wait_inputs(a, f0 + fel - 1);
       constexpr int ROW = 3 * D1;  // doubles per node row (D1 nodes x 3 comps, contiguous)
       long long nb[EPC];  // brick: the pass's element base nodes, once per pass (not per item)
       if (a.brick) {

@@ -84,3 +84,34 @@ def test_host_entry_failed_step_leaves_state():
                               arena[nx:nx + nv].data_ptr(), arena[nx + nv:].data_ptr(), C.byref(info))
         assert rc == _lib.HX_EUNDERFLOW
         assert torch.equal(arena, before)
+
+
+@pytest.mark.parametrize("slabs", ["0", "1", "3", "64"])
+def test_streamed_inputs_match_device_steps(slabs, monkeypatch):
+    """hx_step_host streams x, v, e in z-slabs while the stage-1 rates kernel runs (each pass
+    waits for its slab's flag): every slab count, including one slab per element layer and the
+    single up-front copy (0), gives states bit-identical to the device-resident step."""
+    from paper_2112_07075_b200 import _lib
+    from paper_2112_07075_b200.hydro import StepControls
+
+    monkeypatch.setenv("HX_STREAM_IN", slabs)
+    hy, st = _setup(n=7, p=3)
+    ctl = StepControls(cfl=0.02, dt_max=1.0, t_final=10.0)
+    arena, (nx, nv, ne) = _host_arena(st)
+    lib, h = hy._ctx.lib, hy._ctx.h
+    prm = hy._params(ctl)
+    info = _lib.StepInfo()
+    dev = hy.to_device(st)
+    t = st.t
+    for _ in range(4):
+        hy._ctx.sync_stream()
+        rc = lib.hx_step_host(h, C.byref(prm), float(t), arena[:nx].data_ptr(), arena[nx:nx + nv].data_ptr(),
+                              arena[nx + nv:].data_ptr(), C.byref(info))
+        assert rc == 0
+        t = info.t_new
+        dev, dinfo = hy.step(dev, ctl)
+        ref = hy.to_host(dev)
+        assert np.array_equal(arena[:nx].numpy(), ref.x.reshape(-1))
+        assert np.array_equal(arena[nx:nx + nv].numpy(), ref.v.reshape(-1))
+        assert np.array_equal(arena[nx + nv:].numpy(), ref.e.reshape(-1))
+        assert info.dt == dinfo["dt"]
