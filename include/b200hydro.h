@@ -247,7 +247,10 @@ int hx_step(hx_ctx* ctx, const hx_params* prm, double t, const double* x, const 
 int hx_rk2_step(hx_ctx* ctx, const hx_params* prm, double t, double dt, const double* x, const double* v,
                 const double* e, double* x_out, double* v_out, double* e_out, hx_step_info* info);
 /* Same step with HOST state buffers (pinned or pageable): H2D, step, D2H in one call
- * -- the end-to-end entry a host-side caller binds. In/out may alias. */
+ * -- the end-to-end entry a host-side caller binds. In/out may alias.  On a 3D brick the
+ * H2D is streamed in z-slabs behind the step's launch (HX_STREAM_IN slabs, default 3; 0 =
+ * one up-front copy) and overlaps the stage-1 rates kernel; x' and e' are read back while
+ * stage 2 runs.  Results are bit-identical to hx_step on the same state. */
 int hx_step_host(hx_ctx* ctx, const hx_params* prm, double t, double* x_host, double* v_host,
                  double* e_host, hx_step_info* info);
 /* kinetic_energy / internal_energy (hydro.py:409-420) with the phase mass. */

@@ -140,7 +140,7 @@ struct hx_ctx {
   unsigned long long* h_in = nullptr;     // pinned: the epoch values copied
   unsigned long long* in_err_dev = nullptr;  // device view of h_in[HX_MAX_SLABS] (mapped): wait timed out
   unsigned long long in_epoch = 0;
-  int in_ns = 0, in_ez = 0;               // slabs, element layers per slab
+  int in_ns = 0, in_ez = 0;               // slabs, layer-count key (-1: halving counts)
   std::vector<long long> in_node_end, in_elem_end;
   cudaStream_t istream = nullptr;        // the slab copies (own stream: independent of cstream's
                                         // read-backs, which wait on the step's events)
@@ -390,7 +390,6 @@ struct LaunchRates {
         if (mode == 0 && ctx->in_ns > 0 && x == ctx->hx_x && ctx->brick && !ctx->peer) {
           a.inflag = ctx->in_flag;  // hx_step_host's streamed inputs (a no-op wait otherwise)
           a.inerr = ctx->in_err_dev;
-          a.in_ez = ctx->in_ez;
           a.in_ns = ctx->in_ns;
         }
         // the lean validity kernel is measured faster for p <= 3 (p = 2: 44 vs 51 us,
@@ -2674,14 +2673,37 @@ static int issue_inputs(hx_ctx* ctx) {
 static int g_stream_in = -1;
 static constexpr int HX_MAX_SLABS = 64;
 
-// slab boundaries of the streamed inputs: slab s holds the elements of layers
-// [s*in_ez, (s+1)*in_ez) (e) and every node they touch (x, v: node layers up to P*(s+1)*in_ez),
-// each end rounded up to 16 nodes / 16 elements so that no 128-byte line of x, v or e spans two
-// slabs (16 * 24 B = 3 lines, 16 * nt * 8 B = nt lines)
+// slab boundaries of the streamed inputs: slab s holds the elements of element layers
+// [zend(s-1), zend(s)) (e) and every node they touch (x, v: node layers up to P*zend(s)), each
+// end rounded up to 16 nodes / 16 elements so that no 128-byte line of x, v or e spans two
+// slabs (16 * 24 B = 3 lines, 16 * nt * 8 B = nt lines).  Layer counts halve from slab to slab
+// (HX_STREAM_UNIFORM=1: equal): the rates kernel's work left after the last slab lands is
+// then small.  The device table zend[] sits behind the flags: in_flag[ns + 1 + s].
 static int stream_in_setup(hx_ctx* ctx, int slabs) {
   const int nz = ctx->bk.nz;
-  const int ez = std::max(1, (nz + std::min(slabs, nz) - 1) / std::min(slabs, nz));
-  const int ns = (nz + ez - 1) / ez;
+  const int ns = std::min(std::min(slabs, nz), HX_MAX_SLABS);
+  const char* su = getenv("HX_STREAM_UNIFORM");
+  const int geo = (su && su[0] == '1') ? 0 : 1;
+  std::vector<int> cnt(ns, 1);
+  {
+    double wsum = 0.0;
+    for (int q = 0; q < ns; ++q) wsum += geo ? std::ldexp(1.0, std::min(ns - 1 - q, 30)) : 1.0;
+    int tot = 0;
+    for (int q = 0; q < ns; ++q) {
+      const double w = geo ? std::ldexp(1.0, std::min(ns - 1 - q, 30)) : 1.0;
+      cnt[q] = std::max(1, (int)std::lround(nz * w / wsum));
+      tot += cnt[q];
+    }
+    while (tot > nz) {  // take back from the largest slab
+      int m = 0;
+      for (int q = 1; q < ns; ++q)
+        if (cnt[q] > cnt[m]) m = q;
+      --cnt[m];
+      --tot;
+    }
+    for (; tot < nz; ++tot) ++cnt[0];
+  }
+  const int ez = geo ? -1 : cnt[0];  // cache key (with ns)
   if (!ctx->istream) CK(cudaStreamCreateWithFlags(&ctx->istream, cudaStreamNonBlocking));
   static bool looked = false;
   if (!looked) {
@@ -2706,20 +2728,25 @@ static int stream_in_setup(hx_ctx* ctx, int slabs) {
     ctx->in_err_dev = (unsigned long long*)dp + HX_MAX_SLABS;
   }
   if (ns > HX_MAX_SLABS) return fail(ctx, HX_EINVAL, "streamed inputs: %d slabs > %d", ns, HX_MAX_SLABS);
-  CK(cudaMalloc(&ctx->in_flag, sizeof(unsigned long long) * (ns + 1)));
+  CK(cudaMalloc(&ctx->in_flag, sizeof(unsigned long long) * (2 * ns + 1)));
   CK(cudaMemset(ctx->in_flag, 0, sizeof(unsigned long long) * (ns + 1)));
   ctx->in_epoch = 0;
   ctx->in_node_end.assign(ns, 0);
   ctx->in_elem_end.assign(ns, 0);
   const long long lay = (long long)ctx->bk.nx * ctx->bk.ny;
+  std::vector<unsigned long long> zt(ns);
+  long long zacc = 0;
   for (int s = 0; s < ns; ++s) {
-    const long long zend = std::min<long long>((long long)(s + 1) * ez, nz);
+    zacc += cnt[s];
+    const long long zend = std::min<long long>(zacc, nz);
+    zt[s] = (unsigned long long)zend;
     long long n1 = (zend * ctx->p + 1) * ctx->bk.NxNy, e1 = zend * lay;
     n1 = (n1 + 15) / 16 * 16;
     e1 = (e1 + 15) / 16 * 16;
     ctx->in_node_end[s] = s == ns - 1 ? ctx->nn : std::min(n1, ctx->nn);
     ctx->in_elem_end[s] = s == ns - 1 ? ctx->ne : std::min(e1, ctx->ne);
   }
+  CK(cudaMemcpy(ctx->in_flag + ns + 1, zt.data(), sizeof(unsigned long long) * ns, cudaMemcpyHostToDevice));
   ctx->in_ez = ez;
   ctx->in_ns = ns;
   // graphs captured before the slabs existed launch the rates kernel without the wait

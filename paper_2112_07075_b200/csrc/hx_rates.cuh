@@ -103,7 +103,7 @@ struct RatesPCArgs {
   // null when the inputs are resident
   const unsigned long long* inflag;
   unsigned long long* inerr;  // mapped host word: set on a wait that timed out (hx_step_host fails)
-  int in_ez, in_ns;
+  int in_ns;  // slabs; inflag[in_ns + 1 + s] = end (exclusive) element layer of slab s
 };
 
 // streamed inputs: wait (thread 0, then the CTA) until the slab holding elements up to
@@ -112,7 +112,8 @@ struct RatesPCArgs {
 __device__ __forceinline__ void rates_wait_inputs(const RatesPCArgs& a, long long last) {
   if (threadIdx.x == 0) {
     const int ez = (int)a.b.fnxy.div((unsigned)last);
-    const int s = min(ez / a.in_ez, a.in_ns - 1);
+    int s = 0;
+    while (s < a.in_ns - 1 && (unsigned long long)ez >= __ldg(a.inflag + a.in_ns + 1 + s)) ++s;
     const unsigned long long need = *(volatile const unsigned long long*)(a.inflag + a.in_ns);
     unsigned long long spins = 0;
     while (ld_acquire_sys(a.inflag + s) < need)

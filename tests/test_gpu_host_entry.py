@@ -86,8 +86,8 @@ def test_host_entry_failed_step_leaves_state():
         assert torch.equal(arena, before)
 
 
-@pytest.mark.parametrize("slabs", ["0", "1", "3", "64"])
-def test_streamed_inputs_match_device_steps(slabs, monkeypatch):
+@pytest.mark.parametrize("slabs,pinned", [("0", True), ("1", True), ("3", True), ("64", True), ("3", False)])
+def test_streamed_inputs_match_device_steps(slabs, pinned, monkeypatch):
     """hx_step_host streams x, v, e in z-slabs while the stage-1 rates kernel runs (each pass
     waits for its slab's flag): every slab count, including one slab per element layer and the
     single up-front copy (0), gives states bit-identical to the device-resident step."""
@@ -98,6 +98,8 @@ def test_streamed_inputs_match_device_steps(slabs, monkeypatch):
     hy, st = _setup(n=7, p=3)
     ctl = StepControls(cfl=0.02, dt_max=1.0, t_final=10.0)
     arena, (nx, nv, ne) = _host_arena(st)
+    if not pinned:  # pageable host memory (staged copies)
+        arena = torch.from_numpy(arena.numpy().copy())
     lib, h = hy._ctx.lib, hy._ctx.h
     prm = hy._params(ctl)
     info = _lib.StepInfo()

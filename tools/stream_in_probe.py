@@ -55,11 +55,17 @@ def run(tag, steps=10):
         if k >= 3:
             ts.append(dt)
     print(f"{tag}: hx_step_host {np.median(ts) * 1e3:.3f} ms median, {np.mean(ts) * 1e3:.3f} mean", flush=True)
+    return float(np.median(ts))
 
 
-for s in os.environ.get("SLABS", "0 8 0 8 4 12 23").split():
-    os.environ["HX_STREAM_IN"] = s
-    run(f"slabs={s}")
+res = {}
+for rnd in range(int(os.environ.get("ROUNDS", "1"))):  # configurations interleaved per round
+    for s in os.environ.get("SLABS", "0 3 3u 4 4u 2 6").split():  # 'u': equal layer counts
+        os.environ["HX_STREAM_UNIFORM"] = "1" if s.endswith("u") else "0"
+        os.environ["HX_STREAM_IN"] = s.rstrip("u")
+        res.setdefault(s, []).append(run(f"slabs={s}"))
+for s, v in res.items():
+    print(f"summary slabs={s}: median over rounds {np.median(v) * 1e3:.3f} ms, min {min(v) * 1e3:.3f}", flush=True)
 # device-resident step
 dev = hy.to_device(st)
 for _ in range(3):
