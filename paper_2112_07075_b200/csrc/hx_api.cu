@@ -2318,6 +2318,20 @@ static bool same_params(const hx_params& a, const hx_params& b) { return memcmp(
 
 static int g_early = -1;  // HX_EARLY=0: the serial step graph (x', e', validity at the end)
 
+// end of a captured step: status / CG state / dt words into the pinned host copies
+struct StatusOut {
+  const unsigned long long* src[3];
+  unsigned long long* dst[3];
+  int n[3];
+};
+static_assert(sizeof(StatusDev) % 8 == 0 && sizeof(CGDev) % 8 == 0, "word copies");
+__global__ void k_status_out(StatusOut so) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    for (int i = threadIdx.x; i < so.n[r]; i += blockDim.x) so.dst[r][i] = __ldcg(so.src[r] + i);
+}
+static int g_status_kernel = -1;  // HX_STATUS_KERNEL=0: three D2H copy nodes instead
+
 static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, const double* x, const double* v,
                         const double* e, double* x_out, double* v_out, double* e_out, cudaGraphExec_t* exec,
                         hx_ctx::GProf* gprof = nullptr) {
@@ -2403,9 +2417,26 @@ static int capture_step(hx_ctx* ctx, const hx_params* prm, double dt_fixed, cons
     // validity of the new geometry
     r = validity_launch(ctx, x_out, ctx->st + 2);
     if (r) return r;
-    CK(cudaMemcpyAsync(ctx->h_st, ctx->st, 3 * sizeof(StatusDev), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->h_cg, ctx->cg, 2 * sizeof(CGDev), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->h_dt, ctx->dt, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (g_status_kernel < 0) {
+      const char* sk = getenv("HX_STATUS_KERNEL");
+      g_status_kernel = (sk && sk[0] == '0') ? 0 : 1;
+    }
+    if (g_status_kernel) {
+      // one kernel node writes the step's status, CG states and dt straight into the pinned
+      // (UVA-mapped) host copies instead of three small D2H copy nodes
+      StatusOut so{{reinterpret_cast<const unsigned long long*>(ctx->st),
+                    reinterpret_cast<const unsigned long long*>(ctx->cg),
+                    reinterpret_cast<const unsigned long long*>(ctx->dt)},
+                   {reinterpret_cast<unsigned long long*>(ctx->h_st), reinterpret_cast<unsigned long long*>(ctx->h_cg),
+                    reinterpret_cast<unsigned long long*>(ctx->h_dt)},
+                   {(int)(3 * sizeof(StatusDev) / 8), (int)(2 * sizeof(CGDev) / 8), 2}};
+      k_status_out<<<1, 128, 0, ctx->stream>>>(so);
+      CKL();
+    } else {
+      CK(cudaMemcpyAsync(ctx->h_st, ctx->st, 3 * sizeof(StatusDev), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->h_cg, ctx->cg, 2 * sizeof(CGDev), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->h_dt, ctx->dt, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    }
     r = peer_err_fetch(ctx);
     if (r) return r;
     CK(cudaStreamEndCapture(ctx->stream, &graph));
