@@ -2579,7 +2579,7 @@ static int step_dispatch(hx_ctx* ctx, const hx_params* prm, double t, double dt_
   }
   const StatusDev s0 = ctx->h_st[0], s1 = ctx->h_st[1], s2 = ctx->h_st[2];
   const CGDev c0 = ctx->h_cg[0], c1 = ctx->h_cg[1];
-  ctx->launches += 11 + 2 * (long long)(c0.iters + c1.iters);
+  ctx->launches += 11 + (g_status_kernel > 0 ? 1 : 0) + 2 * (long long)(c0.iters + c1.iters);
   if (dup >= 0 && sg->gprof) {
     const int it[2] = {c0.iters, c1.iters};
     gprof_collect(ctx, sg->gprof.get(), it);
